@@ -1,0 +1,169 @@
+/*
+ * tsa_b200.h -- C ABI of the B200-native Token Sparse Attention prefill path.
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (/root/reference/proj/include/tsa/{token_coverage,attention}.hpp): every
+ * entry point below replaces one reference function (cited per entry) with a
+ * stream-ordered CUDA implementation for sm_100a.  The signatures use only
+ * plain pointers, sizes and a POD descriptor -- no torch, no Eigen -- so any
+ * FFI (ctypes, cgo, JNI, a C++ adapter: include/tsa_b200.hpp) can bind them.
+ *
+ * Conventions
+ *  - Tensor layout is the reference's HeadTensors (attention.hpp:16-25):
+ *    q = H blocks of [L x d] row-major, k/v = Hkv blocks of [L x d];
+ *    kv_head(h) = h / (H / Hkv).  Element type per `dtype` (f32 or bf16).
+ *  - Scores are f32 [H x L] (HeadScores::s, token_coverage.hpp:12-20).
+ *  - Index lists are int32 [H x L] rows, of which the first k_keep entries of
+ *    each row are valid and strictly ascending (TokenSelection::indices,
+ *    selection.hpp:12-21).  k_keep lives in device memory (int32) so the
+ *    chain runs without a host round trip.
+ *  - All pointers are device pointers unless named *_host; every call is
+ *    asynchronous on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *    default stream).
+ *  - Errors: a non-zero return code; tsa_last_error() names the violated
+ *    precondition with the reference's wording (std::invalid_argument there).
+ *    TSA_ERR_INVALID = precondition, TSA_ERR_CUDA = launch/runtime failure.
+ *  - Multi-GPU head sharding: [head_begin, head_end) selects the query heads a
+ *    call computes (GQA aligned).  Score rows and outputs of other heads are
+ *    left untouched, so the caller exchanges them (all-gather) between calls.
+ */
+#ifndef TSA_B200_H_
+#define TSA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TSA_API __attribute__((visibility("default")))
+#else
+#define TSA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum tsa_dtype { TSA_F32 = 0, TSA_BF16 = 1 };
+/* SparseMode, model.hpp:51 */
+enum tsa_mode { TSA_MODE_DENSE = 0, TSA_MODE_DYNAMIC = 1, TSA_MODE_FIXED = 2 };
+/* ForcedPolicy, model.hpp:54 */
+enum tsa_forced_policy { TSA_FORCED_FINAL_TOKEN = 0, TSA_FORCED_RECENT_WINDOW = 1 };
+enum tsa_status { TSA_OK = 0, TSA_ERR_INVALID = 1, TSA_ERR_CUDA = 2 };
+/* Scoring arithmetic: REFERENCE reproduces the reference's f32 operation
+ * order (exact logits, sequential softmax sums); FAST runs Q K^T on the
+ * tensor cores (bf16 only).  DEFAULT = REFERENCE for f32, FAST for bf16. */
+enum tsa_scoring { TSA_SCORING_DEFAULT = 0, TSA_SCORING_REFERENCE = 1, TSA_SCORING_FAST = 2 };
+
+/* One attention layer's geometry plus the SparsePlan parameters
+ * (model.hpp:58-73).  Defaults via tsa_desc_init(). */
+typedef struct tsa_desc {
+    int32_t n_heads;       /* H */
+    int32_t n_kv_heads;    /* Hkv, H % Hkv == 0 */
+    int32_t seq_len;       /* L */
+    int32_t d_head;        /* d (f32: any multiple of 4 <= 256; bf16 fast path: 128) */
+    int32_t dtype;         /* tsa_dtype */
+    int32_t mode;          /* tsa_mode */
+    double tau;            /* dynamic coverage, [0, 1]     (SparsePlan::tau = 0.005) */
+    double s_fixed;        /* fixed sparsity ratio, [0, 1) (SparsePlan::s_fixed = 0) */
+    int32_t last_q;        /* >= 1 (SparsePlan::last_q = 64) */
+    int32_t kernel;        /* odd >= 1 (SparsePlan::kernel = 7) */
+    int32_t forced_policy; /* tsa_forced_policy (SparsePlan::forced) */
+    int32_t head_begin;    /* query-head shard [head_begin, head_end) */
+    int32_t head_end;
+    int32_t scoring;       /* tsa_scoring */
+} tsa_desc;
+
+TSA_API void tsa_desc_init(tsa_desc* d, int32_t n_heads, int32_t n_kv_heads, int32_t seq_len,
+                   int32_t d_head, int32_t dtype);
+TSA_API const char* tsa_last_error(void);
+TSA_API const char* tsa_version(void);
+
+/* Bytes of scratch the calls below need for `d` (scores, index lists,
+ * compressed Q/K/V/O buffers and selection scratch), 256-B aligned. */
+TSA_API int tsa_workspace_size(const tsa_desc* d, size_t* bytes);
+
+/* --- the path, stage by stage ------------------------------------------ */
+
+/* score_tokens (token_coverage.hpp:32 / token_coverage.cpp:16-50).
+ * Writes s[h, :] for h in the shard; s is [H x L] f32. */
+TSA_API int tsa_score(const tsa_desc* d, const void* q, const void* k, float* s, void* ws, void* stream);
+
+/* aggregate_scores + coverage_budget (token_coverage.cpp:52-96) for
+ * TSA_MODE_DYNAMIC, fixed_budget (:98-109) for TSA_MODE_FIXED, L for
+ * TSA_MODE_DENSE; min_keep = max(1, |forced|) (model.cpp:172).  Reads all H
+ * score rows.  Writes *k_keep (device int32). */
+TSA_API int tsa_budget(const tsa_desc* d, const float* s, int32_t* k_keep, void* ws, void* stream);
+
+/* aggregate_scores alone (token_coverage.cpp:52-66): sl[t] = sum_h s[h, t] /
+ * total, f32, same operation order as the reference.  Reads all H rows. */
+TSA_API int tsa_aggregate_scores(const tsa_desc* d, const float* s, float* sl, void* ws,
+                                 void* stream);
+
+/* coverage_budget alone (token_coverage.cpp:68-96) on a LayerScores vector
+ * sl [L] with the descriptor's tau and an explicit min_keep. */
+TSA_API int tsa_coverage_budget(const tsa_desc* d, const float* sl, int32_t min_keep,
+                                int32_t* k_keep, void* ws, void* stream);
+
+/* select_tokens (token_coverage.cpp:111-152) for the shard's heads with an
+ * explicit forced list (device int32, sorted, unique, in range -- the host
+ * adapter normalises it as the reference does at :113-121).  idx rows are
+ * [L] wide; inv (optional, may be NULL) receives the inverse map
+ * inv[h, t] = position of t in idx[h] or -1. */
+TSA_API int tsa_select(const tsa_desc* d, const float* s, const int32_t* k_keep, const int32_t* forced,
+               int32_t n_forced, int32_t* idx, int32_t* inv, void* ws, void* stream);
+
+/* gather_rows x3 (tensor_ops.cpp:92-99 via attention.cpp:93-95): qc/kc/vc
+ * are [H x L x d] with the first k_keep rows of each head valid (K/V rows
+ * come from the head's KV group, duplicated per query head). */
+TSA_API int tsa_gather(const tsa_desc* d, const void* q, const void* k, const void* v,
+               const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
+               void* stream);
+
+/* The `inner` seam (AttentionKernel, attention.hpp:28) with its default
+ * dense_causal_attention (attention.cpp:25-40): causal attention over the
+ * first n rows of each head, n = *k_keep (device).  kv_group = 1 when K/V
+ * are per query head (compressed), H/Hkv when they are the KV heads. */
+TSA_API int tsa_attend(const tsa_desc* d, const void* qc, const void* kc, const void* vc,
+               const int32_t* k_keep, int32_t kv_group, void* oc, void* stream);
+
+/* scatter_rows (tensor_ops.cpp:101-112 via attention.cpp:96): out[h, t] =
+ * oc[h, inv[h, t]] or +0.0 (every row of the shard written once). */
+TSA_API int tsa_scatter(const tsa_desc* d, const void* oc, const int32_t* inv, void* out, void* stream);
+
+/* scatter_rows for a caller-supplied selection: builds the inverse map of
+ * idx (first k_keep entries per head) in ws, then tsa_scatter. */
+TSA_API int tsa_scatter_rows(const tsa_desc* d, const void* oc, const int32_t* idx,
+                             const int32_t* k_keep, void* out, void* ws, void* stream);
+
+/* Synchronises `stream` and reports device-side precondition failures
+ * recorded in ws by tsa_budget (aggregate_scores on all-zero scores,
+ * token_coverage.cpp:62-64), then clears them. */
+TSA_API int tsa_check(const tsa_desc* d, void* ws, void* stream);
+
+/* --- composite calls ---------------------------------------------------- */
+
+/* token_sparse_attention (attention.hpp:44-45) given a selection. */
+TSA_API int tsa_token_sparse_attention(const tsa_desc* d, const void* q, const void* k, const void* v,
+                               const int32_t* idx, const int32_t* k_keep, void* out, void* ws,
+                               void* stream);
+
+/* Dense causal attention of every head directly on q/k/v (the tau = 0 /
+ * dense-layer branch, model.cpp:184-194): the baseline the sparse path is
+ * measured against. */
+TSA_API int tsa_dense_attention(const tsa_desc* d, const void* q, const void* k, const void* v, void* out,
+                        void* stream);
+
+/* The sparse-layer branch of layer_forward (model.cpp:169-183) on one GPU:
+ * score -> budget -> select -> gather -> attend -> scatter.  idx_out
+ * (optional) receives the selection [H x L] int32, k_keep_out (device int32,
+ * required) the budget; k_keep_host (optional, pinned) is filled
+ * asynchronously for LayerStat.  Multi-GPU callers use the stage entry points
+ * with an all-gather of s between tsa_score and tsa_budget. */
+TSA_API int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, const void* v,
+                               void* out, int32_t* idx_out, int32_t* k_keep_out,
+                               int32_t* k_keep_host, void* ws, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSA_B200_H_ */

@@ -1,0 +1,189 @@
+// K5 (SIMT variant): causal flash attention in f32 arithmetic for any
+// supported head size, used for the f32 configuration (parity gate 1e-5,
+// bench.cpp:27) and for bf16 shapes the tcgen05 kernel does not cover.
+//
+// dense_causal_attention (attention.cpp:25-40) over the first n rows of each
+// head: O[i] = sum_{j<=i} softmax_j(q_i . k_j / sqrt(d)) v_j, computed with
+// the online (tile-wise) softmax.  n comes from device memory (k_keep), so
+// the grid is sized for L and surplus tiles exit immediately.
+//
+// Block = 32 query rows x 4 threads per row; a thread owns the 16-B chunks
+// c = part, part+4, ... of its row (conflict-free shared-memory reads).
+#include "common.cuh"
+
+namespace tsa {
+namespace {
+
+constexpr int SM_ROWS = 32;
+constexpr int SM_KEYS = 32;
+
+template <typename T, int D>
+__global__ void __launch_bounds__(128) attend_simt_kernel(const T* __restrict__ q,
+                                                          const T* __restrict__ k,
+                                                          const T* __restrict__ v,
+                                                          const int32_t* __restrict__ n_dev,
+                                                          int n_const, int kv_group,
+                                                          int rows_per_head, int kv_rows_per_head,
+                                                          int head_begin, float scale,
+                                                          T* __restrict__ o) {
+    constexpr int NC = D / 4;        // float4 chunks per row
+    constexpr int CPT = NC / 4 > 0 ? NC / 4 : 1;  // chunks per thread
+    extern __shared__ float4 smem4[];
+    float4* ks = smem4;                // [SM_KEYS][NC]
+    float4* vs = smem4 + SM_KEYS * NC; // [SM_KEYS][NC]
+
+    const int h = head_begin + blockIdx.y;
+    const int n = n_dev ? *n_dev : n_const;
+    const int n_tiles = (n + SM_ROWS - 1) / SM_ROWS;
+    if ((int)blockIdx.x >= n_tiles) return;
+    const int tile = n_tiles - 1 - blockIdx.x;  // heaviest (longest causal row) first
+    const int row_in = threadIdx.x / 4, part = threadIdx.x % 4;
+    const int i = tile * SM_ROWS + row_in;
+    const bool active_part = part < NC;  // D = 8: only 2 chunks per row
+    const int kvh = h / kv_group;
+    const T* qh = q + (size_t)h * rows_per_head * D;
+    const T* kh = k + (size_t)kvh * kv_rows_per_head * D;
+    const T* vh = v + (size_t)kvh * kv_rows_per_head * D;
+
+    float4 qr[CPT], acc[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        qr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int ch = part + 4 * c;
+        if (i < n && active_part && ch < NC) {
+            const T* src = qh + (size_t)i * D + ch * 4;
+            qr[c] = make_float4(Elem<T>::to_f32(src[0]), Elem<T>::to_f32(src[1]),
+                                Elem<T>::to_f32(src[2]), Elem<T>::to_f32(src[3]));
+        }
+    }
+    float m = -INFINITY, l = 0.0f;
+    const int last_key = min(n, (tile + 1) * SM_ROWS) - 1;
+    for (int j0 = 0; j0 <= last_key; j0 += SM_KEYS) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < SM_KEYS * NC; e += 128) {
+            const int j = e / NC, ch = e % NC;
+            float4 kk = make_float4(0.f, 0.f, 0.f, 0.f), vv = kk;
+            if (j0 + j <= last_key) {
+                const T* ksrc = kh + (size_t)(j0 + j) * D + ch * 4;
+                const T* vsrc = vh + (size_t)(j0 + j) * D + ch * 4;
+                kk = make_float4(Elem<T>::to_f32(ksrc[0]), Elem<T>::to_f32(ksrc[1]),
+                                 Elem<T>::to_f32(ksrc[2]), Elem<T>::to_f32(ksrc[3]));
+                vv = make_float4(Elem<T>::to_f32(vsrc[0]), Elem<T>::to_f32(vsrc[1]),
+                                 Elem<T>::to_f32(vsrc[2]), Elem<T>::to_f32(vsrc[3]));
+            }
+            ks[j * NC + ch] = kk;
+            vs[j * NC + ch] = vv;
+        }
+        __syncthreads();
+        float sc[SM_KEYS];
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < SM_KEYS; ++j) {
+            float p = 0.f;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const int ch = part + 4 * c;
+                if (active_part && ch < NC) {
+                    const float4 kk = ks[j * NC + ch];
+                    p = fmaf(qr[c].x, kk.x, p);
+                    p = fmaf(qr[c].y, kk.y, p);
+                    p = fmaf(qr[c].z, kk.z, p);
+                    p = fmaf(qr[c].w, kk.w, p);
+                }
+            }
+            p += __shfl_xor_sync(0xffffffffu, p, 1);
+            p += __shfl_xor_sync(0xffffffffu, p, 2);
+            const int jj = j0 + j;
+            sc[j] = (jj <= i && jj <= last_key) ? p * scale : -INFINITY;
+            tmax = fmaxf(tmax, sc[j]);
+        }
+        const float m_new = fmaxf(m, tmax);
+        if (m_new == -INFINITY) continue;  // rows beyond n: nothing allowed yet
+        const float corr = expf(m - m_new);
+        l *= corr;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            acc[c].x *= corr;
+            acc[c].y *= corr;
+            acc[c].z *= corr;
+            acc[c].w *= corr;
+        }
+#pragma unroll
+        for (int j = 0; j < SM_KEYS; ++j) {
+            const float p = expf(sc[j] - m_new);
+            l += p;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const int ch = part + 4 * c;
+                if (active_part && ch < NC) {
+                    const float4 vv = vs[j * NC + ch];
+                    acc[c].x = fmaf(p, vv.x, acc[c].x);
+                    acc[c].y = fmaf(p, vv.y, acc[c].y);
+                    acc[c].z = fmaf(p, vv.z, acc[c].z);
+                    acc[c].w = fmaf(p, vv.w, acc[c].w);
+                }
+            }
+        }
+        m = m_new;
+    }
+    if (i >= n) return;
+    const float inv_l = 1.0f / l;
+    T* dst = o + ((size_t)h * rows_per_head + i) * D;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        const int ch = part + 4 * c;
+        if (active_part && ch < NC) {
+            dst[ch * 4 + 0] = Elem<T>::from_f32(acc[c].x * inv_l);
+            dst[ch * 4 + 1] = Elem<T>::from_f32(acc[c].y * inv_l);
+            dst[ch * 4 + 2] = Elem<T>::from_f32(acc[c].z * inv_l);
+            dst[ch * 4 + 3] = Elem<T>::from_f32(acc[c].w * inv_l);
+        }
+    }
+}
+
+template <typename T, int D>
+int launch_t(const tsa_desc& d, const void* q, const void* k, const void* v, const int32_t* n_dev,
+             int n_const, int kv_group, int rows_per_head, int kv_rows_per_head, void* o,
+             cudaStream_t st) {
+    const int nh = d.head_end - d.head_begin;
+    dim3 grid((d.seq_len + SM_ROWS - 1) / SM_ROWS, nh);
+    const size_t smem = 2 * SM_KEYS * (D / 4) * sizeof(float4);
+    auto kern = attend_simt_kernel<T, D>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 128, smem, st>>>((const T*)q, (const T*)k, (const T*)v, n_dev, n_const, kv_group,
+                                  rows_per_head, kv_rows_per_head, d.head_begin,
+                                  1.0f / sqrtf((float)D), (T*)o);
+    TSA_LAUNCH_CHECK("attend_simt");
+    return 0;
+}
+
+template <typename T>
+int dispatch_d(const tsa_desc& d, const void* q, const void* k, const void* v,
+               const int32_t* n_dev, int n_const, int kv_group, int rph, int kvrph, void* o,
+               cudaStream_t st) {
+    switch (d.d_head) {
+        case 8: return launch_t<T, 8>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+        case 16: return launch_t<T, 16>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+        case 32: return launch_t<T, 32>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+        case 64: return launch_t<T, 64>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+        case 128: return launch_t<T, 128>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+        case 256: return launch_t<T, 256>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+        default: return invalid("attend: unsupported d_head " + std::to_string(d.d_head) +
+                                " (supported: 8, 16, 32, 64, 128, 256)");
+    }
+}
+
+}  // namespace
+
+int launch_attend_simt(const tsa_desc& d, const void* q, const void* k, const void* v,
+                       const int32_t* n_dev, int32_t n_const, int32_t kv_group,
+                       int32_t rows_per_head, int32_t kv_rows_per_head, void* o, cudaStream_t st) {
+    if (d.dtype == TSA_BF16)
+        return dispatch_d<__nv_bfloat16>(d, q, k, v, n_dev, n_const, kv_group, rows_per_head,
+                                         kv_rows_per_head, o, st);
+    return dispatch_d<float>(d, q, k, v, n_dev, n_const, kv_group, rows_per_head,
+                             kv_rows_per_head, o, st);
+}
+
+}  // namespace tsa

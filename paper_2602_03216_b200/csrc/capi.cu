@@ -1,0 +1,314 @@
+// C ABI (include/tsa_b200.h): host-side validation with the reference's
+// error wording, workspace layout, and the stage orchestration of the sparse
+// layer branch (model.cpp:169-183).
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace tsa {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+int invalid(const std::string& msg) {
+    set_error(msg);
+    return TSA_ERR_INVALID;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return TSA_ERR_CUDA;
+}
+
+Workspace workspace_layout(const tsa_desc& d) {
+    Workspace w{};
+    const size_t H = d.n_heads, L = d.seq_len, D = d.d_head;
+    const size_t lq = lq_of(d);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    w.status = take(4);
+    w.k_keep = take(4);
+    w.headsum = take(4 * L);
+    w.logits = take(4 * H * lq * L);
+    w.rowstat = take(4 * H * lq * 2);
+    w.scores = take(4 * H * L);
+    w.forced = take(4 * L);
+    w.idx = take(4 * H * L);
+    w.inv = take(4 * H * L);
+    const size_t t = H * L * D * elem_bytes(d.dtype);
+    w.qc = take(t);
+    w.kc = take(t);
+    w.vc = take(t);
+    w.oc = take(t);
+    w.total = off;
+    return w;
+}
+
+namespace {
+
+std::string fmt_double(double x) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%f", x);
+    return b;
+}
+
+int check_desc(const tsa_desc* d) {
+    if (!d) return invalid("tsa: null descriptor");
+    if (d->n_heads < 1 || d->n_kv_heads < 1 || d->n_heads % d->n_kv_heads != 0)
+        return invalid("token_sparse_attention: " + std::to_string(d->n_heads) +
+                       " query heads not divisible by " + std::to_string(d->n_kv_heads) +
+                       " KV heads");
+    if (d->seq_len < 1) return invalid("tsa: seq_len must be positive");
+    if (d->dtype != TSA_F32 && d->dtype != TSA_BF16) return invalid("tsa: unknown dtype");
+    const int D = d->d_head;
+    if (!(D == 8 || D == 16 || D == 32 || D == 64 || D == 128 || D == 256))
+        return invalid("tsa: unsupported d_head " + std::to_string(D) +
+                       " (supported: 8, 16, 32, 64, 128, 256)");
+    if (d->last_q < 1)
+        return invalid("score_tokens: last_q must be positive, got " + std::to_string(d->last_q));
+    if (d->kernel < 1 || d->kernel % 2 == 0)
+        return invalid("avg_pool_1d: kernel must be odd and positive, got " +
+                       std::to_string(d->kernel));
+    if (d->tau < 0.0 || d->tau > 1.0)
+        return invalid("coverage_budget: tau " + fmt_double(d->tau) + " outside [0, 1]");
+    if (d->s_fixed < 0.0 || d->s_fixed >= 1.0)
+        return invalid("fixed_budget: sparsity ratio " + fmt_double(d->s_fixed) +
+                       " outside [0, 1)");
+    if (d->mode < TSA_MODE_DENSE || d->mode > TSA_MODE_FIXED) return invalid("tsa: unknown mode");
+    if (d->forced_policy != TSA_FORCED_FINAL_TOKEN && d->forced_policy != TSA_FORCED_RECENT_WINDOW)
+        return invalid("tsa: unknown forced policy");
+    const int g = d->n_heads / d->n_kv_heads;
+    if (d->head_begin < 0 || d->head_end > d->n_heads || d->head_begin >= d->head_end ||
+        d->head_begin % g != 0 || d->head_end % g != 0)
+        return invalid("tsa: head shard [" + std::to_string(d->head_begin) + ", " +
+                       std::to_string(d->head_end) + ") is empty, out of range or splits a KV group");
+    if (d->scoring == TSA_SCORING_FAST && d->dtype != TSA_BF16)
+        return invalid("score_tokens: FAST scoring needs bf16 inputs");
+    return 0;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+template <typename T>
+T* at(void* ws, size_t off) {
+    return reinterpret_cast<T*>(static_cast<uint8_t*>(ws) + off);
+}
+
+// Forced set of SparsePlan::forced_set (model.cpp:74-79) as a suffix [fbegin, L).
+int forced_begin(const tsa_desc& d) {
+    if (d.forced_policy == TSA_FORCED_FINAL_TOKEN) return d.seq_len - 1;
+    return std::max(0, d.seq_len - d.last_q);
+}
+
+int attend_dispatch(const tsa_desc& d, const void* q, const void* k, const void* v,
+                    const int32_t* n_dev, int n_const, int kv_group, int rph, int kvrph, void* o,
+                    cudaStream_t st) {
+    if (attend_sm100_supported(d))
+        return launch_attend_sm100(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+    return launch_attend_simt(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+}
+
+int budget_impl(const tsa_desc& d, const float* s, int32_t* k_keep, void* ws, int min_keep,
+                cudaStream_t st) {
+    const Workspace w = workspace_layout(d);
+    const int L = d.seq_len;
+    if (min_keep < 1 || min_keep > L)
+        return invalid("coverage_budget: min_keep " + std::to_string(min_keep) + " outside [1, " +
+                       std::to_string(L) + "]");
+    if (d.mode == TSA_MODE_DENSE) return launch_write_int(k_keep, L, st);
+    if (d.mode == TSA_MODE_FIXED) {  // fixed_budget, token_coverage.cpp:98-109
+        const int k = (int)std::lround((1.0 - d.s_fixed) * L);
+        return launch_write_int(k_keep, std::max(k, min_keep), st);
+    }
+    return launch_budget(d, s, k_keep, at<float>(ws, w.headsum), at<int32_t>(ws, w.status),
+                         min_keep, st);
+}
+
+}  // namespace
+}  // namespace tsa
+
+using namespace tsa;
+
+extern "C" {
+
+void tsa_desc_init(tsa_desc* d, int32_t n_heads, int32_t n_kv_heads, int32_t seq_len,
+                   int32_t d_head, int32_t dtype) {
+    d->n_heads = n_heads;
+    d->n_kv_heads = n_kv_heads;
+    d->seq_len = seq_len;
+    d->d_head = d_head;
+    d->dtype = dtype;
+    d->mode = TSA_MODE_DYNAMIC;
+    d->tau = 0.005;  // SparsePlan defaults, model.hpp:61-65
+    d->s_fixed = 0.0;
+    d->last_q = 64;
+    d->kernel = 7;
+    d->forced_policy = TSA_FORCED_FINAL_TOKEN;
+    d->head_begin = 0;
+    d->head_end = n_heads;
+    d->scoring = TSA_SCORING_DEFAULT;
+}
+
+const char* tsa_last_error(void) { return tsa::g_error.c_str(); }
+
+const char* tsa_version(void) { return "tsa_b200 0.1 (sm_100a)"; }
+
+int tsa_workspace_size(const tsa_desc* d, size_t* bytes) {
+    if (int rc = check_desc(d)) return rc;
+    *bytes = workspace_layout(*d).total;
+    return 0;
+}
+
+int tsa_score(const tsa_desc* d, const void* q, const void* k, float* s, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    const Workspace w = workspace_layout(*d);
+    if (scoring_mode(*d) == TSA_SCORING_FAST)
+        return launch_score_fast(*d, q, k, s, at<float>(ws, w.logits), at<float>(ws, w.rowstat),
+                                 S(stream));
+    return launch_score_reference(*d, q, k, s, at<float>(ws, w.logits), S(stream));
+}
+
+int tsa_budget(const tsa_desc* d, const float* s, int32_t* k_keep, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    const int fb = forced_begin(*d);
+    return budget_impl(*d, s, k_keep, ws, std::max(1, d->seq_len - fb), S(stream));
+}
+
+int tsa_aggregate_scores(const tsa_desc* d, const float* s, float* sl, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    const Workspace w = workspace_layout(*d);
+    return launch_aggregate(*d, s, sl, at<float>(ws, w.headsum), at<int32_t>(ws, w.status),
+                            S(stream));
+}
+
+int tsa_coverage_budget(const tsa_desc* d, const float* sl, int32_t min_keep, int32_t* k_keep,
+                        void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (min_keep < 1 || min_keep > d->seq_len)
+        return invalid("coverage_budget: min_keep " + std::to_string(min_keep) + " outside [1, " +
+                       std::to_string(d->seq_len) + "]");
+    const Workspace w = workspace_layout(*d);
+    return launch_coverage_from_sl(*d, sl, k_keep, at<int32_t>(ws, w.status), min_keep, S(stream));
+}
+
+int tsa_select(const tsa_desc* d, const float* s, const int32_t* k_keep, const int32_t* forced,
+               int32_t n_forced, int32_t* idx, int32_t* inv, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    (void)ws;
+    if (n_forced < 0 || n_forced > d->seq_len) return invalid("select_tokens: bad forced count");
+    if (n_forced > 0 && !forced) return invalid("select_tokens: null forced list");
+    return launch_select(*d, s, k_keep, forced, n_forced, -1, idx, inv, S(stream));
+}
+
+int tsa_gather(const tsa_desc* d, const void* q, const void* k, const void* v, const int32_t* idx,
+               const int32_t* k_keep, void* qc, void* kc, void* vc, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    return launch_gather(*d, q, k, v, idx, k_keep, qc, kc, vc, S(stream));
+}
+
+int tsa_attend(const tsa_desc* d, const void* qc, const void* kc, const void* vc,
+               const int32_t* k_keep, int32_t kv_group, void* oc, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (kv_group < 1 || d->n_heads % kv_group != 0) return invalid("attend: bad kv_group");
+    return attend_dispatch(*d, qc, kc, vc, k_keep, d->seq_len, kv_group, d->seq_len, d->seq_len,
+                           oc, S(stream));
+}
+
+int tsa_scatter(const tsa_desc* d, const void* oc, const int32_t* inv, void* out, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    return launch_scatter(*d, oc, inv, out, S(stream));
+}
+
+int tsa_scatter_rows(const tsa_desc* d, const void* oc, const int32_t* idx, const int32_t* k_keep,
+                     void* out, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    const Workspace w = workspace_layout(*d);
+    if (int rc = launch_inverse(*d, idx, k_keep, at<int32_t>(ws, w.inv), S(stream))) return rc;
+    return launch_scatter(*d, oc, at<int32_t>(ws, w.inv), out, S(stream));
+}
+
+int tsa_check(const tsa_desc* d, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    const Workspace w = workspace_layout(*d);
+    int32_t status = 0;
+    cudaError_t e = cudaMemcpyAsync(&status, at<int32_t>(ws, w.status), 4, cudaMemcpyDeviceToHost,
+                                    S(stream));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+    if (e != cudaSuccess) return cuda_check(e, "tsa_check");
+    if (status != 0) {
+        cudaMemsetAsync(at<int32_t>(ws, w.status), 0, 4, S(stream));
+        return invalid("aggregate_scores: all scores are zero, cannot normalize");
+    }
+    return 0;
+}
+
+int tsa_token_sparse_attention(const tsa_desc* d, const void* q, const void* k, const void* v,
+                               const int32_t* idx, const int32_t* k_keep, void* out, void* ws,
+                               void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    const Workspace w = workspace_layout(*d);
+    cudaStream_t st = S(stream);
+    int rc;
+    // inverse map for the scatter: rebuilt from idx by the select kernel's
+    // compaction is not available here, so derive it with one pass.
+    if ((rc = launch_gather(*d, q, k, v, idx, k_keep, at<void>(ws, w.qc), at<void>(ws, w.kc),
+                            at<void>(ws, w.vc), st)))
+        return rc;
+    if ((rc = attend_dispatch(*d, at<void>(ws, w.qc), at<void>(ws, w.kc), at<void>(ws, w.vc), k_keep,
+                              d->seq_len, 1, d->seq_len, d->seq_len, at<void>(ws, w.oc), st)))
+        return rc;
+    if ((rc = launch_inverse(*d, idx, k_keep, at<int32_t>(ws, w.inv), st))) return rc;
+    return launch_scatter(*d, at<void>(ws, w.oc), at<int32_t>(ws, w.inv), out, st);
+}
+
+int tsa_dense_attention(const tsa_desc* d, const void* q, const void* k, const void* v, void* out,
+                        void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    return attend_dispatch(*d, q, k, v, nullptr, d->seq_len, d->n_heads / d->n_kv_heads,
+                           d->seq_len, d->seq_len, out, S(stream));
+}
+
+int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, const void* v,
+                               void* out, int32_t* idx_out, int32_t* k_keep_out,
+                               int32_t* k_keep_host, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!k_keep_out) return invalid("tsa_sparse_attention_layer: k_keep_out is required");
+    cudaStream_t st = S(stream);
+    int rc;
+    if (d->mode == TSA_MODE_DENSE) {
+        if ((rc = launch_write_int(k_keep_out, d->seq_len, st))) return rc;
+        if ((rc = tsa_dense_attention(d, q, k, v, out, stream))) return rc;
+    } else {
+        const Workspace w = workspace_layout(*d);
+        float* s = at<float>(ws, w.scores);
+        int32_t* idx = idx_out ? idx_out : at<int32_t>(ws, w.idx);
+        int32_t* inv = at<int32_t>(ws, w.inv);
+        const int fb = forced_begin(*d);
+        const int nf = d->seq_len - fb;
+        if ((rc = tsa_score(d, q, k, s, ws, stream))) return rc;
+        if ((rc = budget_impl(*d, s, k_keep_out, ws, std::max(1, nf), st))) return rc;
+        if ((rc = launch_select(*d, s, k_keep_out, nullptr, nf, fb, idx, inv, st))) return rc;
+        if ((rc = launch_gather(*d, q, k, v, idx, k_keep_out, at<void>(ws, w.qc), at<void>(ws, w.kc),
+                                at<void>(ws, w.vc), st)))
+            return rc;
+        if ((rc = attend_dispatch(*d, at<void>(ws, w.qc), at<void>(ws, w.kc), at<void>(ws, w.vc),
+                                  k_keep_out, d->seq_len, 1, d->seq_len, d->seq_len,
+                                  at<void>(ws, w.oc), st)))
+            return rc;
+        if ((rc = launch_scatter(*d, at<void>(ws, w.oc), inv, out, st))) return rc;
+    }
+    if (k_keep_host) {
+        cudaError_t e = cudaMemcpyAsync(k_keep_host, k_keep_out, 4, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return cuda_check(e, "k_keep copy");
+    }
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+// Shared host/device definitions for the TSA B200 kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/tsa_b200.h"
+
+namespace tsa {
+
+constexpr int kNumSMs = 148;
+
+// Error state (thread-local, read through tsa_last_error()).
+void set_error(const std::string& msg);
+int invalid(const std::string& msg);
+int cuda_check(cudaError_t e, const char* what);
+
+#define TSA_LAUNCH_CHECK(what)                                             \
+    do {                                                                   \
+        cudaError_t e_ = cudaGetLastError();                               \
+        if (e_ != cudaSuccess) return ::tsa::cuda_check(e_, what);         \
+    } while (0)
+
+// Element access for the two supported element types.
+template <typename T>
+struct Elem;
+template <>
+struct Elem<float> {
+    static __device__ __forceinline__ float to_f32(float x) { return x; }
+    static __device__ __forceinline__ float from_f32(float x) { return x; }
+};
+template <>
+struct Elem<__nv_bfloat16> {
+    static __device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+    static __device__ __forceinline__ __nv_bfloat16 from_f32(float x) { return __float2bfloat16(x); }
+};
+
+inline size_t elem_bytes(int dtype) { return dtype == TSA_BF16 ? 2 : 4; }
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Workspace layout (all offsets 256-B aligned).  Sized for the whole layer so
+// one allocation serves every stage.
+struct Workspace {
+    // selection / budget scratch
+    size_t status;    // int32 device status word (0 ok, else error code)
+    size_t k_keep;    // int32 scratch k_keep for composite calls
+    size_t headsum;   // f32 [L]        sum_h s[h, t]
+    size_t logits;    // f32 [H x lq x L] reference-order scoring rows (REFERENCE mode)
+    size_t rowstat;   // f32 [H x lq x 2] (fast scoring: row max / sum)
+    size_t scores;    // f32 [H x L]
+    size_t forced;    // int32 [max(L, 1)]
+    size_t idx;       // int32 [H x L]
+    size_t inv;       // int32 [H x L]
+    size_t qc, kc, vc, oc;  // dtype [H x L x d]
+    size_t total;
+};
+
+Workspace workspace_layout(const tsa_desc& d);
+
+inline int lq_of(const tsa_desc& d) { return d.last_q < d.seq_len ? d.last_q : d.seq_len; }
+
+bool score_fast_available();
+
+inline int scoring_mode(const tsa_desc& d) {
+    if (d.scoring == TSA_SCORING_DEFAULT)
+        return (d.dtype == TSA_BF16 && d.d_head == 128 && score_fast_available())
+                   ? TSA_SCORING_FAST
+                   : TSA_SCORING_REFERENCE;
+    return d.scoring;
+}
+
+// --------------------------------------------------------------- launchers
+// score.cu
+int launch_score_reference(const tsa_desc& d, const void* q, const void* k, float* s,
+                           float* logits, cudaStream_t st);
+int launch_score_fast(const tsa_desc& d, const void* q, const void* k, float* s, float* logits,
+                      float* rowstat, cudaStream_t st);
+// select.cu
+int launch_budget(const tsa_desc& d, const float* s, int32_t* k_keep, float* headsum,
+                  int32_t* status, int min_keep, cudaStream_t st);
+int launch_select(const tsa_desc& d, const float* s, const int32_t* k_keep, const int32_t* forced,
+                  int32_t n_forced, int32_t forced_begin, int32_t* idx, int32_t* inv,
+                  cudaStream_t st);
+int launch_aggregate(const tsa_desc& d, const float* s, float* sl, float* headsum,
+                     int32_t* status, cudaStream_t st);
+int launch_coverage_from_sl(const tsa_desc& d, const float* sl, int32_t* k_keep, int32_t* status,
+                            int min_keep, cudaStream_t st);
+int launch_write_int(int32_t* dst, int32_t value, cudaStream_t st);
+// gather_scatter.cu
+int launch_gather(const tsa_desc& d, const void* q, const void* k, const void* v,
+                  const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
+                  cudaStream_t st);
+int launch_scatter(const tsa_desc& d, const void* oc, const int32_t* inv, void* out,
+                   cudaStream_t st);
+int launch_inverse(const tsa_desc& d, const int32_t* idx, const int32_t* k_keep, int32_t* inv,
+                   cudaStream_t st);
+int launch_colsum_pool(const tsa_desc& d, const float* probs, float* s, cudaStream_t st);
+// attend_simt.cu / attend_sm100.cu
+int launch_attend_simt(const tsa_desc& d, const void* q, const void* k, const void* v,
+                       const int32_t* n_dev, int32_t n_const, int32_t kv_group, int32_t rows_per_head,
+                       int32_t kv_rows_per_head, void* o, cudaStream_t st);
+int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const void* v,
+                        const int32_t* n_dev, int32_t n_const, int32_t kv_group,
+                        int32_t rows_per_head, int32_t kv_rows_per_head, void* o,
+                        cudaStream_t st);
+bool attend_sm100_supported(const tsa_desc& d);
+
+}  // namespace tsa

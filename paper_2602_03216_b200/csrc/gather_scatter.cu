@@ -1,0 +1,149 @@
+// K4 gather / K6 scatter: HBM-bound row movement with 16-byte vector accesses.
+//
+// gather  (gather_rows x3, tensor_ops.cpp:92-99 via attention.cpp:93-95):
+//   qc[h, r] = q[h, idx[h, r]],  kc[h, r] = k[kv(h), idx[h, r]],  vc likewise,
+//   for r < k_keep (device).  Bytes per call: 6 * H_shard * k * d * b (+ 4 * H * k idx).
+// scatter (scatter_rows, tensor_ops.cpp:101-112 via attention.cpp:96):
+//   out[h, t] = oc[h, inv[h, t]] if inv >= 0 else +0.0 -- every output row is
+//   written exactly once (no zero-fill pass).  Bytes: H*L*d*b written +
+//   H*k*d*b read + 4*H*L inv.
+#include "common.cuh"
+
+namespace tsa {
+namespace {
+
+// One warp moves `rows_per_warp` rows; lanes stride over the row's 16-B chunks.
+__global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ q,
+                                                     const uint4* __restrict__ k,
+                                                     const uint4* __restrict__ v,
+                                                     const int32_t* __restrict__ idx,
+                                                     const int32_t* __restrict__ k_keep_p,
+                                                     uint4* __restrict__ qc, uint4* __restrict__ kc,
+                                                     uint4* __restrict__ vc, int L, int group,
+                                                     int chunks /* 16-B chunks per row */,
+                                                     int head_begin) {
+    const int h = head_begin + blockIdx.y;
+    const int kv = h / group;
+    const int n = *k_keep_p;
+    const int rows_per_block = (256 / 32) * 8;
+    const int r0 = blockIdx.x * rows_per_block;
+    if (r0 >= n) {
+        // Zero the rows of the last partial 128-row tile past n: the tensor-core
+        // attention loads whole tiles, and P = 0 times a stale NaN would poison O.
+        const int pad_end = min(L, (n + 127) / 128 * 128);
+        if (r0 >= pad_end) return;
+        const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+        for (int rr = 0; rr < 8; ++rr) {
+            const int r = r0 + warp * 8 + rr;
+            if (r >= pad_end) break;
+            const size_t dst = ((size_t)h * L + r) * chunks;
+            for (int c = lane; c < chunks; c += 32) {
+                qc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+                kc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+                vc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+            }
+        }
+        return;
+    }
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int32_t* idx_h = idx + (size_t)h * L;
+    const int pad_end = min(L, (n + 127) / 128 * 128);
+    for (int rr = 0; rr < 8; ++rr) {
+        const int r = r0 + warp * 8 + rr;
+        if (r >= pad_end) break;
+        if (r >= n) {
+            const size_t dst = ((size_t)h * L + r) * chunks;
+            for (int c = lane; c < chunks; c += 32) {
+                qc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+                kc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+                vc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+            }
+            continue;
+        }
+        const int t = idx_h[r];
+        const size_t src_q = ((size_t)h * L + t) * chunks;
+        const size_t src_kv = ((size_t)kv * L + t) * chunks;
+        const size_t dst = ((size_t)h * L + r) * chunks;
+        for (int c = lane; c < chunks; c += 32) {
+            const uint4 a = __ldg(q + src_q + c);
+            const uint4 b = __ldg(k + src_kv + c);
+            const uint4 e = __ldg(v + src_kv + c);
+            qc[dst + c] = a;
+            kc[dst + c] = b;
+            vc[dst + c] = e;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ oc,
+                                                      const int32_t* __restrict__ inv,
+                                                      uint4* __restrict__ out, int L, int chunks,
+                                                      int head_begin) {
+    const int h = head_begin + blockIdx.y;
+    const int rows_per_block = 64;
+    const int t0 = blockIdx.x * rows_per_block;
+    const int32_t* inv_h = inv + (size_t)h * L;
+    const int total = rows_per_block * chunks;
+    for (int e = threadIdx.x; e < total; e += 256) {
+        const int t = t0 + e / chunks, c = e % chunks;
+        if (t >= L) break;
+        const int r = inv_h[t];
+        uint4 val = make_uint4(0u, 0u, 0u, 0u);
+        if (r >= 0) val = __ldg(oc + ((size_t)h * L + r) * chunks + c);
+        out[((size_t)h * L + t) * chunks + c] = val;
+    }
+}
+
+__global__ void inverse_fill_kernel(int32_t* __restrict__ inv, int L, int head_begin) {
+    const int h = head_begin + blockIdx.y;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < L) inv[(size_t)h * L + t] = -1;
+}
+
+__global__ void inverse_set_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ k_keep_p,
+                                   int32_t* __restrict__ inv, int L, int head_begin) {
+    const int h = head_begin + blockIdx.y;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < *k_keep_p) inv[(size_t)h * L + idx[(size_t)h * L + r]] = r;
+}
+
+}  // namespace
+
+// inv[h, t] = r where idx[h, r] == t, else -1 (for a caller-supplied selection).
+int launch_inverse(const tsa_desc& d, const int32_t* idx, const int32_t* k_keep, int32_t* inv,
+                   cudaStream_t st) {
+    const int L = d.seq_len, nh = d.head_end - d.head_begin;
+    dim3 grid((L + 255) / 256, nh);
+    inverse_fill_kernel<<<grid, 256, 0, st>>>(inv, L, d.head_begin);
+    inverse_set_kernel<<<grid, 256, 0, st>>>(idx, k_keep, inv, L, d.head_begin);
+    TSA_LAUNCH_CHECK("inverse");
+    return 0;
+}
+
+int launch_gather(const tsa_desc& d, const void* q, const void* k, const void* v,
+                  const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
+                  cudaStream_t st) {
+    const int L = d.seq_len;
+    const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / 16);
+    const int nh = d.head_end - d.head_begin;
+    dim3 grid((L + 63) / 64, nh);
+    gather_kernel<<<grid, 256, 0, st>>>((const uint4*)q, (const uint4*)k, (const uint4*)v, idx,
+                                        k_keep, (uint4*)qc, (uint4*)kc, (uint4*)vc, L,
+                                        d.n_heads / d.n_kv_heads, chunks, d.head_begin);
+    TSA_LAUNCH_CHECK("gather");
+    return 0;
+}
+
+int launch_scatter(const tsa_desc& d, const void* oc, const int32_t* inv, void* out,
+                   cudaStream_t st) {
+    const int L = d.seq_len;
+    const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / 16);
+    const int nh = d.head_end - d.head_begin;
+    dim3 grid((L + 63) / 64, nh);
+    scatter_kernel<<<grid, 256, 0, st>>>((const uint4*)oc, inv, (uint4*)out, L, chunks,
+                                         d.head_begin);
+    TSA_LAUNCH_CHECK("scatter");
+    return 0;
+}
+
+}  // namespace tsa

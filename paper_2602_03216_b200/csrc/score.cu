@@ -1,0 +1,230 @@
+// K1: per-head token-importance scoring (score_tokens, token_coverage.cpp:16-50).
+//
+// REFERENCE mode reproduces the reference's f32 arithmetic on the GPU:
+//   logits  x[r, j] = (sum_p q[L-lq+r, p] * k[j, p]) * (1/sqrt(d))   p ascending, no FMA
+//                                                                     (tensor_ops.cpp:19-23)
+//   softmax e = exp(x - max) rounded to f32, sequential f32 row sum, divide
+//                                                                     (tensor_ops.cpp:47-69)
+//   colsum  c[j] = sum_r P[r, j]                                      r ascending (:43-46)
+//   pool    edge-clamped mean with Eigen's SSE2 segment-sum order     (tensor_ops.cpp:114-129)
+// so scores match the reference bit-for-bit except where glibc's expf and a
+// correctly rounded exp differ (<= 1 ulp, rare).  Three launches:
+//   score_logits_ref  -> logits[h, r, j] (only the causally allowed prefix)
+//   score_softmax_ref -> in place: P[h, r, j]
+//   score_colsum_ref  -> s[h, t] (column sums + pooling, halo of kernel/2)
+#include "common.cuh"
+
+namespace tsa {
+namespace {
+
+constexpr int LG_ROWS = 64;   // max lq rows handled per block (lq <= 64 per tile; more tiles if larger)
+constexpr int LG_KEYS = 128;  // keys per block
+constexpr int LG_PCH = 32;    // d-chunk staged in smem
+
+// Block: 256 threads = 16 row-groups (4 rows) x 16 key-groups (8 keys).
+template <typename T>
+__global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q, const T* __restrict__ k,
+                                                        float* __restrict__ logits, int H, int group,
+                                                        int L, int d, int lq, int head_begin,
+                                                        float inv_sqrt_d) {
+    __shared__ float qs[LG_PCH][LG_ROWS];
+    __shared__ float ks[LG_PCH][LG_KEYS];
+    const int h = head_begin + blockIdx.y;
+    const int r_base = blockIdx.z * LG_ROWS;
+    const int j0 = blockIdx.x * LG_KEYS;
+    // keys beyond the causal limit of the last row are never needed
+    if (j0 > L - lq + min(lq - 1, r_base + LG_ROWS - 1)) return;
+    const int kv = h / group;
+    const T* qh = q + ((size_t)h * L + (L - lq)) * d;
+    const T* kh = k + (size_t)kv * L * d;
+    const int tr = threadIdx.x / 16, tk = threadIdx.x % 16;
+    float acc[4][8];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = 0.0f;
+
+    for (int p0 = 0; p0 < d; p0 += LG_PCH) {
+        const int pn = min(LG_PCH, d - p0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < LG_ROWS * LG_PCH; e += 256) {
+            const int r = e / LG_PCH, p = e % LG_PCH;
+            const int rr = r_base + r;
+            qs[p][r] = (rr < lq && p < pn) ? Elem<T>::to_f32(qh[(size_t)rr * d + p0 + p]) : 0.0f;
+        }
+        for (int e = threadIdx.x; e < LG_KEYS * LG_PCH; e += 256) {
+            const int j = e / LG_PCH, p = e % LG_PCH;
+            const int jj = j0 + j;
+            ks[p][j] = (jj < L && p < pn) ? Elem<T>::to_f32(kh[(size_t)jj * d + p0 + p]) : 0.0f;
+        }
+        __syncthreads();
+        for (int p = 0; p < pn; ++p) {
+            float qa[4], kb[8];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) qa[a] = qs[p][tr * 4 + a];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) kb[b] = ks[p][tk * 8 + b];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b) acc[a][b] = __fadd_rn(acc[a][b], __fmul_rn(qa[a], kb[b]));
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int r = r_base + tr * 4 + a;
+        if (r >= lq) continue;
+        const int allowed = L - lq + r + 1;
+        float* out = logits + ((size_t)h * lq + r) * L;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int j = j0 + tk * 8 + b;
+            if (j < allowed) out[j] = __fmul_rn(acc[a][b], inv_sqrt_d);
+        }
+    }
+}
+
+// One warp per (head, row): max, e = (float)exp((double)(x - max)), sequential
+// f32 sum in j order, then divide.  Masked entries (j >= allowed) untouched.
+__global__ void __launch_bounds__(256) score_softmax_ref(float* __restrict__ logits, int L, int lq,
+                                                         int head_begin, int n_rows) {
+    const int warp = blockIdx.x * 8 + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    if (warp >= n_rows) return;
+    const int hl = warp / lq, r = warp % lq;
+    const int h = head_begin + hl;
+    float* row = logits + ((size_t)h * lq + r) * L;
+    const int allowed = L - lq + r + 1;
+    float mx = -INFINITY;
+    for (int j = lane; j < allowed; j += 32) mx = fmaxf(mx, row[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.0f;  // meaningful in lane 0 only
+    for (int j0 = 0; j0 < allowed; j0 += 32) {
+        const int j = j0 + lane;
+        float e = 0.0f;
+        if (j < allowed) {
+            e = (float)exp((double)__fsub_rn(row[j], mx));
+            row[j] = e;
+        }
+        const int cnt = min(32, allowed - j0);
+        for (int i = 0; i < cnt; ++i) {
+            const float ei = __shfl_sync(0xffffffffu, e, i);
+            sum = __fadd_rn(sum, ei);
+        }
+    }
+    sum = __shfl_sync(0xffffffffu, sum, 0);
+    for (int j = lane; j < allowed; j += 32) row[j] = __fdiv_rn(row[j], sum);
+}
+
+// Eigen SSE2 segment sum order (see oracle/tsa_oracle.c eigen_segment_sum).
+__device__ __forceinline__ float eigen_segment_sum(const float* seg, int n, int base) {
+    int a = (4 - (base & 3)) & 3;
+    if (a > n) a = n;
+    const int aligned_size = ((n - a) / 4) * 4;
+    if (aligned_size == 0) {
+        float r = seg[0];
+        for (int i = 1; i < n; ++i) r = __fadd_rn(r, seg[i]);
+        return r;
+    }
+    float p0[4], p1[4];
+    for (int l = 0; l < 4; ++l) p0[l] = seg[a + l];
+    const int aligned_end = a + aligned_size;
+    if (aligned_size > 4) {
+        const int aligned_end2 = a + ((n - a) / 8) * 8;
+        for (int l = 0; l < 4; ++l) p1[l] = seg[a + 4 + l];
+        for (int i = a + 8; i < aligned_end2; i += 8) {
+            for (int l = 0; l < 4; ++l) p0[l] = __fadd_rn(p0[l], seg[i + l]);
+            for (int l = 0; l < 4; ++l) p1[l] = __fadd_rn(p1[l], seg[i + 4 + l]);
+        }
+        for (int l = 0; l < 4; ++l) p0[l] = __fadd_rn(p0[l], p1[l]);
+        if (aligned_end > aligned_end2)
+            for (int l = 0; l < 4; ++l) p0[l] = __fadd_rn(p0[l], seg[aligned_end2 + l]);
+    }
+    float r = __fadd_rn(__fadd_rn(p0[0], p0[2]), __fadd_rn(p0[1], p0[3]));
+    for (int i = 0; i < a; ++i) r = __fadd_rn(r, seg[i]);
+    for (int i = aligned_end; i < n; ++i) r = __fadd_rn(r, seg[i]);
+    return r;
+}
+
+constexpr int CS_T = 256;
+
+// Column sums over the lq proxy rows (r ascending) for a tile of tokens plus a
+// halo, then the edge-clamped pool.  Shared by REFERENCE and FAST modes:
+// P rows are read from `probs` [H x lq x L] (entries past the causal limit are
+// treated as exact zeros, as the reference's masked softmax writes them).
+__global__ void __launch_bounds__(CS_T) score_colsum_pool(const float* __restrict__ probs,
+                                                          float* __restrict__ s, int L, int lq,
+                                                          int kernel, int head_begin) {
+    extern __shared__ float col[];  // CS_T + kernel - 1
+    const int h = head_begin + blockIdx.y;
+    const int t0 = blockIdx.x * CS_T;
+    const int half = kernel / 2;
+    const float* P = probs + (size_t)h * lq * L;
+    for (int i = threadIdx.x; i < CS_T + 2 * half; i += CS_T) {
+        const int t = t0 - half + i;
+        float c = 0.0f;
+        if (t >= 0 && t < L) {
+            // row r allows t iff t <= L - lq + r  <=>  r >= t - (L - lq)
+            const int r_first = max(0, t - (L - lq));
+            for (int r = r_first; r < lq; ++r) c = __fadd_rn(c, P[(size_t)r * L + t]);
+        }
+        col[i] = c;
+    }
+    __syncthreads();
+    const int t = t0 + threadIdx.x;
+    if (t >= L) return;
+    float out;
+    if (kernel == 1) {
+        out = col[threadIdx.x + half];
+    } else {
+        const int lo = max(0, t - half), hi = min(L - 1, t + half);
+        const int cnt = hi - lo + 1;
+        out = __fdiv_rn(eigen_segment_sum(col + (lo - t0 + half), cnt, lo), (float)cnt);
+    }
+    s[(size_t)h * L + t] = out;
+}
+
+}  // namespace
+
+int launch_colsum_pool(const tsa_desc& d, const float* probs, float* s, cudaStream_t st) {
+    const int L = d.seq_len, lq = lq_of(d);
+    const int nh = d.head_end - d.head_begin;
+    dim3 grid((L + CS_T - 1) / CS_T, nh);
+    const size_t smem = sizeof(float) * (CS_T + d.kernel - 1);
+    score_colsum_pool<<<grid, CS_T, smem, st>>>(probs, s, L, lq, d.kernel, d.head_begin);
+    TSA_LAUNCH_CHECK("score_colsum_pool");
+    return 0;
+}
+
+int launch_score_reference(const tsa_desc& d, const void* q, const void* k, float* s,
+                           float* logits, cudaStream_t st) {
+    const int L = d.seq_len, lq = lq_of(d), D = d.d_head;
+    const int nh = d.head_end - d.head_begin;
+    const int group = d.n_heads / d.n_kv_heads;
+    const float inv_sqrt_d = 1.0f / sqrtf((float)D);
+    dim3 grid((L + LG_KEYS - 1) / LG_KEYS, nh, (lq + LG_ROWS - 1) / LG_ROWS);
+    if (d.dtype == TSA_BF16)
+        score_logits_ref<__nv_bfloat16><<<grid, 256, 0, st>>>(
+            (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, logits, d.n_heads, group, L, D, lq,
+            d.head_begin, inv_sqrt_d);
+    else
+        score_logits_ref<float><<<grid, 256, 0, st>>>((const float*)q, (const float*)k, logits,
+                                                      d.n_heads, group, L, D, lq, d.head_begin,
+                                                      inv_sqrt_d);
+    TSA_LAUNCH_CHECK("score_logits_ref");
+    const int n_rows = nh * lq;
+    score_softmax_ref<<<(n_rows + 7) / 8, 256, 0, st>>>(logits, L, lq, d.head_begin, n_rows);
+    TSA_LAUNCH_CHECK("score_softmax_ref");
+    return launch_colsum_pool(d, logits, s, st);
+}
+
+bool score_fast_available() { return false; }
+
+int launch_score_fast(const tsa_desc& d, const void* q, const void* k, float* s, float* logits,
+                      float* rowstat, cudaStream_t st) {
+    (void)d, (void)q, (void)k, (void)s, (void)logits, (void)rowstat, (void)st;
+    return invalid("score_tokens: FAST (tensor-core) scoring is not built in this version");
+}
+
+}  // namespace tsa

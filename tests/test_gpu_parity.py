@@ -1,0 +1,301 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle and the
+reference-generated golden fixtures.  Runs on the B200 box: -m gpu."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_03216_b200 as tsa
+from oracle.oracle import RefRng, equiv_heads, gqa_heads
+from tests import parity
+from tests.golden.make_golden import load_cases
+
+pytestmark = pytest.mark.gpu
+
+CASES = load_cases()
+
+
+def dev(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+def host(t):
+    return t.detach().float().cpu().numpy()
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def heads_of(q, k, v, dtype=torch.float32):
+    return tsa.HeadTensors(dev(q, dtype), dev(k, dtype), dev(v, dtype))
+
+
+# ------------------------------------------------------------------ scoring
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_score_reference_mode_vs_golden(cuda, name):
+    c = CASES[name]
+    hs = tsa.score_tokens(heads_of(c["q"], c["k"], c["v"]), c["last_q"], c["kernel"])
+    s = host(hs.s)
+    exact = np.mean(bits(s) == bits(c["scores"]))
+    assert exact >= 0.99, f"only {exact:.4f} of scores bit-identical"
+    np.testing.assert_allclose(s, c["scores"], rtol=4 * 2**-23, atol=1e-30)
+
+
+def test_score_bf16_inputs_match_oracle_on_upcast(cuda, port):
+    q, k, v = gqa_heads(RefRng(11), 8, 2, 1000, 128)
+    hq = heads_of(q, k, v, torch.bfloat16)
+    up = [host(t) for t in (hq.q, hq.k)]
+    s_gpu = host(tsa.score_tokens(hq, 64, 7, scoring=1).s)
+    s_ora = port.score_tokens(up[0], up[1], 64, 7)
+    assert np.mean(bits(s_gpu) == bits(s_ora)) >= 0.99
+
+
+# ----------------------------------------------------- budget / selection
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_budget_and_select_on_oracle_scores_bit_exact(cuda, port, name):
+    """Integer stages fed identical scores must agree exactly."""
+    c = CASES[name]
+    s = dev(c["scores"])
+    sl = tsa.aggregate_scores(tsa.HeadScores(s))
+    assert np.array_equal(bits(host(sl.s)), bits(port.aggregate_scores(c["scores"])))
+    k_gpu = tsa.coverage_budget(sl, c["tau"], max(1, len(c["forced"])))
+    k_ora, pp, pa = port.coverage_budget(host(sl.s), c["tau"], max(1, len(c["forced"])),
+                                         with_prefix=True)
+    parity.check_budget(k_gpu, k_ora, pp, pa, c["tau"])
+    assert k_ora == c["k_keep"]
+    sel = tsa.select_tokens(tsa.HeadScores(s), c["k_keep"], c["forced"])
+    assert np.array_equal(host(sel.indices).astype(np.int32), c["idx"])
+
+
+@pytest.mark.parametrize("L,H,tau,seed", [(4096, 8, 0.005, 1), (4096, 8, 0.1, 2),
+                                          (4096, 8, 0.5, 3), (2000, 4, 0.99, 4),
+                                          (131072, 2, 0.01, 5), (65537, 4, 0.3, 6)])
+def test_budget_random_scores(cuda, port, L, H, tau, seed):
+    rng = np.random.default_rng(seed)
+    # heavy-tailed positive scores with ties
+    s = np.exp(rng.normal(0, 3, (H, L))).astype(np.float32)
+    s[:, ::17] = s[:, 3:4]
+    s_dev = dev(s)
+    k_gpu = tsa.coverage_budget(tsa.aggregate_scores(tsa.HeadScores(s_dev)), tau, 1)
+    sl = port.aggregate_scores(s)
+    k_ora, pp, pa = port.coverage_budget(sl, tau, 1, with_prefix=True)
+    parity.check_budget(k_gpu, k_ora, pp, pa, tau)
+
+
+@pytest.mark.parametrize("L,k,nf", [(1, 1, 1), (10, 3, 1), (4096, 1000, 1), (4096, 4096, 1),
+                                    (5000, 64, 64), (131072, 70000, 1), (3000, 1, 1)])
+def test_select_random_with_ties(cuda, port, L, k, nf):
+    rng = np.random.default_rng(L + k)
+    s = rng.integers(0, 50, (4, L)).astype(np.float32) / 7.0  # many exact ties
+    forced = list(range(L - nf, L))
+    sel = tsa.select_tokens(tsa.HeadScores(dev(s)), k, forced)
+    assert np.array_equal(host(sel.indices).astype(np.int32), port.select_tokens(s, k, forced))
+
+
+def test_select_kats(cuda):
+    # test_coverage.cpp:227-296
+    def sel(rows, k, forced=()):
+        return host(tsa.select_tokens(tsa.HeadScores(dev(np.array(rows, np.float32))), k,
+                                      forced).indices).astype(int).tolist()
+    assert sel([[0.1, 0.9, 0.3, 0.5], [0.8, 0.1, 0.7, 0.2]], 2) == [[1, 3], [0, 2]]
+    assert sel([[0.5, 0.5, 0.5, 0.5]], 2) == [[0, 1]]
+    assert sel([[0.9, 0.8, 0.7, 0.01]], 2, [3]) == [[0, 3]]
+    assert sel([[0.9, 0.8, 0.7, 0.01]], 1, [3]) == [[3]]
+    assert sel([[0.1, 0.2, 0.3, 0.4]], 2, [1, 0]) == [[0, 1]]
+    assert sel([[0.1, 0.2, 0.3, 0.4]], 2, [1, 1]) == [[1, 3]]
+    with pytest.raises(tsa.InvalidArgument):
+        sel([[0.1, 0.2, 0.3, 0.4]], 1, [0, 1])
+    with pytest.raises(tsa.InvalidArgument):
+        sel([[0.1, 0.2, 0.3, 0.4]], 5)
+
+
+def test_budget_kats(cuda):
+    def cb(v, tau, mk=1):
+        return tsa.coverage_budget(tsa.LayerScores(dev(np.array(v, np.float32))), tau, mk)
+    a = [0.4, 0.3, 0.2, 0.1]
+    assert cb(a, 0.25) == 2 and cb(a, 0.0) == 4 and cb(a, 1.0) == 1 and cb(a, 1.0, 3) == 3
+    assert [cb([0.25] * 4, t) for t in (0.5, 0.26, 0.24)] == [2, 2, 3]
+    assert cb([0.7, 0.1, 0.1, 0.1], 0.9) == 1 and cb([0.7, 0.1, 0.1, 0.1], 0.9, 2) == 2
+    with pytest.raises(tsa.InvalidArgument):
+        tsa.aggregate_scores(tsa.HeadScores(dev(np.zeros((2, 2), np.float32))))
+
+
+# ---------------------------------------------------------------- attention
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_token_sparse_attention_vs_golden(cuda, name):
+    c = CASES[name]
+    h = heads_of(c["q"], c["k"], c["v"])
+    sel = tsa.TokenSelection(indices=dev(c["idx"], torch.int32), k_keep=c["k_keep"],
+                             forced=c["forced"])
+    out = host(tsa.token_sparse_attention(h, sel))
+    assert np.abs(out - c["out"]).max() <= parity.F32_GATE
+    assert parity.unselected_rows_zero(out, c["idx"], c["L"])
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_sparse_layer_end_to_end_vs_golden(cuda, port, name):
+    c = CASES[name]
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=c["tau"],
+                          last_q=c["last_q"], kernel=c["kernel"],
+                          forced=tsa.ForcedPolicy(c["policy"]))
+    out, st = tsa.sparse_attention_layer(heads_of(c["q"], c["k"], c["v"]), plan)
+    assert st.k_keep == c["k_keep"]
+    idx = host(st.selection.indices).astype(np.int32)
+    parity.check_index_sets(idx, c["idx"], c["scores"], c["forced"])
+    if np.array_equal(idx, c["idx"]):
+        assert np.abs(host(out) - c["out"]).max() <= parity.F32_GATE
+
+
+def test_run_equiv_full_grid(cuda, port):
+    """All 135 run_equiv instances (bench.cpp:225-273) through the GPU layer
+    call, checked against masked_sparse_oracle at the 1e-5 gate."""
+    grid = [(L, H, d, tau) for L in (16, 64, 256) for H in (1, 4, 8) for d in (8, 16, 32)
+            for tau in (0.0, 0.005, 0.1, 0.5, 0.99)]
+    for i, (L, H, d, tau) in enumerate(grid):
+        q, k, v = equiv_heads(42, i, L, H, d)
+        plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
+        out, st = tsa.sparse_attention_layer(heads_of(q, k, v), plan)
+        idx = host(st.selection.indices).astype(np.int32)
+        o = host(out)
+        err = max(np.abs(o[h] - port.masked_sparse_oracle(q[h], k[h], v[h], idx[h])).max()
+                  for h in range(H))
+        assert err <= parity.F32_GATE, (i, L, H, d, tau, err)
+        if tau == 0.0:
+            assert st.k_keep == L
+
+
+@pytest.mark.parametrize("H,Hkv,L,n", [(4, 2, 128, 128), (4, 2, 300, 300), (2, 1, 1000, 777),
+                                       (8, 8, 2048, 2048), (4, 1, 4096, 1500), (2, 2, 129, 1)])
+def test_tcgen05_attention_bf16_vs_oracle(cuda, port, H, Hkv, L, n):
+    q, k, v = gqa_heads(RefRng(L + n), H, Hkv, L, 128)
+    h = heads_of(q, k, v, torch.bfloat16)
+    up = [host(t) for t in (h.q, h.k, h.v)]
+    rng = np.random.default_rng(n)
+    idx = np.stack([np.sort(rng.choice(L, n, replace=False)) for _ in range(H)]).astype(np.int32)
+    sel = tsa.TokenSelection(indices=dev(idx, torch.int32), k_keep=n, forced=[])
+    out = host(tsa.token_sparse_attention(h, sel))
+    ref = port.token_sparse_attention(up[0], up[1], up[2], idx, n_threads=8)
+    assert parity.rel_l2(out, ref) <= parity.BF16_REL_L2
+    assert parity.unselected_rows_zero(out, idx, L)
+
+
+@pytest.mark.parametrize("H,Hkv,L", [(4, 2, 512), (2, 1, 1000), (4, 4, 2048)])
+def test_dense_attention_bf16_and_f32(cuda, port, H, Hkv, L):
+    q, k, v = gqa_heads(RefRng(L), H, Hkv, L, 128)
+    for dt, gate in ((torch.bfloat16, "bf16"), (torch.float32, "f32")):
+        h = heads_of(q, k, v, dt)
+        up = [host(t) for t in (h.q, h.k, h.v)]
+        out = torch.empty_like(h.q)
+        for i in range(H):
+            out[i] = tsa.dense_causal_attention(h.q[i], h.k[h.kv_head(i)], h.v[h.kv_head(i)])
+        for i in (0, H - 1):
+            ref = port.dense_causal_attention(up[0][i], up[1][i * Hkv // H], up[2][i * Hkv // H])
+            o = host(out[i])
+            if gate == "bf16":
+                assert parity.rel_l2(o, ref) <= parity.BF16_REL_L2
+            else:
+                assert np.abs(o - ref).max() <= parity.F32_GATE
+
+
+def test_tau0_equals_dense_bitwise(cuda):
+    """test_bench.cpp:134-145 / SPEC: tau = 0 keeps every token and the sparse
+    path reproduces dense attention exactly (same kernel, same inputs)."""
+    q, k, v = gqa_heads(RefRng(21), 4, 2, 640, 128)
+    for dt in (torch.bfloat16, torch.float32):
+        h = heads_of(q, k, v, dt)
+        plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.0)
+        out, st = tsa.sparse_attention_layer(h, plan)
+        dense, _ = tsa.sparse_attention_layer(h, tsa.SparsePlan())
+        assert st.k_keep == 640
+        assert torch.equal(out, dense)
+
+
+def test_causality_bitwise(cuda):
+    """test_attention.cpp:293-316: perturbing K/V after row t leaves rows <= t unchanged."""
+    q, k, v = gqa_heads(RefRng(22), 4, 2, 512, 128)
+    for dt in (torch.bfloat16, torch.float32):
+        h = heads_of(q, k, v, dt)
+        plan = tsa.SparsePlan(mode=tsa.SparseMode.kFixed, sparse_layers=[0], s_fixed=0.5)
+        base, st = tsa.sparse_attention_layer(h, plan)
+        sel = st.selection
+        cut = 300
+        k2, v2 = h.k.clone(), h.v.clone()
+        k2[:, cut + 1:] += 3.0
+        v2[:, cut + 1:] -= 2.0
+        pert = tsa.token_sparse_attention(tsa.HeadTensors(h.q, k2, v2), sel)
+        assert torch.equal(base[:, : cut + 1], pert[:, : cut + 1])
+
+
+def test_inner_seam_sees_compressed_shapes(cuda):
+    """test_attention.cpp:318-338: `inner` is called once per head with k x d."""
+    q, k, v = gqa_heads(RefRng(23), 4, 2, 100, 16)
+    h = heads_of(q, k, v)
+    sel = tsa.select_tokens(tsa.score_tokens(h, 64, 7), 37, [99])
+    shapes = []
+
+    def probe(qc, kc, vc):
+        shapes.append((tuple(qc.shape), tuple(kc.shape), tuple(vc.shape)))
+        return tsa.dense_causal_attention(qc, kc, vc)
+
+    a = tsa.token_sparse_attention(h, sel, inner=probe)
+    b = tsa.token_sparse_attention(h, sel)
+    assert shapes == [((37, 16),) * 3] * 4
+    assert torch.equal(a, b)
+
+
+def test_fixed_mode_and_recent_window(cuda, port):
+    q, k, v = gqa_heads(RefRng(24), 8, 2, 700, 32)
+    h = heads_of(q, k, v)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kFixed, sparse_layers=[0], s_fixed=0.3,
+                          forced=tsa.ForcedPolicy.kRecentWindow, last_q=50)
+    out, st = tsa.sparse_attention_layer(h, plan)
+    assert st.k_keep == port.fixed_budget(700, 0.3, 50) == 490
+    s = port.score_tokens(q, k, 50, 7)
+    forced = list(range(650, 700))
+    ora_idx = port.select_tokens(s, 490, forced)
+    idx = host(st.selection.indices).astype(np.int32)
+    parity.check_index_sets(idx, ora_idx, s, forced)
+    ref = port.token_sparse_attention(q, k, v, idx)
+    assert np.abs(host(out) - ref).max() <= parity.F32_GATE
+
+
+def test_dense_layer_not_in_plan(cuda):
+    q, k, v = gqa_heads(RefRng(25), 4, 2, 256, 128)
+    h = heads_of(q, k, v, torch.bfloat16)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[1], tau=0.5)
+    out, st = tsa.sparse_attention_layer(h, plan, layer=0)
+    assert not st.sparse and st.k_keep == 256 and st.selection is None
+
+
+def test_edge_lengths(cuda, port):
+    for L in (1, 2, 3, 17):
+        q, k, v = gqa_heads(RefRng(30 + L), 2, 1, L, 8)
+        plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.5)
+        out, st = tsa.sparse_attention_layer(heads_of(q, k, v), plan)
+        s = port.score_tokens(q, k, 64, 7)
+        k_ora = port.coverage_budget(port.aggregate_scores(s), 0.5, 1)
+        assert st.k_keep == k_ora
+        idx = port.select_tokens(s, k_ora, [L - 1])
+        assert np.array_equal(host(st.selection.indices).astype(np.int32), idx)
+        assert np.abs(host(out) - port.token_sparse_attention(q, k, v, idx)).max() <= 1e-5
+
+
+@pytest.mark.slow
+def test_cfg1_full_size_f32(cuda, port):
+    """BASELINE configs[0]: H=32/8, d=128, L=4096, f32, tau=0.5 vs the oracle."""
+    rng = RefRng(2026)
+    q, k, v = gqa_heads(rng, 32, 8, 4096, 128)
+    h = heads_of(q, k, v)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.5)
+    out, st = tsa.sparse_attention_layer(h, plan)
+    s = port.score_tokens(q, k, 64, 7, n_threads=8)
+    k_ora, pp, pa = port.coverage_budget(port.aggregate_scores(s), 0.5, 1, with_prefix=True)
+    parity.check_budget(st.k_keep, k_ora, pp, pa, 0.5)
+    idx = host(st.selection.indices).astype(np.int32)
+    if st.k_keep == k_ora:
+        parity.check_index_sets(idx, port.select_tokens(s, k_ora, [4095]), s, [4095])
+    ref = port.token_sparse_attention_sampled(q, k, v, idx, head_stride=4, r0=0,
+                                              r1=st.k_keep, n_threads=8)
+    o = host(out)
+    for hh in range(0, 32, 4):
+        assert np.abs(o[hh] - ref[hh]).max() <= parity.F32_GATE
