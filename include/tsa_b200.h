@@ -77,9 +77,13 @@ TSA_API void tsa_desc_init(tsa_desc* d, int32_t n_heads, int32_t n_kv_heads, int
                    int32_t d_head, int32_t dtype);
 TSA_API const char* tsa_last_error(void);
 TSA_API const char* tsa_version(void);
+/* Number of kernels this library has launched in the process (all streams). */
+TSA_API uint64_t tsa_kernel_launches(void);
 
 /* Bytes of scratch the calls below need for `d` (scores, index lists,
- * compressed Q/K/V/O buffers and selection scratch), 256-B aligned. */
+ * compressed Q/K/V/O buffers and selection scratch), 256-B aligned.
+ * tsa_budget, tsa_aggregate_scores and tsa_coverage_budget only touch the
+ * first 512 + align256(4 L) bytes. */
 TSA_API int tsa_workspace_size(const tsa_desc* d, size_t* bytes);
 
 /* --- the path, stage by stage ------------------------------------------ */

@@ -275,22 +275,23 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2-D map over a [rows x 128] bf16 matrix, 64 x 128 boxes, 128-B swizzle.
-int make_map(CUtensorMap* m, const void* base, uint64_t rows) {
+}  // namespace
+
+// 2-D map over a [rows x 128] bf16 matrix, 64-column x box_rows boxes, 128-B swizzle.
+int make_bf16_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
     auto fn = encode_fn();
-    if (!fn) return invalid("attend: cuTensorMapEncodeTiled unavailable");
+    if (!fn) return invalid("tsa: cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {HD, rows};
     cuuint64_t strides[1] = {HD * 2};
-    cuuint32_t box[2] = {64, 128};
+    cuuint32_t box[2] = {64, box_rows};
     cuuint32_t es[2] = {1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return invalid("attend: tensor map encode failed (" + std::to_string((int)r) + ")");
+    if (r != CUDA_SUCCESS)
+        return invalid("tsa: tensor map encode failed (" + std::to_string((int)r) + ")");
     return 0;
 }
-
-}  // namespace
 
 bool attend_sm100_supported(const tsa_desc& d) { return d.dtype == TSA_BF16 && d.d_head == HD; }
 
@@ -304,9 +305,9 @@ int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const v
     const int n_kv_heads_buf = (n_q_heads + kv_group - 1) / kv_group;
     CUtensorMap mq, mk, mv;
     int rc;
-    if ((rc = make_map(&mq, q, (uint64_t)n_q_heads * rows_per_head))) return rc;
-    if ((rc = make_map(&mk, k, (uint64_t)n_kv_heads_buf * kv_rows_per_head))) return rc;
-    if ((rc = make_map(&mv, v, (uint64_t)n_kv_heads_buf * kv_rows_per_head))) return rc;
+    if ((rc = make_bf16_map_2d(&mq, q, (uint64_t)n_q_heads * rows_per_head, 128))) return rc;
+    if ((rc = make_bf16_map_2d(&mk, k, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
+    if ((rc = make_bf16_map_2d(&mv, v, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
     const int smem = (int)sizeof(AttnSmem) + 1024;
     static bool attr_set = false;
     if (!attr_set) {

@@ -1,6 +1,7 @@
 // C ABI (include/tsa_b200.h): host-side validation with the reference's
 // error wording, workspace layout, and the stage orchestration of the sparse
 // layer branch (model.cpp:169-183).
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -10,6 +11,9 @@
 namespace tsa {
 
 static thread_local std::string g_error;
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_error = msg; }
 
@@ -37,7 +41,7 @@ Workspace workspace_layout(const tsa_desc& d) {
     w.k_keep = take(4);
     w.headsum = take(4 * L);
     w.logits = take(4 * H * lq * L);
-    w.rowstat = take(4 * H * lq * 2);
+    w.rowstat = take(8 * 128 * (2 * (size_t)kNumSMs + H + 8));  // fast-scoring row partials
     w.scores = take(4 * H * L);
     w.forced = take(4 * L);
     w.idx = take(4 * H * L);
@@ -157,6 +161,8 @@ void tsa_desc_init(tsa_desc* d, int32_t n_heads, int32_t n_kv_heads, int32_t seq
 }
 
 const char* tsa_last_error(void) { return tsa::g_error.c_str(); }
+
+uint64_t tsa_kernel_launches(void) { return tsa::g_launches.load(); }
 
 const char* tsa_version(void) { return "tsa_b200 0.1 (sm_100a)"; }
 

@@ -18,10 +18,13 @@ void set_error(const std::string& msg);
 int invalid(const std::string& msg);
 int cuda_check(cudaError_t e, const char* what);
 
+void count_launch();
+
 #define TSA_LAUNCH_CHECK(what)                                             \
     do {                                                                   \
         cudaError_t e_ = cudaGetLastError();                               \
         if (e_ != cudaSuccess) return ::tsa::cuda_check(e_, what);         \
+        ::tsa::count_launch();                                             \
     } while (0)
 
 // Element access for the two supported element types.
@@ -64,12 +67,11 @@ Workspace workspace_layout(const tsa_desc& d);
 inline int lq_of(const tsa_desc& d) { return d.last_q < d.seq_len ? d.last_q : d.seq_len; }
 
 bool score_fast_available();
+bool score_fast_supported(const tsa_desc& d);
 
 inline int scoring_mode(const tsa_desc& d) {
     if (d.scoring == TSA_SCORING_DEFAULT)
-        return (d.dtype == TSA_BF16 && d.d_head == 128 && score_fast_available())
-                   ? TSA_SCORING_FAST
-                   : TSA_SCORING_REFERENCE;
+        return score_fast_supported(d) ? TSA_SCORING_FAST : TSA_SCORING_REFERENCE;
     return d.scoring;
 }
 

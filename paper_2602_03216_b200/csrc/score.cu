@@ -219,12 +219,4 @@ int launch_score_reference(const tsa_desc& d, const void* q, const void* k, floa
     return launch_colsum_pool(d, logits, s, st);
 }
 
-bool score_fast_available() { return false; }
-
-int launch_score_fast(const tsa_desc& d, const void* q, const void* k, float* s, float* logits,
-                      float* rowstat, cudaStream_t st) {
-    (void)d, (void)q, (void)k, (void)s, (void)logits, (void)rowstat, (void)st;
-    return invalid("score_tokens: FAST (tensor-core) scoring is not built in this version");
-}
-
 }  // namespace tsa

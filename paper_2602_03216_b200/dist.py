@@ -1,0 +1,182 @@
+"""Head-parallel Token Sparse Attention over G GPUs (one process per GPU).
+
+The reference is single-process (SPEC.md:166-167 only notes heads "may be
+processed in parallel").  The path shards by query heads, GQA-aligned: rank
+g owns Q heads [g H/G, (g+1) H/G) and KV heads [g Hkv/G, (g+1) Hkv/G), so
+score / select / gather / attend / scatter are local.  Two exchanges:
+
+  C1  all-gather of the score rows s_h  ([H/G x L] f32 per rank) -- the layer
+      budget sums every head (token_coverage.cpp:55-57), and summing the
+      gathered rows in head order 0..H-1 reproduces the 1-GPU k_keep exactly;
+  C2  all-gather of the head outputs    ([H/G x L x d] per rank) -- the head
+      concat before W_O (model.cpp:197-200).
+
+Collectives go through torch.distributed (NCCL on GPUs, gloo in the CPU
+tests).  The per-stage compute is a pluggable backend: ``CudaBackend`` (the
+C ABI, the product) or a test backend; the orchestration is shared.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .ops import SparseMode, SparsePlan, _ptr, _stream
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    n_heads: int
+    n_kv_heads: int
+
+    def __post_init__(self):
+        if self.n_kv_heads % self.world != 0:
+            raise _lib.InvalidArgument(
+                f"dist: {self.n_kv_heads} KV heads cannot be split over {self.world} ranks")
+        g = self.n_heads // self.n_kv_heads
+        self.kv_per = self.n_kv_heads // self.world
+        self.h_per = self.kv_per * g
+        self.h0, self.h1 = self.rank * self.h_per, (self.rank + 1) * self.h_per
+        self.kv0, self.kv1 = self.rank * self.kv_per, (self.rank + 1) * self.kv_per
+
+
+def forced_begin(plan: SparsePlan, L: int) -> int:
+    fs = plan.forced_set(L)
+    return fs[0]
+
+
+class CudaBackend:
+    """Stage calls into libtsa_b200.so on the current CUDA stream."""
+
+    def __init__(self, H, Hkv, L, d, dtype_code, plan: SparsePlan, shard: Shard, device,
+                 scoring: int = 0):
+        self.shard, self.plan, self.device = shard, plan, device
+        self.L, self.d = L, d
+        common = dict(tau=plan.tau, s_fixed=plan.s_fixed, last_q=plan.last_q, kernel=plan.kernel,
+                      forced_policy=int(plan.forced), scoring=scoring,
+                      mode=int(plan.mode))
+        # local heads as a self-contained layer (absolute head 0 = shard.h0)
+        self.local = _lib.make_desc(shard.h_per, shard.kv_per, L, d, dtype_code, **common)
+        # the budget reads all H score rows
+        self.full = _lib.make_desc(H, Hkv, L, d, dtype_code, **common)
+        lib = _lib.load()
+        n1 = C.c_size_t()
+        _lib.check(lib.tsa_workspace_size(C.byref(self.local), C.byref(n1)))
+        # the full-width workspace only serves the budget (headsum/status)
+        self.ws = torch.zeros(max(n1.value, 256), dtype=torch.uint8, device=device)
+        budget_bytes = 512 + (4 * L + 255) // 256 * 256  # see tsa_workspace_size docs
+        self.ws_full = torch.zeros(budget_bytes, dtype=torch.uint8, device=device) \
+            if shard.world > 1 else self.ws
+        self.k_keep = torch.zeros(1, dtype=torch.int32, device=device)
+        self.idx = torch.empty((shard.h_per, L), dtype=torch.int32, device=device)
+        self.inv = torch.empty((shard.h_per, L), dtype=torch.int32, device=device)
+        sz = (shard.h_per, L, d)
+        dt = torch.bfloat16 if dtype_code == _lib.TSA_BF16 else torch.float32
+        self.qc, self.kc, self.vc, self.oc = (torch.empty(sz, dtype=dt, device=device)
+                                              for _ in range(4))
+        fb = forced_begin(plan, L)
+        self.forced = torch.arange(fb, L, dtype=torch.int32, device=device)
+        self.lib = lib
+
+    def score(self, q, k, s_local):
+        _lib.check(self.lib.tsa_score(C.byref(self.local), _ptr(q), _ptr(k), _ptr(s_local),
+                                      _ptr(self.ws), _stream(self.device)))
+
+    def budget(self, s_full):
+        _lib.check(self.lib.tsa_budget(C.byref(self.full), _ptr(s_full), _ptr(self.k_keep),
+                                       _ptr(self.ws_full), _stream(self.device)))
+        return self.k_keep
+
+    def select(self, s_local, k_keep):
+        _lib.check(self.lib.tsa_select(C.byref(self.local), _ptr(s_local), _ptr(k_keep),
+                                       _ptr(self.forced), self.forced.numel(), _ptr(self.idx),
+                                       _ptr(self.inv), _ptr(self.ws), _stream(self.device)))
+
+    def gather(self, q, k, v, k_keep):
+        _lib.check(self.lib.tsa_gather(C.byref(self.local), _ptr(q), _ptr(k), _ptr(v),
+                                       _ptr(self.idx), _ptr(k_keep), _ptr(self.qc), _ptr(self.kc),
+                                       _ptr(self.vc), _stream(self.device)))
+
+    def attend(self, k_keep):
+        _lib.check(self.lib.tsa_attend(C.byref(self.local), _ptr(self.qc), _ptr(self.kc),
+                                       _ptr(self.vc), _ptr(k_keep), 1, _ptr(self.oc),
+                                       _stream(self.device)))
+
+    def scatter(self, out_local):
+        _lib.check(self.lib.tsa_scatter(C.byref(self.local), _ptr(self.oc), _ptr(self.inv),
+                                        _ptr(out_local), _stream(self.device)))
+
+    def dense(self, q, k, v, out_local):
+        _lib.check(self.lib.tsa_dense_attention(C.byref(self.local), _ptr(q), _ptr(k), _ptr(v),
+                                                _ptr(out_local), _stream(self.device)))
+
+
+class ShardedSparseAttention:
+    """One attention layer's sparse branch (model.cpp:169-183), head-sharded.
+
+    ``step(q_local, k_local, v_local)`` takes this rank's heads ([H/G, L, d]
+    and [Hkv/G, L, d]) and returns the gathered output [H, L, d] (or the local
+    [H/G, L, d] when ``gather_output`` is False).  ``marks`` (optional) is a
+    callable(name) invoked between stages -- bench.py records CUDA events there.
+    """
+
+    def __init__(self, H, Hkv, L, d, dtype, plan: SparsePlan, rank=0, world=1, device=None,
+                 backend=None, gather_output=True, scoring: int = 0):
+        self.shard = Shard(rank, world, H, Hkv)
+        self.H, self.Hkv, self.L, self.d = H, Hkv, L, d
+        self.plan = plan
+        self.device = device
+        self.gather_output = gather_output
+        dtype_code = _lib.TSA_BF16 if dtype == torch.bfloat16 else _lib.TSA_F32
+        self.backend = backend or CudaBackend(H, Hkv, L, d, dtype_code, plan, self.shard, device,
+                                              scoring=scoring)
+        sh = self.shard
+        self.s_local = torch.zeros((sh.h_per, L), dtype=torch.float32, device=device)
+        self.s_full = self.s_local if world == 1 else torch.zeros((H, L), dtype=torch.float32,
+                                                                  device=device)
+        self.out_local = torch.empty((sh.h_per, L, d), dtype=dtype, device=device)
+        self.out_full = self.out_local if world == 1 or not gather_output else torch.empty(
+            (H, L, d), dtype=dtype, device=device)
+
+    def _all_gather(self, dst, src):
+        if self.shard.world > 1:
+            dist.all_gather_into_tensor(dst, src)
+
+    def step(self, q, k, v, marks=None, dense: bool = False):
+        mark = marks or (lambda name: None)
+        b = self.backend
+        if dense or self.plan.mode == SparseMode.kDense:
+            mark("start")
+            b.dense(q, k, v, self.out_local)
+            mark("attend")
+            self._all_gather(self.out_full, self.out_local)
+            mark("allgather_out")
+            return self.out_full
+        mark("start")
+        b.score(q, k, self.s_local)
+        mark("score")
+        self._all_gather(self.s_full, self.s_local)
+        mark("allgather_scores")
+        k_keep = b.budget(self.s_full)
+        mark("budget")
+        b.select(self.s_local, k_keep)
+        mark("select")
+        b.gather(q, k, v, k_keep)
+        mark("gather")
+        b.attend(k_keep)
+        mark("attend")
+        b.scatter(self.out_local)
+        mark("scatter")
+        self._all_gather(self.out_full, self.out_local)
+        mark("allgather_out")
+        return self.out_full
+
+    @property
+    def k_keep(self) -> int:
+        return int(self.backend.k_keep.item())

@@ -299,3 +299,39 @@ def test_cfg1_full_size_f32(cuda, port):
     o = host(out)
     for hh in range(0, 32, 4):
         assert np.abs(o[hh] - ref[hh]).max() <= parity.F32_GATE
+
+
+# -------------------------------------------------------------- FAST scoring
+@pytest.mark.parametrize("H,Hkv,L,lq", [(8, 2, 4096, 64), (4, 4, 1000, 64), (8, 1, 3000, 32),
+                                        (4, 2, 700, 128), (2, 2, 64, 64), (32, 8, 16384, 64)])
+def test_score_fast_tensor_core_vs_oracle(cuda, port, H, Hkv, L, lq):
+    from paper_2602_03216_b200 import workloads
+    q, k, v = workloads.heavy_tailed_heads(H, Hkv, L, 128, sigma=3.0, seed=L, last_q=lq)
+    h = tsa.HeadTensors(q, k, v)
+    s_fast = host(tsa.score_tokens(h, lq, 7, scoring=2).s)
+    up = [host(t) for t in (q, k)]
+    s_ora = port.score_tokens(up[0], up[1], lq, 7, n_threads=8)
+    # mass conservation (kernel 1 would be exact): per head ~ lq
+    np.testing.assert_allclose(s_fast.astype(np.float64).sum(1), s_ora.astype(np.float64).sum(1),
+                               rtol=1e-4)
+    big = s_ora > 1e-6 * s_ora.max()
+    rel = np.abs(s_fast - s_ora)[big] / s_ora[big]
+    assert rel.max() <= parity.FAST_SCORE_REL, rel.max()
+    tau = 0.01
+    sl_o = port.aggregate_scores(s_ora)
+    k_o, pp, pa = port.coverage_budget(sl_o, tau, 1, with_prefix=True)
+    k_g = tsa.coverage_budget(tsa.aggregate_scores(tsa.HeadScores(dev(s_fast))), tau, 1)
+    assert abs(k_g - k_o) <= max(2, int(parity.FAST_BUDGET_REL * L)), (k_g, k_o)
+    sel_g = host(tsa.select_tokens(tsa.HeadScores(dev(s_fast)), k_o, [L - 1]).indices)
+    parity.check_index_sets(sel_g.astype(np.int32), port.select_tokens(s_ora, k_o, [L - 1]),
+                            s_ora, [L - 1], rel_tol=parity.FAST_SCORE_REL)
+
+
+def test_fast_scoring_is_default_for_bf16_and_deterministic(cuda):
+    from paper_2602_03216_b200 import workloads
+    q, k, v = workloads.heavy_tailed_heads(8, 2, 8192, 128, seed=3)
+    h = tsa.HeadTensors(q, k, v)
+    a = tsa.score_tokens(h, 64, 7).s
+    b = tsa.score_tokens(h, 64, 7, scoring=2).s
+    c = tsa.score_tokens(h, 64, 7, scoring=2).s
+    assert torch.equal(a, b) and torch.equal(b, c)
