@@ -448,6 +448,8 @@ def calibrate(args):
 
 
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(int(os.environ.get("TSA_BENCH_HANG_S", "1200")), exit=True)
     args = parse()
     if args.calibrate:
         return calibrate(args)

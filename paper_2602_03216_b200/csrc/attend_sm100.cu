@@ -202,11 +202,13 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 lsum += p0 + p1;
                 packed[c / 2] = pack_bf16x2(p0, p1);
             }
-            if (rescale) {
+            // tcgen05.ld/st are warp-collective (.sync.aligned): the whole warp
+            // rescales when any of its rows needs it (alpha = 1 for the others)
+            if (__any_sync(0xffffffffu, rescale)) {
                 // O must hold PV_{j-1} before it is rescaled
                 mbar_wait(&sm.o_done[b ^ 1], ((j - 1) >> 1) & 1);
                 tc_fence_after();
-                const float alpha = ex2_approx(m_run - m_use);
+                const float alpha = rescale ? ex2_approx(m_run - m_use) : 1.0f;
 #pragma unroll
                 for (int c = 0; c < HD; c += 32) {
                     uint32_t r[32];
@@ -216,7 +218,7 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
                     tmem_st32(t_o + lane_off + c, r);
                 }
-                l_run *= alpha;
+                if (rescale) l_run *= alpha;
             }
             l_run += lsum;
             m_run = m_use;

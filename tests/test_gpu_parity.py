@@ -335,3 +335,43 @@ def test_fast_scoring_is_default_for_bf16_and_deterministic(cuda):
     b = tsa.score_tokens(h, 64, 7, scoring=2).s
     c = tsa.score_tokens(h, 64, 7, scoring=2).s
     assert torch.equal(a, b) and torch.equal(b, c)
+
+
+def test_tcgen05_attention_running_max_rescales(cuda, port):
+    """Keys whose logits grow along the sequence force the lazy O rescale on
+    every KV tile for some rows but not others (warp-divergent decision)."""
+    L, d = 1536, 128
+    rng = np.random.default_rng(0)
+    u = rng.normal(size=d)
+    u /= np.linalg.norm(u)
+    q = np.empty((2, L, d), np.float32)
+    q[0] = np.sqrt(d) * u + 0.1 * rng.normal(size=(L, d))
+    q[1] = rng.uniform(-1, 1, (L, d))            # a head that never rescales
+    c = (np.arange(L) / 8.0)[:, None]             # +16 per 128-key tile
+    k = (c * u[None, :] * np.where(np.arange(L) % 3 == 0, 1.0, -0.5)[:, None]
+         + 0.1 * rng.normal(size=(L, d)))[None].astype(np.float32)
+    v = rng.uniform(-1, 1, (1, L, d)).astype(np.float32)
+    h = heads_of(q, k, v, torch.bfloat16)
+    up = [host(t) for t in (h.q, h.k, h.v)]
+    out = torch.empty_like(h.q)
+    for i in range(2):
+        out[i] = tsa.dense_causal_attention(h.q[i], h.k[0], h.v[0])
+    for i in range(2):
+        ref = port.dense_causal_attention(up[0][i], up[1][0], up[2][0])
+        assert parity.rel_l2(host(out[i]), ref) <= parity.BF16_REL_L2
+
+
+def test_heavy_tailed_layer_bf16_vs_oracle(cuda, port):
+    from paper_2602_03216_b200 import workloads
+    L = 8192
+    q, k, v = workloads.heavy_tailed_heads(8, 2, L, 128, seed=9)
+    h = tsa.HeadTensors(q, k, v)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.01)
+    out, st = tsa.sparse_attention_layer(h, plan)
+    up = [host(t) for t in (q, k, v)]
+    idx = host(st.selection.indices).astype(np.int32)
+    ref = port.token_sparse_attention_sampled(up[0], up[1], up[2], idx, head_stride=3, r0=0,
+                                              r1=st.k_keep, n_threads=8)
+    o = host(out)
+    for hh in (0, 3, 6):
+        assert parity.rel_l2(o[hh], ref[hh]) <= parity.BF16_REL_L2
