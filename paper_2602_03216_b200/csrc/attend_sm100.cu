@@ -2,22 +2,30 @@
 //
 // dense_causal_attention (attention.cpp:25-40) -- the `inner` kernel the
 // reference applies to the compressed Q^/K^/V^ of each head -- for bf16 and
-// d = 128, one 128-row query tile per CTA:
+// d = 128.  One CTA owns a PAIR of 128-row query tiles (A = rows 256p..+127,
+// B = rows 256p+128..+255) so every K/V tile that lands in shared memory feeds
+// four MMAs, and the two softmax warpgroups ping-pong against the tensor core:
 //
-//   warp 0      TMA producer: Q tile once, then K/V tiles through an NS-stage ring
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T (SS, both K-major SW128)
-//               into TMEM buffer j%2, then O += P_{j-1} V_{j-1} (TS: P read
-//               from TMEM, V MN-major SW128) so that S_j runs while the softmax
-//               warps work on S_{j-1}
-//   warps 2..5  softmax: thread = query row = TMEM lane; tcgen05.ld the S row,
-//               causal mask on the diagonal tile, online softmax in the log2
-//               domain with lazy rescaling (O is only rescaled when the running
-//               max grows by more than 2^8), P written back as packed bf16 into
-//               the S columns (tcgen05.st); final O / l epilogue.
+//   warp 8        TMA producer: Q_A, Q_B once; K_j and V_j through 2-stage rings
+//   warp 9        MMA issuer (one thread), FA4-style order
+//                   S_A(0) S_B(0) | PV_A(0) S_A(1) PV_B(0) S_B(1) | PV_A(1) S_A(2) ...
+//                 so that while softmax(A, j+1) runs, the tensor core executes
+//                 PV_B(j) and S_B(j+1), and vice versa
+//   warps 0..3    softmax for tile A, warps 4..7 for tile B: thread = query row =
+//                 TMEM lane.  Two passes over the S row in TMEM (max, then
+//                 exp2 / sum / bf16 pack) keep registers low; P overwrites the
+//                 S columns (tcgen05.st) and is consumed by a TS-MMA.  Lazy
+//                 rescaling: O is rescaled only when the running max grows by
+//                 more than 2^8 (warp-uniform decision, tcgen05.ld/st are
+//                 warp-collective).  S(j) completing implies PV(j-1) completed
+//                 (tcgen05.commit tracks all prior MMAs), so the rescale needs
+//                 no extra barrier.  Epilogue: O / l -> bf16 -> global.
 //
-// TMEM (512 columns): S0 [0,128) S1 [128,256) O [256,384).
+// Warps 8..11 drop to 40 registers (setmaxnreg) so the softmax warpgroups can
+// hold a full 128-column S row in registers (232 each).
+// TMEM (512 columns): S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512).
 // n (rows per head) is read from device memory (k_keep): the grid is sized for
-// L and tiles past n exit before allocating anything.
+// L, pairs past n exit before allocating anything, heavy pairs go first.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -31,29 +39,153 @@ namespace {
 
 using namespace tsa_dev;
 
-constexpr int BM = 128;         // query rows per CTA
-constexpr int BN = 128;         // keys per KV tile
-constexpr int HD = 128;         // head dim
-constexpr int NS = 2;           // K/V pipeline stages
-constexpr int TILE_BYTES = BM * HD * 2;   // 32 KiB (two 64-col SW128 halves of 16 KiB)
+constexpr int BM = 128;                   // rows per query tile
+constexpr int BN = 128;                   // keys per KV tile
+constexpr int HD = 128;                   // head dim
+constexpr int NS = 2;                     // K and V ring stages
+constexpr int TILE_BYTES = BM * HD * 2;   // 32 KiB = two 64-column SW128 halves
 constexpr int HALF_BYTES = TILE_BYTES / 2;
 constexpr float kRescaleThreshold = 8.0f; // log2 units
+constexpr int kThreads = 384;             // 12 warps: 2 softmax WGs + producer WG
 
 struct __align__(1024) AttnSmem {
-    uint8_t q[TILE_BYTES];
+    uint8_t q[2][TILE_BYTES];
     uint8_t k[NS][TILE_BYTES];
     uint8_t v[NS][TILE_BYTES];
     uint64_t q_full;
-    uint64_t k_full[NS];
-    uint64_t v_full[NS];
-    uint64_t kv_empty[NS];
-    uint64_t s_full[2];
-    uint64_t p_full[2];
-    uint64_t o_done[2];
+    uint64_t k_full[NS], v_full[NS], k_empty[NS], v_empty[NS];
+    uint64_t s_full[2], p_full[2], o_done[2];
     uint32_t tmem_base;
 };
 
-__global__ void __launch_bounds__(192, 1)
+__device__ __forceinline__ void issue_s(uint32_t t_s, uint32_t q_base, uint32_t k_base,
+                                        uint32_t idesc) {
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
+        mma_bf16_ss(t_s, sdesc_kmajor_sw128(q_base + off), sdesc_kmajor_sw128(k_base + off), idesc,
+                    kk > 0 ? 1u : 0u);
+    }
+}
+
+__device__ __forceinline__ void issue_pv(uint32_t t_o, uint32_t t_p, uint32_t v_base,
+                                         uint32_t idesc, bool accumulate) {
+#pragma unroll
+    for (int kk = 0; kk < BN / 16; ++kk)
+        mma_bf16_ts(t_o, t_p + kk * 8, sdesc_mnmajor_sw128(v_base + kk * 2048, HALF_BYTES), idesc,
+                    (accumulate || kk > 0) ? 1u : 0u);
+}
+
+// Softmax / correction / epilogue for one 128-row query tile (tile 0 = A, 1 = B).
+__device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32_t warp,
+                                             uint32_t lane, int tA, int tB, bool hasB, int n,
+                                             int q_row0, float scale_log2,
+                                             __nv_bfloat16* __restrict__ o) {
+        const int tile = warp < 4 ? 0 : 1;  // warps 0..3 -> A, 4..7 -> B
+    if (tile == 0 || hasB) {
+        const int my_t = tile == 0 ? tA : tB;  // query tile index == its diagonal KV tile
+        const uint32_t sub = warp & 3;        // TMEM lane sub-partition
+        const int row = (int)(sub * 32 + lane);
+        const int qi = my_t * BM + row;
+        const uint32_t lane_off = (sub * 32) << 16;
+        const uint32_t t_s = tmem + (uint32_t)tile * 128 + lane_off;
+        const uint32_t t_o = tmem + 256 + (uint32_t)tile * 128 + lane_off;
+        float m_run = -INFINITY, l_run = 0.0f;
+        for (int j = 0; j <= my_t; ++j) {
+            mbar_wait(&sm.s_full[tile], j & 1);
+            tc_fence_after();
+            // the whole S row in registers: one TMEM pass, one wait
+            uint32_t r[BN];
+            tmem_ld32_at<0>(t_s + 0, r);
+            tmem_ld32_at<32>(t_s + 32, r);
+            tmem_ld32_at<64>(t_s + 64, r);
+            tmem_ld32_at<96>(t_s + 96, r);
+            tmem_wait_ld();
+            if (j == my_t) {  // diagonal tile (warp-uniform): causal mask c > qi - j*BN
+                const int lim = qi - j * BN;
+#pragma unroll
+                for (int c = 0; c < BN; ++c)
+                    if (c > lim) r[c] = __float_as_uint(-INFINITY);
+            }
+            // row max with 8 independent partial maxima (ILP)
+            float pm[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pm[e] = __uint_as_float(r[e]);
+#pragma unroll
+            for (int c = 8; c < BN; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(r[c]));
+            const float tmax = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                     fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) *
+                               scale_log2;
+            float m_use = m_run;
+            bool rescale = false;
+            if (tmax > m_run + kRescaleThreshold || m_run == -INFINITY) {
+                m_use = tmax;
+                rescale = (m_run != -INFINITY);
+            }
+            if (m_use == -INFINITY) m_use = 0.0f;  // fully masked row (rows >= n)
+            if (__any_sync(0xffffffffu, rescale)) {
+                // PV(j-1) is complete: S(j) was issued after it (commit semantics)
+                const float alpha = rescale ? ex2_approx(m_run - m_use) : 1.0f;
+#pragma unroll
+                for (int c0 = 0; c0 < HD; c0 += 32) {
+                    uint32_t ro[32];
+                    tmem_ld32(t_o + c0, ro);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        ro[e] = __float_as_uint(__uint_as_float(ro[e]) * alpha);
+                    tmem_st32(t_o + c0, ro);
+                }
+                if (rescale) l_run *= alpha;
+            }
+            m_run = m_use;
+            // P = 2^(x*scale - m), 8 partial row sums, packed bf16 into S columns [0, 64)
+            float ps[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) ps[e] = 0.0f;
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    const float p0 = ex2_approx(fmaf(__uint_as_float(r[c0 + e]), scale_log2, -m_use));
+                    const float p1 = ex2_approx(fmaf(__uint_as_float(r[c0 + e + 1]), scale_log2, -m_use));
+                    ps[(e >> 1) & 7] += p0 + p1;
+                    pk[e / 2] = pack_bf16x2(p0, p1);
+                }
+                tmem_st16(t_s + c0 / 2, pk);
+            }
+            l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&sm.p_full[tile]);
+        }
+        // epilogue: wait for the last PV, O / l -> bf16 -> global
+        mbar_wait(&sm.o_done[tile], my_t & 1);
+        tc_fence_after();
+        const float inv_l = 1.0f / l_run;
+        __nv_bfloat16* dst = o + ((size_t)q_row0 + tile * BM + row) * HD;
+#pragma unroll
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(t_o + c0, r);
+            tmem_wait_ld();
+            if (qi < n) {
+                uint4 outv[4];
+                uint32_t* ow = reinterpret_cast<uint32_t*>(outv);
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    ow[e] = pack_bf16x2(__uint_as_float(r[2 * e]) * inv_l,
+                                        __uint_as_float(r[2 * e + 1]) * inv_l);
+                uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) d4[e] = outv[e];
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
 attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ n_dev,
                     int n_const, int kv_group, int rows_per_head, int kv_rows_per_head,
@@ -65,11 +197,14 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const int h = head_begin + blockIdx.y;
     const int n = n_dev ? *n_dev : n_const;
     const int n_tiles = (n + BM - 1) / BM;
-    if ((int)blockIdx.x >= n_tiles) return;
-    const int mt = n_tiles - 1 - (int)blockIdx.x;  // longest causal rows first
-    const int nkv = mt + 1;                          // KV tiles 0..mt
+    const int n_pairs = (n_tiles + 1) / 2;
+    if ((int)blockIdx.x >= n_pairs) return;
+    const int p = n_pairs - 1 - (int)blockIdx.x;  // heaviest pairs first
+    const int tA = 2 * p, tB = 2 * p + 1;
+    const bool hasB = tB < n_tiles;
+    const int nkv = hasB ? tB + 1 : tA + 1;  // KV tiles 0..nkv-1
     const int kvh = h / kv_group;
-    const int q_row0 = h * rows_per_head + mt * BM;
+    const int q_row0 = h * rows_per_head + tA * BM;
     const int kv_row0 = kvh * kv_rows_per_head;
 
     const uint32_t warp = warp_id_uniform();
@@ -80,7 +215,8 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         for (int s = 0; s < NS; ++s) {
             mbar_init(&sm.k_full[s], 1);
             mbar_init(&sm.v_full[s], 1);
-            mbar_init(&sm.kv_empty[s], 1);
+            mbar_init(&sm.k_empty[s], 1);
+            mbar_init(&sm.v_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&sm.s_full[b], 1);
@@ -89,179 +225,106 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(&sm.tmem_base, 512);
+    if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
-    const uint32_t t_s[2] = {tmem, tmem + 128};
-    const uint32_t t_o = tmem + 256;
 
-    if (warp == 0) {
+    if (warp < 8) {
+        // ------------------------------------------------------ softmax warps
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+        softmax_role(sm, tmem, warp, lane, tA, tB, hasB, n, q_row0, scale_log2, o);
+        tc_fence_before();
+        named_bar_arrive(1, 288);  // teardown: 256 softmax threads + the MMA warp
+        return;
+    }
+    // producer warpgroup: hand registers to the softmax warpgroups
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == 8) {
         // ------------------------------------------------------ TMA producer
         if (lane == 0) {
-            tma_load_2d(sm.q, &tm_q, &sm.q_full, 0, q_row0);
-            tma_load_2d(sm.q + HALF_BYTES, &tm_q, &sm.q_full, 64, q_row0);
-            mbar_arrive_expect_tx(&sm.q_full, TILE_BYTES);
+            tma_load_2d(sm.q[0], &tm_q, &sm.q_full, 0, q_row0);
+            tma_load_2d(sm.q[0] + HALF_BYTES, &tm_q, &sm.q_full, 64, q_row0);
+            if (hasB) {
+                tma_load_2d(sm.q[1], &tm_q, &sm.q_full, 0, q_row0 + BM);
+                tma_load_2d(sm.q[1] + HALF_BYTES, &tm_q, &sm.q_full, 64, q_row0 + BM);
+            }
+            mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
             for (int j = 0; j < nkv; ++j) {
                 const int st = j % NS;
-                if (j >= NS) mbar_wait(&sm.kv_empty[st], ((j / NS) - 1) & 1);
                 const int r = kv_row0 + j * BN;
+                if (j >= NS) mbar_wait(&sm.k_empty[st], ((j / NS) - 1) & 1);
                 tma_load_2d(sm.k[st], &tm_k, &sm.k_full[st], 0, r);
                 tma_load_2d(sm.k[st] + HALF_BYTES, &tm_k, &sm.k_full[st], 64, r);
                 mbar_arrive_expect_tx(&sm.k_full[st], TILE_BYTES);
+                if (j >= NS) mbar_wait(&sm.v_empty[st], ((j / NS) - 1) & 1);
                 tma_load_2d(sm.v[st], &tm_v, &sm.v_full[st], 0, r);
                 tma_load_2d(sm.v[st] + HALF_BYTES, &tm_v, &sm.v_full[st], 64, r);
                 mbar_arrive_expect_tx(&sm.v_full[st], TILE_BYTES);
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 9) {
         // ------------------------------------------------------ MMA issuer
         if (lane == 0) {
             const uint32_t idesc_s = idesc_bf16_f32(BM, BN, 0, 0);
             const uint32_t idesc_o = idesc_bf16_f32(BM, HD, 0, 1);
-            const uint32_t q_base = smem_u32(sm.q);
+            const uint32_t qa = smem_u32(sm.q[0]), qb = smem_u32(sm.q[1]);
+            const uint32_t tS[2] = {tmem, tmem + 128};
+            const uint32_t tO[2] = {tmem + 256, tmem + 384};
+            auto doA = [&](int j) { return j <= tA; };
+            auto doB = [&](int j) { return hasB && j <= tB; };
             mbar_wait(&sm.q_full, 0);
+            // prologue: S(0) for both tiles
+            mbar_wait(&sm.k_full[0], 0);
             tc_fence_after();
-            auto issue_pv = [&](int j) {
-                const int st = j % NS, b = j & 1;
-                mbar_wait(&sm.p_full[b], (j >> 1) & 1);
-                mbar_wait(&sm.v_full[st], (j / NS) & 1);
-                tc_fence_after();
-                const uint32_t v_base = smem_u32(sm.v[st]);
-#pragma unroll
-                for (int kk = 0; kk < BN / 16; ++kk)
-                    mma_bf16_ts(t_o, t_s[b] + kk * 8, sdesc_mnmajor_sw128(v_base + kk * 2048, HALF_BYTES),
-                                idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-                mma_commit(&sm.o_done[b]);
-                mma_commit(&sm.kv_empty[st]);
-            };
+            issue_s(tS[0], qa, smem_u32(sm.k[0]), idesc_s);
+            mma_commit(&sm.s_full[0]);
+            if (hasB) {
+                issue_s(tS[1], qb, smem_u32(sm.k[0]), idesc_s);
+                mma_commit(&sm.s_full[1]);
+            }
+            mma_commit(&sm.k_empty[0]);
             for (int j = 0; j < nkv; ++j) {
-                const int st = j % NS, b = j & 1;
-                mbar_wait(&sm.k_full[st], (j / NS) & 1);
-                tc_fence_after();
-                const uint32_t k_base = smem_u32(sm.k[st]);
-#pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
-                    mma_bf16_ss(t_s[b], sdesc_kmajor_sw128(q_base + off),
-                                sdesc_kmajor_sw128(k_base + off), idesc_s, kk > 0 ? 1u : 0u);
+                const int st = j % NS;
+                const int j1 = j + 1, st1 = j1 % NS;
+                mbar_wait(&sm.v_full[st], (j / NS) & 1);
+                const uint32_t v_base = smem_u32(sm.v[st]);
+                const bool k1_needed = (j1 < nkv) && (doA(j1) || doB(j1));
+                if (doA(j)) {
+                    mbar_wait(&sm.p_full[0], j & 1);
+                    tc_fence_after();
+                    issue_pv(tO[0], tS[0], v_base, idesc_o, j > 0);
+                    mma_commit(&sm.o_done[0]);
+                    if (doA(j1)) {
+                        mbar_wait(&sm.k_full[st1], (j1 / NS) & 1);
+                        tc_fence_after();
+                        issue_s(tS[0], qa, smem_u32(sm.k[st1]), idesc_s);
+                        mma_commit(&sm.s_full[0]);
+                    }
                 }
-                mma_commit(&sm.s_full[b]);
-                if (j >= 1) issue_pv(j - 1);
-            }
-            issue_pv(nkv - 1);
-        }
-    } else {
-        // ------------------------------------------------------ softmax warps
-        const uint32_t sub = warp & 3;           // TMEM lane sub-partition of this warp
-        const int row = (int)(sub * 32 + lane);  // query row within the tile
-        const int qi = mt * BM + row;            // compressed row index
-        const uint32_t lane_off = (sub * 32) << 16;
-        float m_run = -INFINITY, l_run = 0.0f;
-        for (int j = 0; j < nkv; ++j) {
-            const int b = j & 1;
-            mbar_wait(&sm.s_full[b], (j >> 1) & 1);
-            tc_fence_after();
-            float s[BN];
-#pragma unroll
-            for (int c = 0; c < BN; c += 32) {
-                uint32_t r[32];
-                tmem_ld32(t_s[b] + lane_off + c, r);
-                tmem_wait_ld();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) s[c + e] = __uint_as_float(r[e]);
-            }
-            const bool diag = (j == mt);
-            float tmax = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < BN; ++c) {
-                float x = s[c] * scale_log2;
-                if (diag && (j * BN + c) > qi) x = -INFINITY;
-                s[c] = x;
-                tmax = fmaxf(tmax, x);
-            }
-            // lazy rescale: only move the reference max when it grows by > 2^8
-            float m_use = m_run;
-            bool rescale = false;
-            if (tmax > m_run + kRescaleThreshold || m_run == -INFINITY) {
-                m_use = tmax;
-                rescale = (j > 0) && (m_run != -INFINITY);
-            }
-            if (m_use == -INFINITY) m_use = 0.0f;  // fully masked row (rows >= n)
-            // P_j reuses S buffer b: P_{j-2} must have been consumed (PV_{j-2} done)
-            if (j >= 2) {
-                mbar_wait(&sm.o_done[b], ((j - 2) >> 1) & 1);
-            }
-            float lsum = 0.0f;
-            uint32_t packed[BN / 2];
-#pragma unroll
-            for (int c = 0; c < BN; c += 2) {
-                const float p0 = ex2_approx(s[c] - m_use);
-                const float p1 = ex2_approx(s[c + 1] - m_use);
-                lsum += p0 + p1;
-                packed[c / 2] = pack_bf16x2(p0, p1);
-            }
-            // tcgen05.ld/st are warp-collective (.sync.aligned): the whole warp
-            // rescales when any of its rows needs it (alpha = 1 for the others)
-            if (__any_sync(0xffffffffu, rescale)) {
-                // O must hold PV_{j-1} before it is rescaled
-                mbar_wait(&sm.o_done[b ^ 1], ((j - 1) >> 1) & 1);
-                tc_fence_after();
-                const float alpha = rescale ? ex2_approx(m_run - m_use) : 1.0f;
-#pragma unroll
-                for (int c = 0; c < HD; c += 32) {
-                    uint32_t r[32];
-                    tmem_ld32(t_o + lane_off + c, r);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-                    tmem_st32(t_o + lane_off + c, r);
+                if (doB(j)) {
+                    mbar_wait(&sm.p_full[1], j & 1);
+                    tc_fence_after();
+                    issue_pv(tO[1], tS[1], v_base, idesc_o, j > 0);
+                    mma_commit(&sm.o_done[1]);
+                    if (doB(j1)) {
+                        mbar_wait(&sm.k_full[st1], (j1 / NS) & 1);
+                        tc_fence_after();
+                        issue_s(tS[1], qb, smem_u32(sm.k[st1]), idesc_s);
+                        mma_commit(&sm.s_full[1]);
+                    }
                 }
-                if (rescale) l_run *= alpha;
+                if (k1_needed) mma_commit(&sm.k_empty[st1]);
+                mma_commit(&sm.v_empty[st]);
             }
-            l_run += lsum;
-            m_run = m_use;
-#pragma unroll
-            for (int c = 0; c < BN / 2; c += 32) {
-                uint32_t r[32];
-#pragma unroll
-                for (int e = 0; e < 32; ++e) r[e] = packed[c + e];
-                tmem_st32(t_s[b] + lane_off + c, r);
-            }
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&sm.p_full[b]);
         }
-        // epilogue: O / l -> bf16 -> global (thread writes its 256-B row)
-        const int jl = nkv - 1;
-        mbar_wait(&sm.o_done[jl & 1], (jl >> 1) & 1);
+        // teardown: wait for the softmax warps' last TMEM reads, then free TMEM
+        named_bar_sync(1, 288);
         tc_fence_after();
-        const float inv_l = 1.0f / l_run;
-        __nv_bfloat16* dst = o + ((size_t)q_row0 + row) * HD;
-#pragma unroll
-        for (int c = 0; c < HD; c += 32) {
-            uint32_t r[32];
-            tmem_ld32(t_o + lane_off + c, r);
-            tmem_wait_ld();
-            if (qi < n) {
-                uint4 outv[4];
-                uint32_t* ow = reinterpret_cast<uint32_t*>(outv);
-#pragma unroll
-                for (int e = 0; e < 16; ++e)
-                    ow[e] = pack_bf16x2(__uint_as_float(r[2 * e]) * inv_l,
-                                        __uint_as_float(r[2 * e + 1]) * inv_l);
-                uint4* d4 = reinterpret_cast<uint4*>(dst + c);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) d4[e] = outv[e];
-            }
-        }
+        tmem_dealloc(tmem, 512);
     }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 512);
 }
-
 // ------------------------------------------------------------------ host
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -316,11 +379,12 @@ int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const v
         cudaFuncSetAttribute(attend_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    dim3 grid((rows_per_head + BM - 1) / BM, nh);
+    const int max_tiles = (rows_per_head + BM - 1) / BM;
+    dim3 grid((max_tiles + 1) / 2, nh);
     const float scale_log2 = (1.0f / sqrtf((float)HD)) * 1.4426950408889634f;
-    attend_sm100_kernel<<<grid, 192, smem, st>>>(mq, mk, mv, n_dev, n_const, kv_group, rows_per_head,
-                                                 kv_rows_per_head, d.head_begin, scale_log2,
-                                                 (__nv_bfloat16*)o);
+    attend_sm100_kernel<<<grid, kThreads, smem, st>>>(mq, mk, mv, n_dev, n_const, kv_group,
+                                                      rows_per_head, kv_rows_per_head, d.head_begin,
+                                                      scale_log2, (__nv_bfloat16*)o);
     TSA_LAUNCH_CHECK("attend_sm100");
     return 0;
 }
