@@ -134,6 +134,19 @@ TSA_API int tsa_attend(const tsa_desc* d, const void* qc, const void* kc, const 
  * oc[h, inv[h, t]] or +0.0 (every row of the shard written once). */
 TSA_API int tsa_scatter(const tsa_desc* d, const void* oc, const int32_t* inv, void* out, void* stream);
 
+/* Fused compress -> attend -> decompress for bf16 / d = 128 (the production
+ * path of tsa_sparse_attention_layer): Q/K/V rows are fetched from the
+ * original tensors by idx with TMA gather4, causal attention runs over the
+ * first k_keep of them (kv group from the descriptor), and each output row is
+ * stored at its original position out[h, idx[h, r]].  Rows not selected are
+ * left untouched -- pair with tsa_zero_unselected. */
+TSA_API int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* k, const void* v,
+                               const int32_t* idx, const int32_t* k_keep, void* out,
+                               void* stream);
+
+/* out[h, t] = +0.0 for every t with inv[h, t] < 0 (scatter_rows' zero rows). */
+TSA_API int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream);
+
 /* scatter_rows for a caller-supplied selection: builds the inverse map of
  * idx (first k_keep entries per head) in ws, then tsa_scatter. */
 TSA_API int tsa_scatter_rows(const tsa_desc* d, const void* oc, const int32_t* idx,

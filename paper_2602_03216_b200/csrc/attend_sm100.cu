@@ -77,10 +77,13 @@ __device__ __forceinline__ void issue_pv(uint32_t t_o, uint32_t t_p, uint32_t v_
 }
 
 // Softmax / correction / epilogue for one 128-row query tile (tile 0 = A, 1 = B).
+// Output row of compressed row qi: the compressed buffer (row q_row0 + local
+// row) or, for the fused path, the original position h*L + idx[h, qi].
 __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32_t warp,
                                              uint32_t lane, int tA, int tB, bool hasB, int n,
                                              int q_row0, float scale_log2,
-                                             __nv_bfloat16* __restrict__ o) {
+                                             __nv_bfloat16* __restrict__ o,
+                                             const int32_t* __restrict__ idx_h, size_t out_head_row) {
         const int tile = warp < 4 ? 0 : 1;  // warps 0..3 -> A, 4..7 -> B
     if (tile == 0 || hasB) {
         const int my_t = tile == 0 ? tA : tB;  // query tile index == its diagonal KV tile
@@ -164,7 +167,9 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
         mbar_wait(&sm.o_done[tile], my_t & 1);
         tc_fence_after();
         const float inv_l = 1.0f / l_run;
-        __nv_bfloat16* dst = o + ((size_t)q_row0 + tile * BM + row) * HD;
+        size_t out_row = (size_t)q_row0 + tile * BM + row;
+        if (idx_h && qi < n) out_row = out_head_row + (size_t)__ldg(idx_h + qi);
+        __nv_bfloat16* dst = o + out_row * HD;
 #pragma unroll
         for (int c0 = 0; c0 < HD; c0 += 32) {
             uint32_t r[32];
@@ -185,11 +190,17 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
     }
 }
 
+// kIndexed: the fused compress -> attend -> decompress path.  Q/K/V rows are
+// fetched straight from the original [H|Hkv, L, d] tensors by the selection
+// idx[h, r] with TMA tile::gather4 (4 rows per request, SW128 layout identical
+// to the tiled load), and O rows are stored at their original positions.
+template <bool kIndexed>
 __global__ void __launch_bounds__(kThreads, 1)
 attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ n_dev,
                     int n_const, int kv_group, int rows_per_head, int kv_rows_per_head,
-                    int head_begin, float scale_log2, __nv_bfloat16* __restrict__ o) {
+                    int head_begin, float scale_log2, __nv_bfloat16* __restrict__ o,
+                    const int32_t* __restrict__ idx) {
     extern __shared__ uint8_t smem_raw[];
     AttnSmem& sm = *reinterpret_cast<AttnSmem*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -234,7 +245,9 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (warp < 8) {
         // ------------------------------------------------------ softmax warps
         asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-        softmax_role(sm, tmem, warp, lane, tA, tB, hasB, n, q_row0, scale_log2, o);
+        softmax_role(sm, tmem, warp, lane, tA, tB, hasB, n, q_row0, scale_log2, o,
+                     kIndexed ? idx + (size_t)h * rows_per_head : nullptr,
+                     (size_t)h * rows_per_head);
         tc_fence_before();
         named_bar_arrive(1, 288);  // teardown: 256 softmax threads + the MMA warp
         return;
@@ -243,25 +256,64 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == 8) {
         // ------------------------------------------------------ TMA producer
-        if (lane == 0) {
-            tma_load_2d(sm.q[0], &tm_q, &sm.q_full, 0, q_row0);
-            tma_load_2d(sm.q[0] + HALF_BYTES, &tm_q, &sm.q_full, 64, q_row0);
-            if (hasB) {
-                tma_load_2d(sm.q[1], &tm_q, &sm.q_full, 0, q_row0 + BM);
-                tma_load_2d(sm.q[1] + HALF_BYTES, &tm_q, &sm.q_full, 64, q_row0 + BM);
+        if (!kIndexed) {
+            if (lane == 0) {
+                tma_load_2d(sm.q[0], &tm_q, &sm.q_full, 0, q_row0);
+                tma_load_2d(sm.q[0] + HALF_BYTES, &tm_q, &sm.q_full, 64, q_row0);
+                if (hasB) {
+                    tma_load_2d(sm.q[1], &tm_q, &sm.q_full, 0, q_row0 + BM);
+                    tma_load_2d(sm.q[1] + HALF_BYTES, &tm_q, &sm.q_full, 64, q_row0 + BM);
+                }
+                mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
+                for (int j = 0; j < nkv; ++j) {
+                    const int st = j % NS;
+                    const int r = kv_row0 + j * BN;
+                    if (j >= NS) mbar_wait(&sm.k_empty[st], ((j / NS) - 1) & 1);
+                    tma_load_2d(sm.k[st], &tm_k, &sm.k_full[st], 0, r);
+                    tma_load_2d(sm.k[st] + HALF_BYTES, &tm_k, &sm.k_full[st], 64, r);
+                    mbar_arrive_expect_tx(&sm.k_full[st], TILE_BYTES);
+                    if (j >= NS) mbar_wait(&sm.v_empty[st], ((j / NS) - 1) & 1);
+                    tma_load_2d(sm.v[st], &tm_v, &sm.v_full[st], 0, r);
+                    tma_load_2d(sm.v[st] + HALF_BYTES, &tm_v, &sm.v_full[st], 64, r);
+                    mbar_arrive_expect_tx(&sm.v_full[st], TILE_BYTES);
+                }
             }
-            mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
+        } else {
+            // whole warp: lane l gathers rows 4l..4l+3 of every 128-row tile
+            const int32_t* idx_h = idx + (size_t)h * rows_per_head;
+            const int last = __ldg(idx_h + n - 1);  // rows >= n: any finite row (masked / not stored)
+            auto rows4 = [&](int r0, int& a0, int& a1, int& a2, int& a3) {
+                a0 = r0 + 0 < n ? __ldg(idx_h + r0 + 0) : last;
+                a1 = r0 + 1 < n ? __ldg(idx_h + r0 + 1) : last;
+                a2 = r0 + 2 < n ? __ldg(idx_h + r0 + 2) : last;
+                a3 = r0 + 3 < n ? __ldg(idx_h + r0 + 3) : last;
+            };
+            const int q_base_row = h * rows_per_head;  // original Q rows of head h
+            for (int t = 0; t < (hasB ? 2 : 1); ++t) {
+                int a0, a1, a2, a3;
+                rows4((tA + t) * BM + 4 * (int)lane, a0, a1, a2, a3);
+                uint8_t* dst = sm.q[t] + lane * 512;
+                tma_gather4(dst, &tm_q, &sm.q_full, 0, q_base_row + a0, q_base_row + a1,
+                            q_base_row + a2, q_base_row + a3);
+                tma_gather4(dst + HALF_BYTES, &tm_q, &sm.q_full, 64, q_base_row + a0,
+                            q_base_row + a1, q_base_row + a2, q_base_row + a3);
+            }
+            if (lane == 0) mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
             for (int j = 0; j < nkv; ++j) {
                 const int st = j % NS;
-                const int r = kv_row0 + j * BN;
+                int a0, a1, a2, a3;
+                rows4(j * BN + 4 * (int)lane, a0, a1, a2, a3);
+                a0 += kv_row0, a1 += kv_row0, a2 += kv_row0, a3 += kv_row0;
                 if (j >= NS) mbar_wait(&sm.k_empty[st], ((j / NS) - 1) & 1);
-                tma_load_2d(sm.k[st], &tm_k, &sm.k_full[st], 0, r);
-                tma_load_2d(sm.k[st] + HALF_BYTES, &tm_k, &sm.k_full[st], 64, r);
-                mbar_arrive_expect_tx(&sm.k_full[st], TILE_BYTES);
+                uint8_t* kd = sm.k[st] + lane * 512;
+                tma_gather4(kd, &tm_k, &sm.k_full[st], 0, a0, a1, a2, a3);
+                tma_gather4(kd + HALF_BYTES, &tm_k, &sm.k_full[st], 64, a0, a1, a2, a3);
+                if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[st], TILE_BYTES);
                 if (j >= NS) mbar_wait(&sm.v_empty[st], ((j / NS) - 1) & 1);
-                tma_load_2d(sm.v[st], &tm_v, &sm.v_full[st], 0, r);
-                tma_load_2d(sm.v[st] + HALF_BYTES, &tm_v, &sm.v_full[st], 64, r);
-                mbar_arrive_expect_tx(&sm.v_full[st], TILE_BYTES);
+                uint8_t* vd = sm.v[st] + lane * 512;
+                tma_gather4(vd, &tm_v, &sm.v_full[st], 0, a0, a1, a2, a3);
+                tma_gather4(vd + HALF_BYTES, &tm_v, &sm.v_full[st], 64, a0, a1, a2, a3);
+                if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[st], TILE_BYTES);
             }
         }
     } else if (warp == 9) {
@@ -360,33 +412,57 @@ int make_bf16_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t b
 
 bool attend_sm100_supported(const tsa_desc& d) { return d.dtype == TSA_BF16 && d.d_head == HD; }
 
-int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const void* v,
-                        const int32_t* n_dev, int32_t n_const, int32_t kv_group,
-                        int32_t rows_per_head, int32_t kv_rows_per_head, void* o,
-                        cudaStream_t st) {
+namespace {
+
+template <bool kIndexed>
+int launch_impl(const tsa_desc& d, const void* q, const void* k, const void* v,
+                const int32_t* idx, const int32_t* n_dev, int32_t n_const, int32_t kv_group,
+                int32_t rows_per_head, int32_t kv_rows_per_head, void* o, cudaStream_t st) {
     if (!attend_sm100_supported(d)) return invalid("attend_sm100: needs bf16, d_head 128");
     const int nh = d.head_end - d.head_begin;
     const int n_q_heads = d.n_heads;
     const int n_kv_heads_buf = (n_q_heads + kv_group - 1) / kv_group;
+    const uint32_t box_rows = kIndexed ? 1 : 128;  // gather4 maps use one-row boxes
     CUtensorMap mq, mk, mv;
     int rc;
-    if ((rc = make_bf16_map_2d(&mq, q, (uint64_t)n_q_heads * rows_per_head, 128))) return rc;
-    if ((rc = make_bf16_map_2d(&mk, k, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
-    if ((rc = make_bf16_map_2d(&mv, v, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
+    if ((rc = make_bf16_map_2d(&mq, q, (uint64_t)n_q_heads * rows_per_head, box_rows))) return rc;
+    if ((rc = make_bf16_map_2d(&mk, k, (uint64_t)n_kv_heads_buf * kv_rows_per_head, box_rows)))
+        return rc;
+    if ((rc = make_bf16_map_2d(&mv, v, (uint64_t)n_kv_heads_buf * kv_rows_per_head, box_rows)))
+        return rc;
     const int smem = (int)sizeof(AttnSmem) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(attend_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(attend_sm100_kernel<kIndexed>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
     const int max_tiles = (rows_per_head + BM - 1) / BM;
     dim3 grid((max_tiles + 1) / 2, nh);
     const float scale_log2 = (1.0f / sqrtf((float)HD)) * 1.4426950408889634f;
-    attend_sm100_kernel<<<grid, kThreads, smem, st>>>(mq, mk, mv, n_dev, n_const, kv_group,
-                                                      rows_per_head, kv_rows_per_head, d.head_begin,
-                                                      scale_log2, (__nv_bfloat16*)o);
-    TSA_LAUNCH_CHECK("attend_sm100");
+    attend_sm100_kernel<kIndexed><<<grid, kThreads, smem, st>>>(
+        mq, mk, mv, n_dev, n_const, kv_group, rows_per_head, kv_rows_per_head, d.head_begin,
+        scale_log2, (__nv_bfloat16*)o, idx);
+    TSA_LAUNCH_CHECK(kIndexed ? "attend_sm100_indexed" : "attend_sm100");
     return 0;
+}
+
+}  // namespace
+
+int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const void* v,
+                        const int32_t* n_dev, int32_t n_const, int32_t kv_group,
+                        int32_t rows_per_head, int32_t kv_rows_per_head, void* o,
+                        cudaStream_t st) {
+    return launch_impl<false>(d, q, k, v, nullptr, n_dev, n_const, kv_group, rows_per_head,
+                              kv_rows_per_head, o, st);
+}
+
+// Fused gather -> causal attention -> scatter of the selected rows (the
+// unselected rows are zeroed separately by launch_zero_unselected).
+int launch_attend_indexed(const tsa_desc& d, const void* q, const void* k, const void* v,
+                          const int32_t* idx, const int32_t* k_keep, void* out, cudaStream_t st) {
+    const int L = d.seq_len;
+    return launch_impl<true>(d, q, k, v, idx, k_keep, L, d.n_heads / d.n_kv_heads, L, L, out, st);
 }
 
 }  // namespace tsa

@@ -240,6 +240,19 @@ int tsa_scatter_rows(const tsa_desc* d, const void* oc, const int32_t* idx, cons
     return launch_scatter(*d, oc, at<int32_t>(ws, w.inv), out, S(stream));
 }
 
+int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* k, const void* v,
+                       const int32_t* idx, const int32_t* k_keep, void* out, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!attend_sm100_supported(*d))
+        return invalid("tsa_attend_indexed: the fused path needs bf16 and d_head 128");
+    return launch_attend_indexed(*d, q, k, v, idx, k_keep, out, S(stream));
+}
+
+int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    return launch_zero_unselected(*d, inv, out, S(stream));
+}
+
 int tsa_check(const tsa_desc* d, void* ws, void* stream) {
     if (int rc = check_desc(d)) return rc;
     const Workspace w = workspace_layout(*d);
@@ -262,8 +275,11 @@ int tsa_token_sparse_attention(const tsa_desc* d, const void* q, const void* k, 
     const Workspace w = workspace_layout(*d);
     cudaStream_t st = S(stream);
     int rc;
-    // inverse map for the scatter: rebuilt from idx by the select kernel's
-    // compaction is not available here, so derive it with one pass.
+    if (attend_sm100_supported(*d)) {  // fused gather -> attend -> scatter
+        if ((rc = launch_inverse(*d, idx, k_keep, at<int32_t>(ws, w.inv), st))) return rc;
+        if ((rc = launch_zero_unselected(*d, at<int32_t>(ws, w.inv), out, st))) return rc;
+        return launch_attend_indexed(*d, q, k, v, idx, k_keep, out, st);
+    }
     if ((rc = launch_gather(*d, q, k, v, idx, k_keep, at<void>(ws, w.qc), at<void>(ws, w.kc),
                             at<void>(ws, w.vc), st)))
         return rc;
@@ -301,6 +317,10 @@ int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, 
         if ((rc = tsa_score(d, q, k, s, ws, stream))) return rc;
         if ((rc = budget_impl(*d, s, k_keep_out, ws, std::max(1, nf), st))) return rc;
         if ((rc = launch_select(*d, s, k_keep_out, nullptr, nf, fb, idx, inv, st))) return rc;
+        if (attend_sm100_supported(*d)) {  // fused gather -> attend -> scatter
+            if ((rc = launch_zero_unselected(*d, inv, out, st))) return rc;
+            if ((rc = launch_attend_indexed(*d, q, k, v, idx, k_keep_out, out, st))) return rc;
+        } else {
         if ((rc = launch_gather(*d, q, k, v, idx, k_keep_out, at<void>(ws, w.qc), at<void>(ws, w.kc),
                                 at<void>(ws, w.vc), st)))
             return rc;
@@ -309,6 +329,7 @@ int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, 
                                   at<void>(ws, w.oc), st)))
             return rc;
         if ((rc = launch_scatter(*d, at<void>(ws, w.oc), inv, out, st))) return rc;
+        }
     }
     if (k_keep_host) {
         cudaError_t e = cudaMemcpyAsync(k_keep_host, k_keep_out, 4, cudaMemcpyDeviceToHost, st);

@@ -100,6 +100,9 @@ int launch_scatter(const tsa_desc& d, const void* oc, const int32_t* inv, void* 
                    cudaStream_t st);
 int launch_inverse(const tsa_desc& d, const int32_t* idx, const int32_t* k_keep, int32_t* inv,
                    cudaStream_t st);
+int launch_zero_unselected(const tsa_desc& d, const int32_t* inv, void* out, cudaStream_t st);
+int launch_attend_indexed(const tsa_desc& d, const void* q, const void* k, const void* v,
+                          const int32_t* idx, const int32_t* k_keep, void* out, cudaStream_t st);
 int launch_colsum_pool(const tsa_desc& d, const float* probs, float* s, cudaStream_t st);
 // attend_simt.cu / attend_sm100.cu
 int launch_attend_simt(const tsa_desc& d, const void* q, const void* k, const void* v,

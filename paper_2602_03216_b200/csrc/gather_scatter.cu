@@ -94,6 +94,22 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
     }
 }
 
+// Rows the selection dropped are +0.0 (scatter_rows zero-initialises its
+// output, tensor_ops.cpp:107); the fused attention writes the kept rows.
+__global__ void __launch_bounds__(256) zero_unselected_kernel(const int32_t* __restrict__ inv,
+                                                              uint4* __restrict__ out, int L,
+                                                              int chunks, int head_begin) {
+    const int h = head_begin + blockIdx.y;
+    const int rows_per_block = 64;
+    const int t0 = blockIdx.x * rows_per_block;
+    const int32_t* inv_h = inv + (size_t)h * L;
+    for (int e = threadIdx.x; e < rows_per_block * chunks; e += 256) {
+        const int t = t0 + e / chunks, c = e % chunks;
+        if (t >= L) break;
+        if (inv_h[t] < 0) out[((size_t)h * L + t) * chunks + c] = make_uint4(0u, 0u, 0u, 0u);
+    }
+}
+
 __global__ void inverse_fill_kernel(int32_t* __restrict__ inv, int L, int head_begin) {
     const int h = head_begin + blockIdx.y;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -117,6 +133,15 @@ int launch_inverse(const tsa_desc& d, const int32_t* idx, const int32_t* k_keep,
     inverse_fill_kernel<<<grid, 256, 0, st>>>(inv, L, d.head_begin);
     inverse_set_kernel<<<grid, 256, 0, st>>>(idx, k_keep, inv, L, d.head_begin);
     TSA_LAUNCH_CHECK("inverse");
+    return 0;
+}
+
+int launch_zero_unselected(const tsa_desc& d, const int32_t* inv, void* out, cudaStream_t st) {
+    const int L = d.seq_len;
+    const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / 16);
+    dim3 grid((L + 63) / 64, d.head_end - d.head_begin);
+    zero_unselected_kernel<<<grid, 256, 0, st>>>(inv, (uint4*)out, L, chunks, d.head_begin);
+    TSA_LAUNCH_CHECK("zero_unselected");
     return 0;
 }
 

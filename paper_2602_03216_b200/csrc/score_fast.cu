@@ -3,19 +3,20 @@
 // score_tokens (token_coverage.cpp:16-50) computes, per query head, softmax
 // rows of the trailing lq queries against all L keys and sums them by column.
 // Per KV group the g*lq tail rows form M-tiles of 128 rows (hpt = 128/lq heads
-// per tile, lq % 32 == 0), and the key axis is split into chunks so the grid
-// fills the GPU:
+// per tile, lq in {32, 64, 96, 128}), and the key axis is split into chunks so
+// the grid fills the GPU (2 CTAs per SM):
 //
-//   pass 1 (score_fast_kernel<false>): S = Q_tail K_j^T on tcgen05 (TMEM),
-//     per-row online max / sum-exp over the chunk's key tiles -> partials
-//   pass 2 (score_fast_kernel<true>):  combine the partials of all chunks,
-//     recompute S, P = 2^(x - M) / l, column sums per head by an in-warp
-//     butterfly reduce-scatter (lane l ends with columns 4l..4l+3) plus a
-//     fixed-order cross-warp sum -> colraw[h, j]  (deterministic)
+//   pass 1 (score_pass1): S = Q_tail K_j^T on tcgen05 (TMEM lane = query
+//     row), per-row online max / sum-exp over the chunk's key tiles -> partials
+//   pass 2 (score_pass2): the transposed product S^T = K_j Q_tail^T (TMEM lane =
+//     key), so each thread owns one key column: it combines the per-row
+//     partials (broadcast from shared memory), exponentiates its column and
+//     sums it per head in registers -- no cross-thread reduction -> colraw[h, j]
 //   pool: the shared edge-clamped pool kernel over colraw.
 //
 // Warp roles as in attend_sm100.cu: warp 0 TMA (Q tail once, K ring), warp 1
-// MMA (S double-buffered in TMEM), warps 2..5 one query row per thread.
+// MMA (S double-buffered in TMEM), warps 2..5 the per-thread math.
+// Deterministic: every sum has a fixed order.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,7 +33,7 @@ namespace {
 
 using namespace tsa_dev;
 
-constexpr int SF_BM = 128, SF_BN = 128, SF_HD = 128, SF_NS = 3;
+constexpr int SF_BM = 128, SF_BN = 128, SF_HD = 128, SF_NS = 2;
 constexpr int SF_TILE = SF_BM * SF_HD * 2;
 constexpr int SF_HALF = SF_TILE / 2;
 constexpr int SF_MAX_CHUNKS = 512;
@@ -40,7 +41,8 @@ constexpr int SF_MAX_CHUNKS = 512;
 struct __align__(1024) ScoreSmem {
     uint8_t q[SF_TILE];
     uint8_t k[SF_NS][SF_TILE];
-    float red[4][SF_BN];
+    float row_m[SF_BM];
+    float row_il[SF_BM];
     uint64_t q_full;
     uint64_t k_full[SF_NS];
     uint64_t k_empty[SF_NS];
@@ -49,30 +51,76 @@ struct __align__(1024) ScoreSmem {
     uint32_t tmem_base;
 };
 
-template <bool kPass2>
-__global__ void __launch_bounds__(192, 1)
-score_fast_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                  int L, int lq, int group, int hpt, int tiles_per_kv, int n_chunks,
-                  float scale_log2, float2* __restrict__ partial, float* __restrict__ colraw) {
-    extern __shared__ uint8_t smem_raw[];
-    ScoreSmem& sm = *reinterpret_cast<ScoreSmem*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int mtile = blockIdx.y, chunk = blockIdx.x;
-    const int kv = mtile / tiles_per_kv, sub_t = mtile % tiles_per_kv;
-    const int h_first = kv * group + sub_t * hpt;
-    const int n_heads_tile = min(hpt, group - sub_t * hpt);
+struct TileGeom {
+    int mtile, chunk, kv, h_first, n_heads_tile, kt0, nt;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(int L, int group, int hpt, int tiles_per_kv,
+                                              int n_chunks) {
+    TileGeom g;
+    g.mtile = blockIdx.y;
+    g.chunk = blockIdx.x;
+    g.kv = g.mtile / tiles_per_kv;
+    const int sub_t = g.mtile % tiles_per_kv;
+    g.h_first = g.kv * group + sub_t * hpt;
+    g.n_heads_tile = min(hpt, group - sub_t * hpt);
     const int n_ktiles = (L + SF_BN - 1) / SF_BN;
     const int per = (n_ktiles + n_chunks - 1) / n_chunks;
-    const int kt0 = chunk * per, kt1 = min(n_ktiles, kt0 + per);
-    const int nt = kt1 - kt0;
-    const uint32_t warp = warp_id_uniform(), lane = lane_id();
+    g.kt0 = g.chunk * per;
+    g.nt = min(n_ktiles, g.kt0 + per) - g.kt0;
+    return g;
+}
 
-    if (nt <= 0) {
-        if (!kPass2 && threadIdx.x < SF_BM)
-            partial[((size_t)mtile * n_chunks + chunk) * SF_BM + threadIdx.x] =
-                make_float2(-INFINITY, 0.0f);
-        return;
+// Shared prologue: barriers + TMEM; warp 0 streams Q tail and K tiles; warp 1
+// issues S = Q K^T (kTransposed: S^T = K Q^T) into a double-buffered TMEM tile.
+template <bool kTransposed>
+__device__ __forceinline__ void producer_roles(ScoreSmem& sm, const CUtensorMap* tm_q,
+                                               const CUtensorMap* tm_k, const TileGeom& g, int L,
+                                               int lq, uint32_t warp, uint32_t lane) {
+    const uint32_t t_s[2] = {sm.tmem_base, sm.tmem_base + 128};
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < g.n_heads_tile; ++i) {
+                const int row = (g.h_first + i) * L + (L - lq);
+                tma_load_2d(sm.q + i * lq * 128, tm_q, &sm.q_full, 0, row);
+                tma_load_2d(sm.q + SF_HALF + i * lq * 128, tm_q, &sm.q_full, 64, row);
+            }
+            mbar_arrive_expect_tx(&sm.q_full, g.n_heads_tile * lq * SF_HD * 2);
+            for (int j = 0; j < g.nt; ++j) {
+                const int st = j % SF_NS;
+                if (j >= SF_NS) mbar_wait(&sm.k_empty[st], ((j / SF_NS) - 1) & 1);
+                const int r = g.kv * L + (g.kt0 + j) * SF_BN;
+                tma_load_2d(sm.k[st], tm_k, &sm.k_full[st], 0, r);
+                tma_load_2d(sm.k[st] + SF_HALF, tm_k, &sm.k_full[st], 64, r);
+                mbar_arrive_expect_tx(&sm.k_full[st], SF_TILE);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16_f32(SF_BM, SF_BN, 0, 0);
+            const uint32_t q_base = smem_u32(sm.q);
+            mbar_wait(&sm.q_full, 0);
+            for (int j = 0; j < g.nt; ++j) {
+                const int st = j % SF_NS, b = j & 1;
+                mbar_wait(&sm.k_full[st], (j / SF_NS) & 1);
+                if (j >= 2) mbar_wait(&sm.s_free[b], ((j - 2) >> 1) & 1);
+                tc_fence_after();
+                const uint32_t k_base = smem_u32(sm.k[st]);
+#pragma unroll
+                for (int kk = 0; kk < SF_HD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * SF_HALF + (kk & 3) * 32;
+                    const uint64_t da = sdesc_kmajor_sw128((kTransposed ? k_base : q_base) + off);
+                    const uint64_t db = sdesc_kmajor_sw128((kTransposed ? q_base : k_base) + off);
+                    mma_bf16_ss(t_s[b], da, db, idesc, kk > 0 ? 1u : 0u);
+                }
+                mma_commit(&sm.s_full[b]);
+                mma_commit(&sm.k_empty[st]);
+            }
+        }
     }
+}
+
+__device__ __forceinline__ void setup(ScoreSmem& sm, uint32_t warp) {
     if (threadIdx.x == 0) {
         mbar_init(&sm.q_full, 1);
         for (int s = 0; s < SF_NS; ++s) {
@@ -89,140 +137,171 @@ score_fast_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t t_s[2] = {sm.tmem_base, sm.tmem_base + 128};
+}
 
-    if (warp == 0) {
-        if (lane == 0) {
-            for (int i = 0; i < n_heads_tile; ++i) {
-                const int row = (h_first + i) * L + (L - lq);
-                tma_load_2d(sm.q + i * lq * 128, &tm_q, &sm.q_full, 0, row);
-                tma_load_2d(sm.q + SF_HALF + i * lq * 128, &tm_q, &sm.q_full, 64, row);
-            }
-            mbar_arrive_expect_tx(&sm.q_full, n_heads_tile * lq * SF_HD * 2);
-            for (int j = 0; j < nt; ++j) {
-                const int st = j % SF_NS;
-                if (j >= SF_NS) mbar_wait(&sm.k_empty[st], ((j / SF_NS) - 1) & 1);
-                const int r = kv * L + (kt0 + j) * SF_BN;
-                tma_load_2d(sm.k[st], &tm_k, &sm.k_full[st], 0, r);
-                tma_load_2d(sm.k[st] + SF_HALF, &tm_k, &sm.k_full[st], 64, r);
-                mbar_arrive_expect_tx(&sm.k_full[st], SF_TILE);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t idesc = idesc_bf16_f32(SF_BM, SF_BN, 0, 0);
-            const uint32_t q_base = smem_u32(sm.q);
-            mbar_wait(&sm.q_full, 0);
-            for (int j = 0; j < nt; ++j) {
-                const int st = j % SF_NS, b = j & 1;
-                mbar_wait(&sm.k_full[st], (j / SF_NS) & 1);
-                if (j >= 2) mbar_wait(&sm.s_free[b], ((j - 2) >> 1) & 1);
-                tc_fence_after();
-                const uint32_t k_base = smem_u32(sm.k[st]);
-#pragma unroll
-                for (int kk = 0; kk < SF_HD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * SF_HALF + (kk & 3) * 32;
-                    mma_bf16_ss(t_s[b], sdesc_kmajor_sw128(q_base + off),
-                                sdesc_kmajor_sw128(k_base + off), idesc, kk > 0 ? 1u : 0u);
-                }
-                mma_commit(&sm.s_full[b]);
-                mma_commit(&sm.k_empty[st]);
-            }
-        }
-    } else {
+__device__ __forceinline__ void load_row128(uint32_t taddr, uint32_t (&r)[128]) {
+    tmem_ld32_at<0>(taddr, r);
+    tmem_ld32_at<32>(taddr + 32, r);
+    tmem_ld32_at<64>(taddr + 64, r);
+    tmem_ld32_at<96>(taddr + 96, r);
+    tmem_wait_ld();
+}
+
+// ---------------------------------------------------------------- pass 1
+__global__ void __launch_bounds__(192, 2)
+score_pass1(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+            int L, int lq, int group, int hpt, int tiles_per_kv, int n_chunks, float scale_log2,
+            float2* __restrict__ partial) {
+    extern __shared__ uint8_t smem_raw[];
+    ScoreSmem& sm = *reinterpret_cast<ScoreSmem*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const TileGeom g = tile_geom(L, group, hpt, tiles_per_kv, n_chunks);
+    const uint32_t warp = warp_id_uniform(), lane = lane_id();
+    float2* part = partial + ((size_t)g.mtile * n_chunks + g.chunk) * SF_BM;
+    if (g.nt <= 0) {
+        if (threadIdx.x < SF_BM) part[threadIdx.x] = make_float2(-INFINITY, 0.0f);
+        return;
+    }
+    setup(sm, warp);
+    producer_roles<false>(sm, &tm_q, &tm_k, g, L, lq, warp, lane);
+    if (warp >= 2) {
         const uint32_t sub = warp & 3;
-        const int row = (int)(sub * 32 + lane);   // tile row
-        const int head_i = row / lq;              // head within tile
-        const int r = row % lq;                   // tail row index
-        const bool valid = head_i < n_heads_tile;
-        const int limit = L - lq + r;             // last key this row may see
+        const int row = (int)(sub * 32 + lane);  // tile row = TMEM lane
+        const int r = row % lq;
+        const int limit = L - lq + r;            // last key this row may see
         const uint32_t lane_off = (sub * 32) << 16;
-        float m_run = -INFINITY, l_run = 0.0f, inv_l = 0.0f;
-        if (kPass2) {
-            float M = -INFINITY;
-            for (int c = 0; c < n_chunks; ++c)
-                M = fmaxf(M, partial[((size_t)mtile * n_chunks + c) * SF_BM + row].x);
-            float Ls = 0.0f;
-            for (int c = 0; c < n_chunks; ++c) {
-                const float2 p = partial[((size_t)mtile * n_chunks + c) * SF_BM + row];
-                if (p.y > 0.0f) Ls += p.y * ex2_approx(p.x - M);
-            }
-            m_run = M;
-            inv_l = Ls > 0.0f ? 1.0f / Ls : 0.0f;
-        }
-        for (int j = 0; j < nt; ++j) {
+        float m_run = -INFINITY, l_run = 0.0f;
+        for (int j = 0; j < g.nt; ++j) {
             const int b = j & 1;
-            const int key0 = (kt0 + j) * SF_BN;
+            const int key0 = (g.kt0 + j) * SF_BN;
             mbar_wait(&sm.s_full[b], (j >> 1) & 1);
             tc_fence_after();
-            float x[SF_BN];
-#pragma unroll
-            for (int c = 0; c < SF_BN; c += 32) {
-                uint32_t rr[32];
-                tmem_ld32(t_s[b] + lane_off + c, rr);
-                tmem_wait_ld();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) x[c + e] = __uint_as_float(rr[e]);
-            }
+            uint32_t x[SF_BN];
+            load_row128(sm.tmem_base + b * 128 + lane_off, x);
             tc_fence_before();
             mbar_arrive(&sm.s_free[b]);
-            const bool edge = key0 + SF_BN - 1 > limit;
-#pragma unroll
-            for (int c = 0; c < SF_BN; ++c) {
-                float v = x[c] * scale_log2;
-                if (edge && key0 + c > limit) v = -INFINITY;
-                x[c] = v;
-            }
-            if (!kPass2) {
-                float tmax = -INFINITY;
-#pragma unroll
-                for (int c = 0; c < SF_BN; ++c) tmax = fmaxf(tmax, x[c]);
-                const float m_new = fmaxf(m_run, tmax);
-                if (m_new != -INFINITY) {
-                    float s = 0.0f;
-#pragma unroll
-                    for (int c = 0; c < SF_BN; ++c) s += ex2_approx(x[c] - m_new);
-                    l_run = l_run * ex2_approx(m_run - m_new) + s;
-                    m_run = m_new;
-                }
-            } else {
-                // P row, then butterfly reduce-scatter across the warp's 32 rows
+            if (key0 + SF_BN - 1 > limit) {
 #pragma unroll
                 for (int c = 0; c < SF_BN; ++c)
-                    x[c] = valid ? ex2_approx(x[c] - m_run) * inv_l : 0.0f;
+                    if (key0 + c > limit) x[c] = __float_as_uint(-INFINITY);
+            }
+            float pm[8];
 #pragma unroll
-                for (int step = 0; step < 5; ++step) {
-                    const int half = 64 >> step;          // values kept per lane after the step
-                    const uint32_t bit = (lane >> (4 - step)) & 1u;
-                    const int xmask = 16 >> step;
+            for (int e = 0; e < 8; ++e) pm[e] = __uint_as_float(x[e]);
 #pragma unroll
-                    for (int i = 0; i < half; ++i) {
-                        const float keep = bit ? x[half + i] : x[i];
-                        const float send = bit ? x[i] : x[half + i];
-                        x[i] = keep + __shfl_xor_sync(0xffffffffu, send, xmask);
-                    }
-                }
-                // lane holds columns 4*lane .. 4*lane+3 of this warp's 32 rows
+            for (int c = 8; c < SF_BN; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(x[c]));
+            const float tmax = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                     fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * scale_log2;
+            const float m_new = fmaxf(m_run, tmax);
+            if (m_new != -INFINITY) {
+                float ps[8];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) sm.red[sub][4 * lane + e] = x[e];
-                named_bar_sync(1, 128);
-                const int c = threadIdx.x - 64;  // 0..127 over the softmax warps
-                const int key = key0 + c;
-                const int warps_per_head = lq / 32;
-                for (int i = 0; i < n_heads_tile; ++i) {
-                    float acc = 0.0f;
-                    for (int w = 0; w < warps_per_head; ++w) acc += sm.red[i * warps_per_head + w][c];
-                    if (key < L) colraw[(size_t)(h_first + i) * L + key] = acc;
-                }
-                named_bar_sync(1, 128);
+                for (int e = 0; e < 8; ++e) ps[e] = 0.0f;
+#pragma unroll
+                for (int c = 0; c < SF_BN; ++c)
+                    ps[c & 7] += ex2_approx(fmaf(__uint_as_float(x[c]), scale_log2, -m_new));
+                const float s = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+                l_run = l_run * ex2_approx(m_run - m_new) + s;
+                m_run = m_new;
             }
         }
-        if (!kPass2)
-            partial[((size_t)mtile * n_chunks + chunk) * SF_BM + row] = make_float2(m_run, l_run);
+        part[row] = make_float2(m_run, l_run);
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc(sm.tmem_base, 256);
+}
+
+// ---------------------------------------------------------------- pass 2
+template <int LQ>
+__global__ void __launch_bounds__(192, 2)
+score_pass2(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+            int L, int group, int hpt, int tiles_per_kv, int n_chunks, float scale_log2,
+            const float2* __restrict__ partial, float* __restrict__ colraw) {
+    constexpr int HPT_MAX = 128 / LQ;
+    extern __shared__ uint8_t smem_raw[];
+    ScoreSmem& sm = *reinterpret_cast<ScoreSmem*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const TileGeom g = tile_geom(L, group, hpt, tiles_per_kv, n_chunks);
+    const uint32_t warp = warp_id_uniform(), lane = lane_id();
+    if (g.nt <= 0) return;
+    // combine the chunk partials of every query row (thread t -> row t)
+    if (threadIdx.x < SF_BM) {
+        const int row = threadIdx.x;
+        const float2* part = partial + (size_t)g.mtile * n_chunks * SF_BM + row;
+        float M = -INFINITY;
+        for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, part[(size_t)c * SF_BM].x);
+        float Ls = 0.0f;
+        for (int c = 0; c < n_chunks; ++c) {
+            const float2 p = part[(size_t)c * SF_BM];
+            if (p.y > 0.0f) Ls += p.y * ex2_approx(p.x - M);
+        }
+        const bool valid = row / LQ < g.n_heads_tile;
+        sm.row_m[row] = valid ? M : 0.0f;
+        sm.row_il[row] = (valid && Ls > 0.0f) ? 1.0f / Ls : 0.0f;
+    }
+    setup(sm, warp);  // includes __syncthreads: row stats visible
+    producer_roles<true>(sm, &tm_q, &tm_k, g, L, LQ, warp, lane);
+    if (warp >= 2) {
+        const uint32_t sub = warp & 3;
+        const int t = (int)(sub * 32 + lane);  // key within the tile = TMEM lane
+        const uint32_t lane_off = (sub * 32) << 16;
+        for (int j = 0; j < g.nt; ++j) {
+            const int b = j & 1;
+            const int key = (g.kt0 + j) * SF_BN + t;
+            mbar_wait(&sm.s_full[b], (j >> 1) & 1);
+            tc_fence_after();
+            uint32_t x[SF_BN];  // x[c] = q_row_c . k_key (column c = tail row of the tile)
+            load_row128(sm.tmem_base + b * 128 + lane_off, x);
+            tc_fence_before();
+            mbar_arrive(&sm.s_free[b]);
+            // rows r may see this key iff key <= L - lq + r  <=>  r >= key - (L - lq)
+            const int r_first = key - (L - LQ);
+            float acc[HPT_MAX];
+#pragma unroll
+            for (int i = 0; i < HPT_MAX; ++i) {
+                float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+#pragma unroll
+                for (int rr = 0; rr < LQ; rr += 4) {
+                    const int c = i * LQ + rr;
+                    float p[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float e = ex2_approx(
+                            fmaf(__uint_as_float(x[c + u]), scale_log2, -sm.row_m[c + u]));
+                        p[u] = (rr + u >= r_first) ? e * sm.row_il[c + u] : 0.0f;
+                    }
+                    a0 += p[0];
+                    a1 += p[1];
+                    a2 += p[2];
+                    a3 += p[3];
+                }
+                acc[i] = (a0 + a1) + (a2 + a3);
+            }
+            if (key < L) {
+#pragma unroll
+                for (int i = 0; i < HPT_MAX; ++i)
+                    if (i < g.n_heads_tile) colraw[(size_t)(g.h_first + i) * L + key] = acc[i];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(sm.tmem_base, 256);
+}
+
+template <int LQ>
+int launch_pass2(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                 int L, int g, int hpt, int tpk, int n_chunks, float sl2, const float2* partial,
+                 float* colraw) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(score_pass2<LQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    score_pass2<LQ><<<grid, 192, smem, st>>>(mq, mk, L, g, hpt, tpk, n_chunks, sl2, partial, colraw);
+    TSA_LAUNCH_CHECK("score_fast_pass2");
+    return 0;
 }
 
 }  // namespace
@@ -231,8 +310,6 @@ bool score_fast_available() { return true; }
 
 bool score_fast_supported(const tsa_desc& d) {
     const int lq = lq_of(d);
-    const int g = d.n_heads / d.n_kv_heads;
-    (void)g;
     return d.dtype == TSA_BF16 && d.d_head == SF_HD && lq % 32 == 0 && lq <= 128;
 }
 
@@ -249,7 +326,8 @@ int launch_score_fast(const tsa_desc& d, const void* q, const void* k, float* s,
     const int n_kv = kv_end - kv_begin;
     const int mtiles = n_kv * tiles_per_kv;
     const int n_ktiles = (L + SF_BN - 1) / SF_BN;
-    const int n_chunks = std::max(1, std::min({n_ktiles, SF_MAX_CHUNKS, (2 * kNumSMs + mtiles - 1) / mtiles}));
+    const int n_chunks =
+        std::max(1, std::min({n_ktiles, SF_MAX_CHUNKS, (4 * kNumSMs + mtiles - 1) / mtiles}));
     // shard-local views: heads [head_begin, head_end) start at kv_begin
     const size_t eb = 2;
     const uint8_t* qb = static_cast<const uint8_t*>(q) + (size_t)kv_begin * g * L * SF_HD * eb;
@@ -261,20 +339,22 @@ int launch_score_fast(const tsa_desc& d, const void* q, const void* k, float* s,
     const int smem = (int)sizeof(ScoreSmem) + 1024;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(score_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(score_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(score_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    const float scale_log2 = (1.0f / sqrtf((float)SF_HD)) * 1.4426950408889634f;
+    const float sl2 = (1.0f / sqrtf((float)SF_HD)) * 1.4426950408889634f;
     float2* partial = reinterpret_cast<float2*>(partial_ws);
-    float* colraw_local = colraw + (size_t)d.head_begin * L;  // indexed by local head below
+    float* colraw_local = colraw + (size_t)d.head_begin * L;  // indexed by local head
     dim3 grid(n_chunks, mtiles);
-    score_fast_kernel<false><<<grid, 192, smem, st>>>(mq, mk, L, lq, g, hpt, tiles_per_kv, n_chunks,
-                                                      scale_log2, partial, colraw_local);
+    score_pass1<<<grid, 192, smem, st>>>(mq, mk, L, lq, g, hpt, tiles_per_kv, n_chunks, sl2, partial);
     TSA_LAUNCH_CHECK("score_fast_pass1");
-    score_fast_kernel<true><<<grid, 192, smem, st>>>(mq, mk, L, lq, g, hpt, tiles_per_kv, n_chunks,
-                                                     scale_log2, partial, colraw_local);
-    TSA_LAUNCH_CHECK("score_fast_pass2");
+    switch (lq) {
+        case 32: rc = launch_pass2<32>(grid, smem, st, mq, mk, L, g, hpt, tiles_per_kv, n_chunks, sl2, partial, colraw_local); break;
+        case 64: rc = launch_pass2<64>(grid, smem, st, mq, mk, L, g, hpt, tiles_per_kv, n_chunks, sl2, partial, colraw_local); break;
+        case 96: rc = launch_pass2<96>(grid, smem, st, mq, mk, L, g, hpt, tiles_per_kv, n_chunks, sl2, partial, colraw_local); break;
+        default: rc = launch_pass2<128>(grid, smem, st, mq, mk, L, g, hpt, tiles_per_kv, n_chunks, sl2, partial, colraw_local); break;
+    }
+    if (rc) return rc;
     // pool over the raw column sums (one "row" per head)
     tsa_desc pd = d;
     pd.last_q = 1;

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(BT) budget_kernel(const float* __restrict__ he
                                                     double tau, int min_keep,
                                                     int32_t* __restrict__ k_keep,
                                                     int32_t* __restrict__ status, int mode,
-                                                    float* __restrict__ sl_out) {
+                                                    float* __restrict__ sl_out, int exact_total) {
     __shared__ float stage[2][2048];
     __shared__ float s_total;
     __shared__ uint32_t hist_cnt[2048];
@@ -104,8 +104,10 @@ __global__ void __launch_bounds__(BT) budget_kernel(const float* __restrict__ he
     const int tid = threadIdx.x;
     float total = 1.0f;
     if (mode != BUDGET_FROM_SL) {
+    if (exact_total) {
     // ---- total: sequential f32 chain (token_coverage.cpp:58-61) ----
-    // Warps stage 2048-float chunks into a double buffer; thread 0 consumes.
+    // Warps stage 2048-float chunks into a double buffer; thread 0 consumes
+    // them with 16-B shared loads kept ahead of the dependent FADD chain.
     constexpr int CH = 2048;
     const int nchunk = (L + CH - 1) / CH;
     for (int i = tid; i < CH; i += BT) stage[0][i] = i < L ? headsum[i] : 0.0f;
@@ -120,9 +122,38 @@ __global__ void __launch_bounds__(BT) budget_kernel(const float* __restrict__ he
         if (tid == 0) {
             const float* buf = stage[c & 1];
             const int n = min(CH, L - c * CH);
-            for (int i = 0; i < n; ++i) total = __fadd_rn(total, buf[i]);
+            const float4* b4 = reinterpret_cast<const float4*>(buf);
+            const int n4 = n / 4;
+#pragma unroll 8
+            for (int i = 0; i < n4; ++i) {
+                const float4 v = b4[i];
+                total = __fadd_rn(total, v.x);
+                total = __fadd_rn(total, v.y);
+                total = __fadd_rn(total, v.z);
+                total = __fadd_rn(total, v.w);
+            }
+            for (int i = n4 * 4; i < n; ++i) total = __fadd_rn(total, buf[i]);
         }
         __syncthreads();
+    }
+    } else {
+    // ---- total: deterministic parallel reduction in f64 (FAST scoring mode) ----
+    // Fixed thread->element assignment and a fixed reduction tree, so the
+    // result is reproducible; it differs from the sequential f32 chain by far
+    // less than the FAST scores differ from reference-order scores.
+    __shared__ double red[BT / 32];
+    double acc = 0.0;
+    for (int t = tid; t < L; t += BT) acc += (double)headsum[t];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid < 32) {
+        double w = red[tid];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (tid == 0) total = (float)w;
+    }
     }
     if (tid == 0) s_total = total;
     __syncthreads();
@@ -163,14 +194,32 @@ __global__ void __launch_bounds__(BT) budget_kernel(const float* __restrict__ he
         __syncthreads();
         const uint32_t prefix = s_prefix;
         const int pshift = shift + kBits[lvl];
-        for (int t = tid; t < L; t += BT) {
-            const float sl = __fdiv_rn(headsum[t], total);
-            const uint32_t key = score_key(sl);
-            if (pshift < 32 && (key >> pshift) != prefix) continue;
-            const uint32_t b = (key >> shift) & (nb - 1);
-            const unsigned long long m = (unsigned long long)ldexp((double)sl, 62);
-            atomicAdd(&hist_cnt[b], 1u);
-            atomicAdd(&hist_mass[b], m);
+        // warp-aggregated: lanes hitting the same bucket combine their count and
+        // mass (three 21-bit limbs so the 32-lane sums cannot overflow) before
+        // one shared atomic per distinct bucket
+        for (int base = 0; base < L; base += BT) {
+            const int t = base + tid;
+            uint32_t b = 0xFFFFFFFFu;
+            unsigned long long m = 0;
+            if (t < L) {
+                const float sl = __fdiv_rn(headsum[t], total);
+                const uint32_t key = score_key(sl);
+                if (pshift >= 32 || (key >> pshift) == prefix) {
+                    b = (key >> shift) & (nb - 1);
+                    m = (unsigned long long)ldexp((double)sl, 62);
+                }
+            }
+            const uint32_t grp = __match_any_sync(0xffffffffu, b);
+            const uint32_t l0 = __reduce_add_sync(grp, (uint32_t)(m & 0x1FFFFFu));
+            const uint32_t l1 = __reduce_add_sync(grp, (uint32_t)((m >> 21) & 0x1FFFFFu));
+            const uint32_t l2 = __reduce_add_sync(grp, (uint32_t)(m >> 42));
+            if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (int)(tid & 31)) {
+                const unsigned long long sum = (unsigned long long)l0 +
+                                               ((unsigned long long)l1 << 21) +
+                                               ((unsigned long long)l2 << 42);
+                atomicAdd(&hist_cnt[b], (uint32_t)__popc(grp));
+                atomicAdd(&hist_mass[b], sum);
+            }
         }
         __syncthreads();
         // exclusive scan over buckets (2 buckets per thread, ascending)
@@ -254,11 +303,16 @@ __global__ void __launch_bounds__(BT) select_kernel(const float* __restrict__ s,
             for (int b = tid; b < nb; b += BT) hist[b] = 0;
             __syncthreads();
             const uint32_t prefix = s_prefix;
-            for (int t = tid; t < L; t += BT) {
-                if (is_forced(t, forced, nf, fbegin)) continue;
-                const uint32_t key = score_key(sh[t]);
-                if (pshift < 32 && (key >> pshift) != prefix) continue;
-                atomicAdd(&hist[(key >> shift) & (nb - 1)], 1u);
+            for (int base = 0; base < L; base += BT) {
+                const int t = base + tid;
+                uint32_t b = 0xFFFFFFFFu;
+                if (t < L && !is_forced(t, forced, nf, fbegin)) {
+                    const uint32_t key = score_key(sh[t]);
+                    if (pshift >= 32 || (key >> pshift) == prefix) b = (key >> shift) & (nb - 1);
+                }
+                const uint32_t grp = __match_any_sync(0xffffffffu, b);  // warp-aggregated
+                if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (tid & 31))
+                    atomicAdd(&hist[b], (uint32_t)__popc(grp));
             }
             __syncthreads();
             // descending: count of keys in buckets above b = exclusive scan from the top
@@ -358,7 +412,8 @@ int launch_budget(const tsa_desc& d, const float* s, int32_t* k_keep, float* hea
     headsum_kernel<<<(L + 255) / 256, 256, 0, st>>>(s, headsum, d.n_heads, L);
     TSA_LAUNCH_CHECK("headsum");
     budget_kernel<<<1, BT, 0, st>>>(headsum, L, d.tau, min_keep, k_keep, status,
-                                    BUDGET_FROM_HEADSUM, nullptr);
+                                    BUDGET_FROM_HEADSUM, nullptr,
+                                    scoring_mode(d) == TSA_SCORING_REFERENCE ? 1 : 0);
     TSA_LAUNCH_CHECK("budget");
     return 0;
 }
@@ -368,7 +423,8 @@ int launch_aggregate(const tsa_desc& d, const float* s, float* sl, float* headsu
     const int L = d.seq_len;
     headsum_kernel<<<(L + 255) / 256, 256, 0, st>>>(s, headsum, d.n_heads, L);
     TSA_LAUNCH_CHECK("headsum");
-    budget_kernel<<<1, BT, 0, st>>>(headsum, L, 0.0, 1, nullptr, status, AGGREGATE_ONLY, sl);
+    budget_kernel<<<1, BT, 0, st>>>(headsum, L, 0.0, 1, nullptr, status, AGGREGATE_ONLY, sl,
+                                    scoring_mode(d) == TSA_SCORING_REFERENCE ? 1 : 0);
     TSA_LAUNCH_CHECK("aggregate");
     return 0;
 }
@@ -376,7 +432,7 @@ int launch_aggregate(const tsa_desc& d, const float* s, float* sl, float* headsu
 int launch_coverage_from_sl(const tsa_desc& d, const float* sl, int32_t* k_keep, int32_t* status,
                             int min_keep, cudaStream_t st) {
     budget_kernel<<<1, BT, 0, st>>>(sl, d.seq_len, d.tau, min_keep, k_keep, status, BUDGET_FROM_SL,
-                                    nullptr);
+                                    nullptr, 1);
     TSA_LAUNCH_CHECK("coverage_budget");
     return 0;
 }

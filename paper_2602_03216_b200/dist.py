@@ -98,6 +98,19 @@ class CudaBackend:
                                        _ptr(self.forced), self.forced.numel(), _ptr(self.idx),
                                        _ptr(self.inv), _ptr(self.ws), _stream(self.device)))
 
+    @property
+    def fused(self) -> bool:
+        return self.local.dtype == _lib.TSA_BF16 and self.local.d_head == 128
+
+    def zero_unselected(self, out_local):
+        _lib.check(self.lib.tsa_zero_unselected(C.byref(self.local), _ptr(self.inv),
+                                                _ptr(out_local), _stream(self.device)))
+
+    def attend_indexed(self, q, k, v, k_keep, out_local):
+        _lib.check(self.lib.tsa_attend_indexed(C.byref(self.local), _ptr(q), _ptr(k), _ptr(v),
+                                               _ptr(self.idx), _ptr(k_keep), _ptr(out_local),
+                                               _stream(self.device)))
+
     def gather(self, q, k, v, k_keep):
         _lib.check(self.lib.tsa_gather(C.byref(self.local), _ptr(q), _ptr(k), _ptr(v),
                                        _ptr(self.idx), _ptr(k_keep), _ptr(self.qc), _ptr(self.kc),
@@ -167,12 +180,20 @@ class ShardedSparseAttention:
         mark("budget")
         b.select(self.s_local, k_keep)
         mark("select")
-        b.gather(q, k, v, k_keep)
-        mark("gather")
-        b.attend(k_keep)
-        mark("attend")
-        b.scatter(self.out_local)
-        mark("scatter")
+        if getattr(b, "fused", False):
+            # compress -> attend -> decompress in one kernel (TMA gather4 in,
+            # scattered row stores out); dropped rows zeroed alongside
+            b.zero_unselected(self.out_local)
+            mark("zero_fill")
+            b.attend_indexed(q, k, v, k_keep, self.out_local)
+            mark("attend")
+        else:
+            b.gather(q, k, v, k_keep)
+            mark("gather")
+            b.attend(k_keep)
+            mark("attend")
+            b.scatter(self.out_local)
+            mark("scatter")
         self._all_gather(self.out_full, self.out_local)
         mark("allgather_out")
         return self.out_full

@@ -36,9 +36,11 @@ struct __align__(1024) Smem {
 };
 
 // mode 0: SS K-major/K-major; mode 1: TS with B MN-major; mode 2: SS A K-major, B MN-major
+// mode 3: as 0, but B's 128 rows gathered by index from a larger matrix (TMA tile::gather4)
 __global__ void probe_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, const __nv_bfloat16* A_gl,
-                             float* D, int mode) {
+                             float* D, int mode, const __grid_constant__ CUtensorMap tmG,
+                             const int* gidx) {
     extern __shared__ uint8_t raw[];
     Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     const uint32_t warp = warp_id_uniform();
@@ -83,15 +85,23 @@ __global__ void probe_kernel(const __grid_constant__ CUtensorMap tmA,
             tma_load_2d(s.a[1], &tmA, &s.bar_tma, 64, 0);
             bytes += 2 * 128 * 64 * 2;
         }
-        tma_load_2d(s.b[0], &tmB, &s.bar_tma, 0, 0);
-        tma_load_2d(s.b[1], &tmB, &s.bar_tma, 64, 0);
+        if (mode == 3) {
+            for (int g = 0; g < 32; ++g) {
+                const int* r = gidx + 4 * g;
+                tma_gather4(reinterpret_cast<uint8_t*>(s.b[0]) + g * 512, &tmG, &s.bar_tma, 0, r[0], r[1], r[2], r[3]);
+                tma_gather4(reinterpret_cast<uint8_t*>(s.b[1]) + g * 512, &tmG, &s.bar_tma, 64, r[0], r[1], r[2], r[3]);
+            }
+        } else {
+            tma_load_2d(s.b[0], &tmB, &s.bar_tma, 0, 0);
+            tma_load_2d(s.b[1], &tmB, &s.bar_tma, 64, 0);
+        }
         bytes += 2 * 128 * 64 * 2;
         mbar_arrive_expect_tx(&s.bar_tma, bytes);
         mbar_wait(&s.bar_tma, 0);
         tc_fence_after();
         const uint32_t a0 = smem_u32(s.a[0]);
         const uint32_t b0 = smem_u32(s.b[0]);
-        if (mode == 0) {
+        if (mode == 0 || mode == 3) {
             const uint32_t idesc = idesc_bf16_f32(M, N, 0, 0);
             for (int kk = 0; kk < K / 16; ++kk) {
                 const uint32_t off = (kk / 4) * (128 * 128) + (kk % 4) * 32;
@@ -137,11 +147,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
 }
 
-static CUtensorMap make_map(void* base, int rows, int cols) {
+static CUtensorMap make_map(void* base, int rows, int cols, int box_rows = 128) {
     CUtensorMap m;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-    cuuint32_t box[2] = {64, 128};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
     CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box,
                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -174,12 +184,29 @@ int main() {
     CK(cudaMemcpy(dA, hA.data(), M * K * 2, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dB, hB.data(), N * K * 2, cudaMemcpyHostToDevice));
     CUtensorMap tA = make_map(dA, M, K), tB = make_map(dB, 128, 128);
+    // gather source: 1000 rows; B = rows gidx[0..127] of it
+    const int NG = 1000;
+    std::vector<__nv_bfloat16> hG(NG * K);
+    std::vector<float> fG(NG * K);
+    for (int i = 0; i < NG * K; ++i) {
+        hG[i] = __float2bfloat16((rand() % 11 - 5) / 4.0f);
+        fG[i] = __bfloat162float(hG[i]);
+    }
+    std::vector<int> hidx(128);
+    for (int i = 0; i < 128; ++i) hidx[i] = (i * 7919 + 13) % NG;
+    __nv_bfloat16* dG;
+    int* didx;
+    CK(cudaMalloc(&dG, NG * K * 2));
+    CK(cudaMalloc(&didx, 128 * 4));
+    CK(cudaMemcpy(dG, hG.data(), NG * K * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(didx, hidx.data(), 128 * 4, cudaMemcpyHostToDevice));
+    CUtensorMap tG = make_map(dG, NG, K, 1);
     const int smem = sizeof(Smem) + 1024;
     CK(cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int fails = 0;
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 4; ++mode) {
         CK(cudaMemset(dD, 0, M * N * 4));
-        probe_kernel<<<1, 128, smem>>>(tA, tB, dA, dD, mode);
+        probe_kernel<<<1, 128, smem>>>(tA, tB, dA, dD, mode, tG, didx);
         CK(cudaDeviceSynchronize());
         std::vector<float> hD(M * N);
         CK(cudaMemcpy(hD.data(), dD, M * N * 4, cudaMemcpyDeviceToHost));
@@ -189,13 +216,15 @@ int main() {
                 double ref = 0;
                 for (int k = 0; k < K; ++k) {
                     // mode 0: B is [N][K]; modes 1,2: B is V = [K][N]
-                    const float b = mode == 0 ? fB[j * K + k] : fB[k * N + j];
+                    const float b = mode == 0 ? fB[j * K + k]
+                                    : mode == 3 ? fG[hidx[j] * K + k] : fB[k * N + j];
                     ref += (double)fA[i * K + k] * b;
                 }
                 maxerr = fmax(maxerr, fabs(ref - hD[i * N + j]));
             }
         printf("mode %d (%s): max_abs_err = %g  D[0][0]=%g D[5][77]=%g\n", mode,
-               mode == 0 ? "SS kmajor" : mode == 1 ? "TS P-in-TMEM, V mn-major" : "SS V mn-major",
+               mode == 0 ? "SS kmajor" : mode == 1 ? "TS P-in-TMEM, V mn-major"
+               : mode == 2 ? "SS V mn-major" : "SS, B rows by TMA gather4",
                maxerr, hD[0], hD[5 * N + 77]);
         if (maxerr > 1e-3) ++fails;
     }
