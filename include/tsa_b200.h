@@ -118,7 +118,8 @@ TSA_API int tsa_select(const tsa_desc* d, const float* s, const int32_t* k_keep,
 
 /* gather_rows x3 (tensor_ops.cpp:92-99 via attention.cpp:93-95): qc/kc/vc
  * are [H x L x d] with the first k_keep rows of each head valid (K/V rows
- * come from the head's KV group, duplicated per query head). */
+ * come from the head's KV group, duplicated per query head).  qc may be NULL
+ * (K/V only, for tsa_attend_indexed). */
 TSA_API int tsa_gather(const tsa_desc* d, const void* q, const void* k, const void* v,
                const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
                void* stream);
@@ -134,13 +135,13 @@ TSA_API int tsa_attend(const tsa_desc* d, const void* qc, const void* kc, const 
  * oc[h, inv[h, t]] or +0.0 (every row of the shard written once). */
 TSA_API int tsa_scatter(const tsa_desc* d, const void* oc, const int32_t* inv, void* out, void* stream);
 
-/* Fused compress -> attend -> decompress for bf16 / d = 128 (the production
- * path of tsa_sparse_attention_layer): Q/K/V rows are fetched from the
- * original tensors by idx with TMA gather4, causal attention runs over the
- * first k_keep of them (kv group from the descriptor), and each output row is
- * stored at its original position out[h, idx[h, r]].  Rows not selected are
- * left untouched -- pair with tsa_zero_unselected. */
-TSA_API int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* k, const void* v,
+/* Fused attend + decompress for bf16 / d = 128 (the production path of
+ * tsa_sparse_attention_layer): Q rows are fetched from the original q by idx
+ * with TMA gather4, K/V tiles from the compressed per-head kc/vc (tsa_gather
+ * with qc = NULL), causal attention runs over the first k_keep rows, and each
+ * output row is stored at its original position out[h, idx[h, r]].  Rows not
+ * selected are left untouched -- pair with tsa_zero_unselected. */
+TSA_API int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* kc, const void* vc,
                                const int32_t* idx, const int32_t* k_keep, void* out,
                                void* stream);
 

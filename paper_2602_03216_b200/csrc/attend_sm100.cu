@@ -190,10 +190,13 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
     }
 }
 
-// kIndexed: the fused compress -> attend -> decompress path.  Q/K/V rows are
-// fetched straight from the original [H|Hkv, L, d] tensors by the selection
+// kIndexed: the fused compress -> attend -> decompress path.  Q rows are
+// fetched straight from the original [H, L, d] tensor by the selection
 // idx[h, r] with TMA tile::gather4 (4 rows per request, SW128 layout identical
-// to the tiled load), and O rows are stored at their original positions.
+// to the tiled load; once per CTA), K/V tiles stream from the compressed
+// per-head buffers, and O rows are stored at their original positions.
+// (Gathering K/V with gather4 as well costs 128 TMA requests per KV step and
+// measured 2.3x slower on B200; see profiles/r1/README.md.)
 template <bool kIndexed>
 __global__ void __launch_bounds__(kThreads, 1)
 attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -299,21 +302,21 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             q_base_row + a1, q_base_row + a2, q_base_row + a3);
             }
             if (lane == 0) mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
-            for (int j = 0; j < nkv; ++j) {
-                const int st = j % NS;
-                int a0, a1, a2, a3;
-                rows4(j * BN + 4 * (int)lane, a0, a1, a2, a3);
-                a0 += kv_row0, a1 += kv_row0, a2 += kv_row0, a3 += kv_row0;
-                if (j >= NS) mbar_wait(&sm.k_empty[st], ((j / NS) - 1) & 1);
-                uint8_t* kd = sm.k[st] + lane * 512;
-                tma_gather4(kd, &tm_k, &sm.k_full[st], 0, a0, a1, a2, a3);
-                tma_gather4(kd + HALF_BYTES, &tm_k, &sm.k_full[st], 64, a0, a1, a2, a3);
-                if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[st], TILE_BYTES);
-                if (j >= NS) mbar_wait(&sm.v_empty[st], ((j / NS) - 1) & 1);
-                uint8_t* vd = sm.v[st] + lane * 512;
-                tma_gather4(vd, &tm_v, &sm.v_full[st], 0, a0, a1, a2, a3);
-                tma_gather4(vd + HALF_BYTES, &tm_v, &sm.v_full[st], 64, a0, a1, a2, a3);
-                if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[st], TILE_BYTES);
+            // K/V: tiled loads of the compressed per-head buffers (kc/vc from the
+            // gather kernel) -- 4 TMA requests per KV step instead of 128 gathers
+            if (lane == 0) {
+                for (int j = 0; j < nkv; ++j) {
+                    const int st = j % NS;
+                    const int r = kv_row0 + j * BN;
+                    if (j >= NS) mbar_wait(&sm.k_empty[st], ((j / NS) - 1) & 1);
+                    tma_load_2d(sm.k[st], &tm_k, &sm.k_full[st], 0, r);
+                    tma_load_2d(sm.k[st] + HALF_BYTES, &tm_k, &sm.k_full[st], 64, r);
+                    mbar_arrive_expect_tx(&sm.k_full[st], TILE_BYTES);
+                    if (j >= NS) mbar_wait(&sm.v_empty[st], ((j / NS) - 1) & 1);
+                    tma_load_2d(sm.v[st], &tm_v, &sm.v_full[st], 0, r);
+                    tma_load_2d(sm.v[st] + HALF_BYTES, &tm_v, &sm.v_full[st], 64, r);
+                    mbar_arrive_expect_tx(&sm.v_full[st], TILE_BYTES);
+                }
             }
         }
     } else if (warp == 9) {
@@ -422,14 +425,13 @@ int launch_impl(const tsa_desc& d, const void* q, const void* k, const void* v,
     const int nh = d.head_end - d.head_begin;
     const int n_q_heads = d.n_heads;
     const int n_kv_heads_buf = (n_q_heads + kv_group - 1) / kv_group;
-    const uint32_t box_rows = kIndexed ? 1 : 128;  // gather4 maps use one-row boxes
     CUtensorMap mq, mk, mv;
     int rc;
-    if ((rc = make_bf16_map_2d(&mq, q, (uint64_t)n_q_heads * rows_per_head, box_rows))) return rc;
-    if ((rc = make_bf16_map_2d(&mk, k, (uint64_t)n_kv_heads_buf * kv_rows_per_head, box_rows)))
+    // the gather4 Q map uses one-row boxes
+    if ((rc = make_bf16_map_2d(&mq, q, (uint64_t)n_q_heads * rows_per_head, kIndexed ? 1 : 128)))
         return rc;
-    if ((rc = make_bf16_map_2d(&mv, v, (uint64_t)n_kv_heads_buf * kv_rows_per_head, box_rows)))
-        return rc;
+    if ((rc = make_bf16_map_2d(&mk, k, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
+    if ((rc = make_bf16_map_2d(&mv, v, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
     const int smem = (int)sizeof(AttnSmem) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
@@ -459,10 +461,10 @@ int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const v
 
 // Fused gather -> causal attention -> scatter of the selected rows (the
 // unselected rows are zeroed separately by launch_zero_unselected).
-int launch_attend_indexed(const tsa_desc& d, const void* q, const void* k, const void* v,
+int launch_attend_indexed(const tsa_desc& d, const void* q, const void* kc, const void* vc,
                           const int32_t* idx, const int32_t* k_keep, void* out, cudaStream_t st) {
     const int L = d.seq_len;
-    return launch_impl<true>(d, q, k, v, idx, k_keep, L, d.n_heads / d.n_kv_heads, L, L, out, st);
+    return launch_impl<true>(d, q, kc, vc, idx, k_keep, L, 1, L, L, out, st);
 }
 
 }  // namespace tsa

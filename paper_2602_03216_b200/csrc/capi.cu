@@ -216,6 +216,7 @@ int tsa_select(const tsa_desc* d, const float* s, const int32_t* k_keep, const i
 int tsa_gather(const tsa_desc* d, const void* q, const void* k, const void* v, const int32_t* idx,
                const int32_t* k_keep, void* qc, void* kc, void* vc, void* stream) {
     if (int rc = check_desc(d)) return rc;
+    if (!kc || !vc) return invalid("gather_rows: kc and vc are required (qc may be NULL)");
     return launch_gather(*d, q, k, v, idx, k_keep, qc, kc, vc, S(stream));
 }
 
@@ -240,12 +241,12 @@ int tsa_scatter_rows(const tsa_desc* d, const void* oc, const int32_t* idx, cons
     return launch_scatter(*d, oc, at<int32_t>(ws, w.inv), out, S(stream));
 }
 
-int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* k, const void* v,
+int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* kc, const void* vc,
                        const int32_t* idx, const int32_t* k_keep, void* out, void* stream) {
     if (int rc = check_desc(d)) return rc;
     if (!attend_sm100_supported(*d))
         return invalid("tsa_attend_indexed: the fused path needs bf16 and d_head 128");
-    return launch_attend_indexed(*d, q, k, v, idx, k_keep, out, S(stream));
+    return launch_attend_indexed(*d, q, kc, vc, idx, k_keep, out, S(stream));
 }
 
 int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream) {
@@ -278,7 +279,11 @@ int tsa_token_sparse_attention(const tsa_desc* d, const void* q, const void* k, 
     if (attend_sm100_supported(*d)) {  // fused gather -> attend -> scatter
         if ((rc = launch_inverse(*d, idx, k_keep, at<int32_t>(ws, w.inv), st))) return rc;
         if ((rc = launch_zero_unselected(*d, at<int32_t>(ws, w.inv), out, st))) return rc;
-        return launch_attend_indexed(*d, q, k, v, idx, k_keep, out, st);
+        if ((rc = launch_gather(*d, q, k, v, idx, k_keep, nullptr, at<void>(ws, w.kc),
+                                at<void>(ws, w.vc), st)))
+            return rc;
+        return launch_attend_indexed(*d, q, at<void>(ws, w.kc), at<void>(ws, w.vc), idx, k_keep,
+                                     out, st);
     }
     if ((rc = launch_gather(*d, q, k, v, idx, k_keep, at<void>(ws, w.qc), at<void>(ws, w.kc),
                             at<void>(ws, w.vc), st)))
@@ -317,9 +322,14 @@ int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, 
         if ((rc = tsa_score(d, q, k, s, ws, stream))) return rc;
         if ((rc = budget_impl(*d, s, k_keep_out, ws, std::max(1, nf), st))) return rc;
         if ((rc = launch_select(*d, s, k_keep_out, nullptr, nf, fb, idx, inv, st))) return rc;
-        if (attend_sm100_supported(*d)) {  // fused gather -> attend -> scatter
+        if (attend_sm100_supported(*d)) {  // K/V gather, then fused Q-gather/attend/scatter
             if ((rc = launch_zero_unselected(*d, inv, out, st))) return rc;
-            if ((rc = launch_attend_indexed(*d, q, k, v, idx, k_keep_out, out, st))) return rc;
+            if ((rc = launch_gather(*d, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
+                                    at<void>(ws, w.vc), st)))
+                return rc;
+            if ((rc = launch_attend_indexed(*d, q, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
+                                            k_keep_out, out, st)))
+                return rc;
         } else {
         if ((rc = launch_gather(*d, q, k, v, idx, k_keep_out, at<void>(ws, w.qc), at<void>(ws, w.kc),
                                 at<void>(ws, w.vc), st)))

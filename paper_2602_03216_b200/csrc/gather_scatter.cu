@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ q
             if (r >= pad_end) break;
             const size_t dst = ((size_t)h * L + r) * chunks;
             for (int c = lane; c < chunks; c += 32) {
-                qc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+                if (qc) qc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
                 kc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
                 vc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
             }
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ q
         if (r >= n) {
             const size_t dst = ((size_t)h * L + r) * chunks;
             for (int c = lane; c < chunks; c += 32) {
-                qc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+                if (qc) qc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
                 kc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
                 vc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
             }
@@ -64,13 +64,22 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ q
         const size_t src_q = ((size_t)h * L + t) * chunks;
         const size_t src_kv = ((size_t)kv * L + t) * chunks;
         const size_t dst = ((size_t)h * L + r) * chunks;
-        for (int c = lane; c < chunks; c += 32) {
-            const uint4 a = __ldg(q + src_q + c);
-            const uint4 b = __ldg(k + src_kv + c);
-            const uint4 e = __ldg(v + src_kv + c);
-            qc[dst + c] = a;
-            kc[dst + c] = b;
-            vc[dst + c] = e;
+        if (qc) {
+            for (int c = lane; c < chunks; c += 32) {
+                const uint4 a = __ldg(q + src_q + c);
+                const uint4 b = __ldg(k + src_kv + c);
+                const uint4 e = __ldg(v + src_kv + c);
+                qc[dst + c] = a;
+                kc[dst + c] = b;
+                vc[dst + c] = e;
+            }
+        } else {  // K/V only (the fused attention gathers Q itself)
+            for (int c = lane; c < chunks; c += 32) {
+                const uint4 b = __ldg(k + src_kv + c);
+                const uint4 e = __ldg(v + src_kv + c);
+                kc[dst + c] = b;
+                vc[dst + c] = e;
+            }
         }
     }
 }

@@ -106,10 +106,15 @@ class CudaBackend:
         _lib.check(self.lib.tsa_zero_unselected(C.byref(self.local), _ptr(self.inv),
                                                 _ptr(out_local), _stream(self.device)))
 
-    def attend_indexed(self, q, k, v, k_keep, out_local):
-        _lib.check(self.lib.tsa_attend_indexed(C.byref(self.local), _ptr(q), _ptr(k), _ptr(v),
-                                               _ptr(self.idx), _ptr(k_keep), _ptr(out_local),
-                                               _stream(self.device)))
+    def gather_kv(self, k, v, k_keep):
+        _lib.check(self.lib.tsa_gather(C.byref(self.local), None, _ptr(k), _ptr(v),
+                                       _ptr(self.idx), _ptr(k_keep), None, _ptr(self.kc),
+                                       _ptr(self.vc), _stream(self.device)))
+
+    def attend_indexed(self, q, k_keep, out_local):
+        _lib.check(self.lib.tsa_attend_indexed(C.byref(self.local), _ptr(q), _ptr(self.kc),
+                                               _ptr(self.vc), _ptr(self.idx), _ptr(k_keep),
+                                               _ptr(out_local), _stream(self.device)))
 
     def gather(self, q, k, v, k_keep):
         _lib.check(self.lib.tsa_gather(C.byref(self.local), _ptr(q), _ptr(k), _ptr(v),
@@ -181,11 +186,13 @@ class ShardedSparseAttention:
         b.select(self.s_local, k_keep)
         mark("select")
         if getattr(b, "fused", False):
-            # compress -> attend -> decompress in one kernel (TMA gather4 in,
-            # scattered row stores out); dropped rows zeroed alongside
+            # K/V compress, then attend with Q gathered by TMA gather4 and the
+            # output rows stored at their original positions; dropped rows zeroed
             b.zero_unselected(self.out_local)
             mark("zero_fill")
-            b.attend_indexed(q, k, v, k_keep, self.out_local)
+            b.gather_kv(k, v, k_keep)
+            mark("gather")
+            b.attend_indexed(q, k_keep, self.out_local)
             mark("attend")
         else:
             b.gather(q, k, v, k_keep)
