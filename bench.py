@@ -238,17 +238,22 @@ def run_ours(args):
     # roofline of the dominant kernel (attend): algorithmic flops / event time
     attend_ms = stages.get("attend")
     achieved = f_attn(k_keep, D, sh.h_per) / (attend_ms * 1e-3) / 1e12 if attend_ms else None
-    roofline = {"kernel": "attend_sm100 (tcgen05 causal flash attention)", "bound": "tensor",
+    roofline = {"kernel": "attend_sm100_kernel<indexed> (tcgen05 causal flash attention, fused "
+                          "Q gather + scattered output)", "bound": "tensor",
                 "achieved": round(achieved, 1) if achieved else None, "peak": pk_sust,
                 "unit": "TFLOP/s", "frac": round(achieved / pk_sust, 4) if achieved else None,
                 "peak_kind": f"{pk_kind} sustained bf16 (kernel timed inside a long step)",
                 "frac_of_burst": round(achieved / pk_burst, 4) if achieved else None,
                 "traffic": profile_traffic("attend")}
-    # HBM roofline for the data-movement stages
+    # HBM roofline for the data-movement stages (algorithmic bytes)
     b = 2
     hbm_rows = {}
     for name, nbytes in (
-            ("gather", 6 * sh.h_per * k_keep * D * b + 4 * sh.h_per * k_keep),
+            # K/V rows of the KV head per query head: read + write compressed, + idx
+            ("gather", 4 * sh.h_per * k_keep * D * b + 4 * sh.h_per * k_keep),
+            # zero rows the selection dropped + read the inverse map
+            ("zero_fill", sh.h_per * (L - k_keep) * D * b + 4 * sh.h_per * L),
+            # unfused path only
             ("scatter", sh.h_per * (k_keep + L) * D * b + 4 * sh.h_per * L)):
         if stages.get(name):
             gbs = nbytes / (stages[name] * 1e-3) / 1e9

@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -54,12 +55,22 @@ struct __align__(1024) AttnSmem {
     uint8_t v[NS][TILE_BYTES];
     uint64_t q_full;
     uint64_t k_full[NS], v_full[NS], k_empty[NS], v_empty[NS];
-    uint64_t s_full[2], p_full[2], o_done[2];
+    uint64_t s_full[2], p_full[2][2], o_done[2];  // p_full[tile][half]
     uint32_t tmem_base;
 };
 
+// The issuing warp runs with 40 registers (setmaxnreg): launder the smem base
+// so the compiler recomputes the cheap descriptors instead of hoisting 16
+// loop-invariant 64-bit values (which spilled).
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(x));
+    return x;
+}
+
 __device__ __forceinline__ void issue_s(uint32_t t_s, uint32_t q_base, uint32_t k_base,
                                         uint32_t idesc) {
+    q_base = opaque(q_base);
+    k_base = opaque(k_base);
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
         const uint32_t off = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
@@ -68,12 +79,16 @@ __device__ __forceinline__ void issue_s(uint32_t t_s, uint32_t q_base, uint32_t 
     }
 }
 
-__device__ __forceinline__ void issue_pv(uint32_t t_o, uint32_t t_p, uint32_t v_base,
-                                         uint32_t idesc, bool accumulate) {
+// O += P[:, 64h .. 64h+63] V[64h .. 64h+63, :] (half h of the 128-key tile).
+__device__ __forceinline__ void issue_pv_half(uint32_t t_o, uint32_t t_p, uint32_t v_base,
+                                              uint32_t idesc, bool accumulate, int half) {
+    v_base = opaque(v_base);
 #pragma unroll
-    for (int kk = 0; kk < BN / 16; ++kk)
+    for (int k2 = 0; k2 < BN / 32; ++k2) {
+        const int kk = half * (BN / 32) + k2;
         mma_bf16_ts(t_o, t_p + kk * 8, sdesc_mnmajor_sw128(v_base + kk * 2048, HALF_BYTES), idesc,
                     (accumulate || kk > 0) ? 1u : 0u);
+    }
 }
 
 // Softmax / correction / epilogue for one 128-row query tile (tile 0 = A, 1 = B).
@@ -157,11 +172,15 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
                     pk[e / 2] = pack_bf16x2(p0, p1);
                 }
                 tmem_st16(t_s + c0 / 2, pk);
+                if (c0 == 32 || c0 == 96) {
+                    // release P in two 64-key halves: PV on keys 0..63 overlaps
+                    // the exponentials of keys 64..127
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(&sm.p_full[tile][c0 == 96]);
+                }
             }
             l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&sm.p_full[tile]);
         }
         // epilogue: wait for the last PV, O / l -> bf16 -> global
         mbar_wait(&sm.o_done[tile], my_t & 1);
@@ -234,7 +253,8 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&sm.s_full[b], 1);
-            mbar_init(&sm.p_full[b], 128);
+            mbar_init(&sm.p_full[b][0], 128);
+            mbar_init(&sm.p_full[b][1], 128);
             mbar_init(&sm.o_done[b], 1);
         }
         fence_barrier_init();
@@ -347,9 +367,12 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const uint32_t v_base = smem_u32(sm.v[st]);
                 const bool k1_needed = (j1 < nkv) && (doA(j1) || doB(j1));
                 if (doA(j)) {
-                    mbar_wait(&sm.p_full[0], j & 1);
+                    mbar_wait(&sm.p_full[0][0], j & 1);
                     tc_fence_after();
-                    issue_pv(tO[0], tS[0], v_base, idesc_o, j > 0);
+                    issue_pv_half(tO[0], tS[0], v_base, idesc_o, j > 0, 0);
+                    mbar_wait(&sm.p_full[0][1], j & 1);
+                    tc_fence_after();
+                    issue_pv_half(tO[0], tS[0], v_base, idesc_o, j > 0, 1);
                     mma_commit(&sm.o_done[0]);
                     if (doA(j1)) {
                         mbar_wait(&sm.k_full[st1], (j1 / NS) & 1);
@@ -359,9 +382,12 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                 }
                 if (doB(j)) {
-                    mbar_wait(&sm.p_full[1], j & 1);
+                    mbar_wait(&sm.p_full[1][0], j & 1);
                     tc_fence_after();
-                    issue_pv(tO[1], tS[1], v_base, idesc_o, j > 0);
+                    issue_pv_half(tO[1], tS[1], v_base, idesc_o, j > 0, 0);
+                    mbar_wait(&sm.p_full[1][1], j & 1);
+                    tc_fence_after();
+                    issue_pv_half(tO[1], tS[1], v_base, idesc_o, j > 0, 1);
                     mma_commit(&sm.o_done[1]);
                     if (doB(j1)) {
                         mbar_wait(&sm.k_full[st1], (j1 / NS) & 1);
