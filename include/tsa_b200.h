@@ -60,7 +60,7 @@ typedef struct tsa_desc {
     int32_t n_heads;       /* H */
     int32_t n_kv_heads;    /* Hkv, H % Hkv == 0 */
     int32_t seq_len;       /* L */
-    int32_t d_head;        /* d (f32: any multiple of 4 <= 256; bf16 fast path: 128) */
+    int32_t d_head;        /* d in [1, 256] (bf16: even); tensor-core path: bf16, d = 128 */
     int32_t dtype;         /* tsa_dtype */
     int32_t mode;          /* tsa_mode */
     double tau;            /* dynamic coverage, [0, 1]     (SparsePlan::tau = 0.005) */

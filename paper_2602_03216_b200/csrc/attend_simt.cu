@@ -142,6 +142,49 @@ __global__ void __launch_bounds__(128) attend_simt_kernel(const T* __restrict__ 
     }
 }
 
+// Any other head size (the reference's unit tests use d = 1 and 4): one
+// thread per query row, per-key online softmax, K/V straight from global.
+template <typename T>
+__global__ void __launch_bounds__(128) attend_simt_any_d(const T* __restrict__ q,
+                                                         const T* __restrict__ k,
+                                                         const T* __restrict__ v,
+                                                         const int32_t* __restrict__ n_dev,
+                                                         int n_const, int kv_group,
+                                                         int rows_per_head, int kv_rows_per_head,
+                                                         int head_begin, int D, float scale,
+                                                         T* __restrict__ o) {
+    constexpr int DMAX = 256;
+    const int h = head_begin + blockIdx.y;
+    const int n = n_dev ? *n_dev : n_const;
+    const int i = blockIdx.x * 128 + threadIdx.x;
+    if (i >= n) return;
+    const int kvh = h / kv_group;
+    const T* qi = q + ((size_t)h * rows_per_head + i) * D;
+    const T* kh = k + (size_t)kvh * kv_rows_per_head * D;
+    const T* vh = v + (size_t)kvh * kv_rows_per_head * D;
+    float qr[DMAX], acc[DMAX];
+    for (int p = 0; p < D; ++p) {
+        qr[p] = Elem<T>::to_f32(qi[p]);
+        acc[p] = 0.0f;
+    }
+    float m = -INFINITY, l = 0.0f;
+    for (int j = 0; j <= i; ++j) {
+        float s = 0.0f;
+        for (int p = 0; p < D; ++p) s = fmaf(qr[p], Elem<T>::to_f32(kh[(size_t)j * D + p]), s);
+        s *= scale;
+        const float m_new = fmaxf(m, s);
+        const float corr = expf(m - m_new);
+        const float pj = expf(s - m_new);
+        l = l * corr + pj;
+        for (int p = 0; p < D; ++p)
+            acc[p] = fmaf(pj, Elem<T>::to_f32(vh[(size_t)j * D + p]), acc[p] * corr);
+        m = m_new;
+    }
+    T* dst = o + ((size_t)h * rows_per_head + i) * D;
+    const float inv_l = 1.0f / l;
+    for (int p = 0; p < D; ++p) dst[p] = Elem<T>::from_f32(acc[p] * inv_l);
+}
+
 template <typename T, int D>
 int launch_t(const tsa_desc& d, const void* q, const void* k, const void* v, const int32_t* n_dev,
              int n_const, int kv_group, int rows_per_head, int kv_rows_per_head, void* o,
@@ -169,8 +212,16 @@ int dispatch_d(const tsa_desc& d, const void* q, const void* k, const void* v,
         case 64: return launch_t<T, 64>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
         case 128: return launch_t<T, 128>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
         case 256: return launch_t<T, 256>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
-        default: return invalid("attend: unsupported d_head " + std::to_string(d.d_head) +
-                                " (supported: 8, 16, 32, 64, 128, 256)");
+        default: {
+            if (d.d_head < 1 || d.d_head > 256)
+                return invalid("attend: unsupported d_head " + std::to_string(d.d_head));
+            dim3 grid((d.seq_len + 127) / 128, d.head_end - d.head_begin);
+            attend_simt_any_d<T><<<grid, 128, 0, st>>>(
+                (const T*)q, (const T*)k, (const T*)v, n_dev, n_const, kv_group, rph, kvrph,
+                d.head_begin, d.d_head, 1.0f / sqrtf((float)d.d_head), (T*)o);
+            TSA_LAUNCH_CHECK("attend_simt_any_d");
+            return 0;
+        }
     }
 }
 

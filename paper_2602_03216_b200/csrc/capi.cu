@@ -72,9 +72,10 @@ int check_desc(const tsa_desc* d) {
     if (d->seq_len < 1) return invalid("tsa: seq_len must be positive");
     if (d->dtype != TSA_F32 && d->dtype != TSA_BF16) return invalid("tsa: unknown dtype");
     const int D = d->d_head;
-    if (!(D == 8 || D == 16 || D == 32 || D == 64 || D == 128 || D == 256))
-        return invalid("tsa: unsupported d_head " + std::to_string(D) +
-                       " (supported: 8, 16, 32, 64, 128, 256)");
+    if (D < 1 || D > 256)
+        return invalid("tsa: unsupported d_head " + std::to_string(D) + " (supported: 1..256)");
+    if (d->dtype == TSA_BF16 && D % 2 != 0)
+        return invalid("tsa: bf16 rows need an even d_head, got " + std::to_string(D));
     if (d->last_q < 1)
         return invalid("score_tokens: last_q must be positive, got " + std::to_string(d->last_q));
     if (d->kernel < 1 || d->kernel % 2 == 0)

@@ -12,14 +12,18 @@
 namespace tsa {
 namespace {
 
-// One warp moves `rows_per_warp` rows; lanes stride over the row's 16-B chunks.
-__global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ q,
-                                                     const uint4* __restrict__ k,
-                                                     const uint4* __restrict__ v,
+// One warp moves `rows_per_warp` rows; lanes stride over the row's chunks.
+// V is the access unit: 16 B when a row is a multiple of 16 B (every
+// production shape), else 4 or 2 B for the small head sizes the reference's
+// unit tests use (d = 1, 4).
+template <typename V>
+__global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
+                                                     const V* __restrict__ k,
+                                                     const V* __restrict__ v,
                                                      const int32_t* __restrict__ idx,
                                                      const int32_t* __restrict__ k_keep_p,
-                                                     uint4* __restrict__ qc, uint4* __restrict__ kc,
-                                                     uint4* __restrict__ vc, int L, int group,
+                                                     V* __restrict__ qc, V* __restrict__ kc,
+                                                     V* __restrict__ vc, int L, int group,
                                                      int chunks /* 16-B chunks per row */,
                                                      int head_begin) {
     const int h = head_begin + blockIdx.y;
@@ -38,9 +42,9 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ q
             if (r >= pad_end) break;
             const size_t dst = ((size_t)h * L + r) * chunks;
             for (int c = lane; c < chunks; c += 32) {
-                if (qc) qc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
-                kc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
-                vc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+                if (qc) qc[dst + c] = V{};
+                kc[dst + c] = V{};
+                vc[dst + c] = V{};
             }
         }
         return;
@@ -54,9 +58,9 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ q
         if (r >= n) {
             const size_t dst = ((size_t)h * L + r) * chunks;
             for (int c = lane; c < chunks; c += 32) {
-                if (qc) qc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
-                kc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
-                vc[dst + c] = make_uint4(0u, 0u, 0u, 0u);
+                if (qc) qc[dst + c] = V{};
+                kc[dst + c] = V{};
+                vc[dst + c] = V{};
             }
             continue;
         }
@@ -66,17 +70,17 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ q
         const size_t dst = ((size_t)h * L + r) * chunks;
         if (qc) {
             for (int c = lane; c < chunks; c += 32) {
-                const uint4 a = __ldg(q + src_q + c);
-                const uint4 b = __ldg(k + src_kv + c);
-                const uint4 e = __ldg(v + src_kv + c);
+                const V a = __ldg(q + src_q + c);
+                const V b = __ldg(k + src_kv + c);
+                const V e = __ldg(v + src_kv + c);
                 qc[dst + c] = a;
                 kc[dst + c] = b;
                 vc[dst + c] = e;
             }
         } else {  // K/V only (the fused attention gathers Q itself)
             for (int c = lane; c < chunks; c += 32) {
-                const uint4 b = __ldg(k + src_kv + c);
-                const uint4 e = __ldg(v + src_kv + c);
+                const V b = __ldg(k + src_kv + c);
+                const V e = __ldg(v + src_kv + c);
                 kc[dst + c] = b;
                 vc[dst + c] = e;
             }
@@ -84,9 +88,10 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint4* __restrict__ q
     }
 }
 
-__global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ oc,
+template <typename V>
+__global__ void __launch_bounds__(256) scatter_kernel(const V* __restrict__ oc,
                                                       const int32_t* __restrict__ inv,
-                                                      uint4* __restrict__ out, int L, int chunks,
+                                                      V* __restrict__ out, int L, int chunks,
                                                       int head_begin) {
     const int h = head_begin + blockIdx.y;
     const int rows_per_block = 64;
@@ -97,7 +102,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
         const int t = t0 + e / chunks, c = e % chunks;
         if (t >= L) break;
         const int r = inv_h[t];
-        uint4 val = make_uint4(0u, 0u, 0u, 0u);
+        V val = V{};
         if (r >= 0) val = __ldg(oc + ((size_t)h * L + r) * chunks + c);
         out[((size_t)h * L + t) * chunks + c] = val;
     }
@@ -105,8 +110,9 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint4* __restrict__ 
 
 // Rows the selection dropped are +0.0 (scatter_rows zero-initialises its
 // output, tensor_ops.cpp:107); the fused attention writes the kept rows.
+template <typename V>
 __global__ void __launch_bounds__(256) zero_unselected_kernel(const int32_t* __restrict__ inv,
-                                                              uint4* __restrict__ out, int L,
+                                                              V* __restrict__ out, int L,
                                                               int chunks, int head_begin) {
     const int h = head_begin + blockIdx.y;
     const int rows_per_block = 64;
@@ -115,7 +121,7 @@ __global__ void __launch_bounds__(256) zero_unselected_kernel(const int32_t* __r
     for (int e = threadIdx.x; e < rows_per_block * chunks; e += 256) {
         const int t = t0 + e / chunks, c = e % chunks;
         if (t >= L) break;
-        if (inv_h[t] < 0) out[((size_t)h * L + t) * chunks + c] = make_uint4(0u, 0u, 0u, 0u);
+        if (inv_h[t] < 0) out[((size_t)h * L + t) * chunks + c] = V{};
     }
 }
 
@@ -145,39 +151,74 @@ int launch_inverse(const tsa_desc& d, const int32_t* idx, const int32_t* k_keep,
     return 0;
 }
 
-int launch_zero_unselected(const tsa_desc& d, const int32_t* inv, void* out, cudaStream_t st) {
+// Row access width: 16, 4 or 2 bytes.
+static int unit_bytes(const tsa_desc& d) {
+    const size_t row = d.d_head * elem_bytes(d.dtype);
+    return row % 16 == 0 ? 16 : row % 4 == 0 ? 4 : 2;
+}
+
+template <typename V>
+static int zero_t(const tsa_desc& d, const int32_t* inv, void* out, cudaStream_t st) {
     const int L = d.seq_len;
-    const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / 16);
+    const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / sizeof(V));
     dim3 grid((L + 63) / 64, d.head_end - d.head_begin);
-    zero_unselected_kernel<<<grid, 256, 0, st>>>(inv, (uint4*)out, L, chunks, d.head_begin);
+    zero_unselected_kernel<V><<<grid, 256, 0, st>>>(inv, (V*)out, L, chunks, d.head_begin);
     TSA_LAUNCH_CHECK("zero_unselected");
+    return 0;
+}
+
+int launch_zero_unselected(const tsa_desc& d, const int32_t* inv, void* out, cudaStream_t st) {
+    switch (unit_bytes(d)) {
+        case 16: return zero_t<uint4>(d, inv, out, st);
+        case 4: return zero_t<uint32_t>(d, inv, out, st);
+        default: return zero_t<uint16_t>(d, inv, out, st);
+    }
+}
+
+template <typename V>
+static int gather_t(const tsa_desc& d, const void* q, const void* k, const void* v,
+                    const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
+                    cudaStream_t st) {
+    const int L = d.seq_len;
+    const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / sizeof(V));
+    const int nh = d.head_end - d.head_begin;
+    dim3 grid((L + 63) / 64, nh);
+    gather_kernel<V><<<grid, 256, 0, st>>>((const V*)q, (const V*)k, (const V*)v, idx, k_keep,
+                                           (V*)qc, (V*)kc, (V*)vc, L, d.n_heads / d.n_kv_heads,
+                                           chunks, d.head_begin);
+    TSA_LAUNCH_CHECK("gather");
     return 0;
 }
 
 int launch_gather(const tsa_desc& d, const void* q, const void* k, const void* v,
                   const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
                   cudaStream_t st) {
+    switch (unit_bytes(d)) {
+        case 16: return gather_t<uint4>(d, q, k, v, idx, k_keep, qc, kc, vc, st);
+        case 4: return gather_t<uint32_t>(d, q, k, v, idx, k_keep, qc, kc, vc, st);
+        default: return gather_t<uint16_t>(d, q, k, v, idx, k_keep, qc, kc, vc, st);
+    }
+}
+
+template <typename V>
+static int scatter_t(const tsa_desc& d, const void* oc, const int32_t* inv, void* out,
+                     cudaStream_t st) {
     const int L = d.seq_len;
-    const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / 16);
+    const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / sizeof(V));
     const int nh = d.head_end - d.head_begin;
     dim3 grid((L + 63) / 64, nh);
-    gather_kernel<<<grid, 256, 0, st>>>((const uint4*)q, (const uint4*)k, (const uint4*)v, idx,
-                                        k_keep, (uint4*)qc, (uint4*)kc, (uint4*)vc, L,
-                                        d.n_heads / d.n_kv_heads, chunks, d.head_begin);
-    TSA_LAUNCH_CHECK("gather");
+    scatter_kernel<V><<<grid, 256, 0, st>>>((const V*)oc, inv, (V*)out, L, chunks, d.head_begin);
+    TSA_LAUNCH_CHECK("scatter");
     return 0;
 }
 
 int launch_scatter(const tsa_desc& d, const void* oc, const int32_t* inv, void* out,
                    cudaStream_t st) {
-    const int L = d.seq_len;
-    const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / 16);
-    const int nh = d.head_end - d.head_begin;
-    dim3 grid((L + 63) / 64, nh);
-    scatter_kernel<<<grid, 256, 0, st>>>((const uint4*)oc, inv, (uint4*)out, L, chunks,
-                                         d.head_begin);
-    TSA_LAUNCH_CHECK("scatter");
-    return 0;
+    switch (unit_bytes(d)) {
+        case 16: return scatter_t<uint4>(d, oc, inv, out, st);
+        case 4: return scatter_t<uint32_t>(d, oc, inv, out, st);
+        default: return scatter_t<uint16_t>(d, oc, inv, out, st);
+    }
 }
 
 }  // namespace tsa

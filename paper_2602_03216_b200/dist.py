@@ -163,8 +163,13 @@ class ShardedSparseAttention:
             (H, L, d), dtype=dtype, device=device)
 
     def _all_gather(self, dst, src):
-        if self.shard.world > 1:
-            dist.all_gather_into_tensor(dst, src)
+        if self.shard.world == 1:
+            return
+        if dist.get_backend() == "nccl":
+            dist.all_gather_into_tensor(dst, src)  # NVLink, rank-ordered = head-ordered
+        else:  # gloo (CPU tests of the orchestration)
+            parts = list(dst.chunk(self.shard.world, dim=0))
+            dist.all_gather(parts, src.contiguous())
 
     def step(self, q, k, v, marks=None, dense: bool = False):
         mark = marks or (lambda name: None)

@@ -47,7 +47,7 @@ def test_desc_defaults_follow_sparse_plan():
     ("kernel", 4, "avg_pool_1d: kernel must be odd and positive, got 4"),
     ("tau", 1.5, "coverage_budget: tau 1.500000 outside [0, 1]"),
     ("s_fixed", 1.0, "fixed_budget: sparsity ratio 1.000000 outside [0, 1)"),
-    ("d_head", 96, "unsupported d_head 96"),
+    ("d_head", 300, "unsupported d_head 300"),
     ("head_end", 3, "splits a KV group"),
 ])
 def test_validation_messages(field, value, msg):
