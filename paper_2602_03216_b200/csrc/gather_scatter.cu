@@ -12,10 +12,17 @@
 namespace tsa {
 namespace {
 
-// One warp moves `rows_per_warp` rows; lanes stride over the row's chunks.
+// A block moves 64 rows of one head: the 64 indices are staged in shared
+// memory first, then every thread copies whole access units (chunk c of row
+// r) with all of its loads issued before its stores, so each thread keeps
+// several independent 16-B requests in flight.
 // V is the access unit: 16 B when a row is a multiple of 16 B (every
 // production shape), else 4 or 2 B for the small head sizes the reference's
-// unit tests use (d = 1, 4).
+// unit tests use (d = 1, 4).  Rows [n, ceil128(n)) are zeroed: the
+// tensor-core attention loads whole tiles, and P = 0 times a stale NaN would
+// poison O.
+constexpr int G_ROWS = 64;
+
 template <typename V>
 __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
                                                      const V* __restrict__ k,
@@ -24,66 +31,51 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
                                                      const int32_t* __restrict__ k_keep_p,
                                                      V* __restrict__ qc, V* __restrict__ kc,
                                                      V* __restrict__ vc, int L, int group,
-                                                     int chunks /* 16-B chunks per row */,
+                                                     int chunks /* access units per row */,
                                                      int head_begin) {
+    __shared__ int32_t rows[G_ROWS];
     const int h = head_begin + blockIdx.y;
     const int kv = h / group;
     const int n = *k_keep_p;
-    const int rows_per_block = (256 / 32) * 8;
-    const int r0 = blockIdx.x * rows_per_block;
-    if (r0 >= n) {
-        // Zero the rows of the last partial 128-row tile past n: the tensor-core
-        // attention loads whole tiles, and P = 0 times a stale NaN would poison O.
-        const int pad_end = min(L, (n + 127) / 128 * 128);
-        if (r0 >= pad_end) return;
-        const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-        for (int rr = 0; rr < 8; ++rr) {
-            const int r = r0 + warp * 8 + rr;
-            if (r >= pad_end) break;
-            const size_t dst = ((size_t)h * L + r) * chunks;
-            for (int c = lane; c < chunks; c += 32) {
-                if (qc) qc[dst + c] = V{};
-                kc[dst + c] = V{};
-                vc[dst + c] = V{};
-            }
-        }
-        return;
-    }
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int32_t* idx_h = idx + (size_t)h * L;
+    const int r0 = blockIdx.x * G_ROWS;
     const int pad_end = min(L, (n + 127) / 128 * 128);
-    for (int rr = 0; rr < 8; ++rr) {
-        const int r = r0 + warp * 8 + rr;
-        if (r >= pad_end) break;
-        if (r >= n) {
-            const size_t dst = ((size_t)h * L + r) * chunks;
-            for (int c = lane; c < chunks; c += 32) {
-                if (qc) qc[dst + c] = V{};
-                kc[dst + c] = V{};
-                vc[dst + c] = V{};
+    if (r0 >= pad_end) return;
+    if (threadIdx.x < G_ROWS) {
+        const int r = r0 + threadIdx.x;
+        rows[threadIdx.x] = r < n ? idx[(size_t)h * L + r] : -1;
+    }
+    __syncthreads();
+    const int total = G_ROWS * chunks;
+    constexpr int U = 4;
+    for (int e0 = threadIdx.x; e0 < total; e0 += 256 * U) {
+        V kb[U], vb[U], qb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * 256;
+            kb[u] = V{};
+            vb[u] = V{};
+            qb[u] = V{};
+            if (e < total) {
+                const int rr = e / chunks, c = e % chunks;
+                const int t = rows[rr];
+                if (t >= 0) {
+                    const size_t src_kv = ((size_t)kv * L + t) * chunks + c;
+                    kb[u] = __ldg(k + src_kv);
+                    vb[u] = __ldg(v + src_kv);
+                    if (qc) qb[u] = __ldg(q + ((size_t)h * L + t) * chunks + c);
+                }
             }
-            continue;
         }
-        const int t = idx_h[r];
-        const size_t src_q = ((size_t)h * L + t) * chunks;
-        const size_t src_kv = ((size_t)kv * L + t) * chunks;
-        const size_t dst = ((size_t)h * L + r) * chunks;
-        if (qc) {
-            for (int c = lane; c < chunks; c += 32) {
-                const V a = __ldg(q + src_q + c);
-                const V b = __ldg(k + src_kv + c);
-                const V e = __ldg(v + src_kv + c);
-                qc[dst + c] = a;
-                kc[dst + c] = b;
-                vc[dst + c] = e;
-            }
-        } else {  // K/V only (the fused attention gathers Q itself)
-            for (int c = lane; c < chunks; c += 32) {
-                const V b = __ldg(k + src_kv + c);
-                const V e = __ldg(v + src_kv + c);
-                kc[dst + c] = b;
-                vc[dst + c] = e;
-            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * 256;
+            if (e >= total) continue;
+            const int rr = e / chunks, c = e % chunks;
+            if (r0 + rr >= pad_end) continue;
+            const size_t dst = ((size_t)h * L + r0 + rr) * chunks + c;
+            kc[dst] = kb[u];
+            vc[dst] = vb[u];
+            if (qc) qc[dst] = qb[u];
         }
     }
 }

@@ -13,11 +13,15 @@
 // the prefix in double; the exact fixed-point sum differs from it by less than
 // L * 2^-53, documented as the near-tie rule in DESIGN.md.
 //
-// K3 (select_tokens, token_coverage.cpp:111-152), one CTA per head:
+// Both run as thread-block clusters of 8 CTAs (the token axis split 8 ways,
+// histograms merged through distributed shared memory).
+// K3 (select_tokens, token_coverage.cpp:111-152), one cluster per head:
 //   radix select of the (k - |F|)-th largest non-forced score, then one
 //   ordered compaction pass: keep t if forced, if s > v*, or if s == v* and t
 //   is among the lowest-index (k - |F| - count(> v*)) ties.  Output is
 //   ascending by construction; the inverse map is written in the same pass.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace tsa {
@@ -87,121 +91,139 @@ __device__ U block_excl_scan(U v, U* total) {
 // mode AGGREGATE_ONLY:       write s_l = headsum / total to sl_out and stop.
 enum { BUDGET_FROM_HEADSUM = 0, BUDGET_FROM_SL = 1, AGGREGATE_ONLY = 2 };
 
-__global__ void __launch_bounds__(BT) budget_kernel(const float* __restrict__ headsum, int L,
-                                                    double tau, int min_keep,
-                                                    int32_t* __restrict__ k_keep,
-                                                    int32_t* __restrict__ status, int mode,
-                                                    float* __restrict__ sl_out, int exact_total) {
-    __shared__ float stage[2][2048];
-    __shared__ float s_total;
+constexpr int CL = 8;  // CTAs per cluster: the token axis of one head (or of s_l) is split 8 ways
+
+// Sum of `v` over the block (all threads get it).
+template <typename U>
+__device__ U block_sum(U v) {
+    U tot;
+    block_excl_scan<U>(v, &tot);
+    return tot;
+}
+
+// ---------------------------------------------------------------- budget
+// One cluster of CL CTAs; CTA r owns tokens [r*S, (r+1)*S).  Per radix level:
+// local warp-aggregated histograms (count + exact 2^-62 fixed-point mass),
+// cluster barrier, CTA r merges bucket range r across the cluster through
+// DSMEM, range totals decide which CTA holds the crossing, that CTA finds the
+// bucket and broadcasts it into every CTA's shared memory.
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BT, 1)
+budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep,
+              int32_t* __restrict__ k_keep, int32_t* __restrict__ status, int mode,
+              float* __restrict__ sl_out, int exact_total) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int tid = threadIdx.x;
+    __shared__ __align__(16) float stage[2][2048];
     __shared__ uint32_t hist_cnt[2048];
     __shared__ unsigned long long hist_mass[2048];
-    __shared__ uint32_t s_prefix;
-    __shared__ unsigned long long s_mass_below;
-    __shared__ uint32_t s_cnt_below;
-    __shared__ int s_done;
+    __shared__ uint32_t m_cnt[2048 / CL];
+    __shared__ unsigned long long m_mass[2048 / CL];
+    __shared__ uint32_t range_cnt;
+    __shared__ unsigned long long range_mass;
+    __shared__ double part_total;
+    __shared__ float s_total;
+    __shared__ uint32_t res_bucket, res_cnt;
+    __shared__ unsigned long long res_mass;
+    __shared__ int s_done, s_rstar;
+    __shared__ unsigned long long s_below_r;
+    __shared__ uint32_t s_cbelow_r;
+    const int S = (L + CL - 1) / CL;
+    const int t_begin = min(L, rank * S), t_end = min(L, t_begin + S);
 
-    const int tid = threadIdx.x;
+    // ---- total ----
     float total = 1.0f;
     if (mode != BUDGET_FROM_SL) {
-    if (exact_total) {
-    // ---- total: sequential f32 chain (token_coverage.cpp:58-61) ----
-    // Warps stage 2048-float chunks into a double buffer; thread 0 consumes
-    // them with 16-B shared loads kept ahead of the dependent FADD chain.
-    constexpr int CH = 2048;
-    const int nchunk = (L + CH - 1) / CH;
-    for (int i = tid; i < CH; i += BT) stage[0][i] = i < L ? headsum[i] : 0.0f;
-    __syncthreads();
-    total = 0.0f;
-    for (int c = 0; c < nchunk; ++c) {
-        if (c + 1 < nchunk) {
-            const int base = (c + 1) * CH;
-            for (int i = tid; i < CH; i += BT)
-                stage[(c + 1) & 1][i] = base + i < L ? headsum[base + i] : 0.0f;
-        }
-        if (tid == 0) {
-            const float* buf = stage[c & 1];
-            const int n = min(CH, L - c * CH);
-            const float4* b4 = reinterpret_cast<const float4*>(buf);
-            const int n4 = n / 4;
+        if (exact_total) {
+            // sequential f32 chain (token_coverage.cpp:58-61) in rank 0; thread 0
+            // consumes 2048-float chunks staged by the other warps
+            if (rank == 0) {
+                constexpr int CH = 2048;
+                const int nchunk = (L + CH - 1) / CH;
+                for (int i = tid; i < CH; i += BT) stage[0][i] = i < L ? headsum[i] : 0.0f;
+                __syncthreads();
+                float acc = 0.0f;
+                for (int c = 0; c < nchunk; ++c) {
+                    if (c + 1 < nchunk) {
+                        const int base = (c + 1) * CH;
+                        for (int i = tid; i < CH; i += BT)
+                            stage[(c + 1) & 1][i] = base + i < L ? headsum[base + i] : 0.0f;
+                    }
+                    if (tid == 0) {
+                        const float* buf = stage[c & 1];
+                        const int n = min(CH, L - c * CH);
+                        const float4* b4 = reinterpret_cast<const float4*>(buf);
+                        const int n4 = n / 4;
 #pragma unroll 8
-            for (int i = 0; i < n4; ++i) {
-                const float4 v = b4[i];
-                total = __fadd_rn(total, v.x);
-                total = __fadd_rn(total, v.y);
-                total = __fadd_rn(total, v.z);
-                total = __fadd_rn(total, v.w);
+                        for (int i = 0; i < n4; ++i) {
+                            const float4 v = b4[i];
+                            acc = __fadd_rn(acc, v.x);
+                            acc = __fadd_rn(acc, v.y);
+                            acc = __fadd_rn(acc, v.z);
+                            acc = __fadd_rn(acc, v.w);
+                        }
+                        for (int i = n4 * 4; i < n; ++i) acc = __fadd_rn(acc, buf[i]);
+                    }
+                    __syncthreads();
+                }
+                if (tid == 0)
+                    for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(&s_total, r) = acc;
             }
-            for (int i = n4 * 4; i < n; ++i) total = __fadd_rn(total, buf[i]);
+            cluster.sync();
+            total = s_total;
+        } else {
+            // deterministic parallel f64 reduction (FAST scoring mode): fixed
+            // per-CTA partials combined in rank order by every CTA
+            double acc = 0.0;
+            for (int t = t_begin + tid; t < t_end; t += BT) acc += (double)headsum[t];
+            acc = block_sum<double>(acc);
+            if (tid == 0) part_total = acc;
+            cluster.sync();
+            double tot = 0.0;
+            for (int r = 0; r < CL; ++r) tot += *cluster.map_shared_rank(&part_total, r);
+            total = (float)tot;
         }
-        __syncthreads();
-    }
-    } else {
-    // ---- total: deterministic parallel reduction in f64 (FAST scoring mode) ----
-    // Fixed thread->element assignment and a fixed reduction tree, so the
-    // result is reproducible; it differs from the sequential f32 chain by far
-    // less than the FAST scores differ from reference-order scores.
-    __shared__ double red[BT / 32];
-    double acc = 0.0;
-    for (int t = tid; t < L; t += BT) acc += (double)headsum[t];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((tid & 31) == 0) red[tid >> 5] = acc;
-    __syncthreads();
-    if (tid < 32) {
-        double w = red[tid];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-        if (tid == 0) total = (float)w;
-    }
-    }
-    if (tid == 0) s_total = total;
-    __syncthreads();
-    total = s_total;
-    if (!(total > 0.0f)) {  // aggregate_scores throws (:62-64)
-        if (tid == 0) {
-            *status = 1;
-            if (k_keep) *k_keep = min_keep;
+        if (!(total > 0.0f)) {  // aggregate_scores throws (:62-64)
+            if (rank == 0 && tid == 0) {
+                *status = 1;
+                if (k_keep) *k_keep = min_keep;
+            }
+            cluster.sync();
+            return;
         }
-        return;
+        if (mode == AGGREGATE_ONLY) {
+            for (int t = t_begin + tid; t < t_end; t += BT) sl_out[t] = __fdiv_rn(headsum[t], total);
+            cluster.sync();
+            return;
+        }
     }
-    if (mode == AGGREGATE_ONLY) {
-        for (int t = tid; t < L; t += BT) sl_out[t] = __fdiv_rn(headsum[t], total);
-        return;
-    }
-    }  // mode != BUDGET_FROM_SL
     // ---- coverage crossing ----
     // T = ceil(tau * 2^62); tau = 0 -> k_sparse = 0 (prefix 0 >= 0, :82).
     const double tscaled = ldexp(tau, 62);
     unsigned long long T = (unsigned long long)tscaled;
     if ((double)T < tscaled) ++T;
     if (T == 0ull) {
-        if (tid == 0) *k_keep = max(L, min_keep);
+        if (rank == 0 && tid == 0) *k_keep = max(L, min_keep);
+        cluster.sync();
         return;
     }
-    if (tid == 0) {
-        s_prefix = 0;
-        s_mass_below = 0;
-        s_cnt_below = 0;
-        s_done = 0;
-    }
+    uint32_t prefix = 0, cnt_below = 0;
+    unsigned long long mass_below = 0;
+    bool done = false;  // total mass never reaches tau: k_sparse = L
     for (int lvl = 0; lvl < 3; ++lvl) {
-        const int shift = kShift[lvl], nb = 1 << kBits[lvl];
+        const int shift = kShift[lvl], bits = kBits[lvl], nb = 1 << bits, per = nb / CL;
+        const int pshift = shift + bits;
         for (int b = tid; b < nb; b += BT) {
             hist_cnt[b] = 0;
             hist_mass[b] = 0;
         }
         __syncthreads();
-        const uint32_t prefix = s_prefix;
-        const int pshift = shift + kBits[lvl];
-        // warp-aggregated: lanes hitting the same bucket combine their count and
-        // mass (three 21-bit limbs so the 32-lane sums cannot overflow) before
-        // one shared atomic per distinct bucket
-        for (int base = 0; base < L; base += BT) {
+        for (int base = t_begin; base < t_end; base += BT) {
             const int t = base + tid;
             uint32_t b = 0xFFFFFFFFu;
             unsigned long long m = 0;
-            if (t < L) {
+            if (t < t_end) {
                 const float sl = __fdiv_rn(headsum[t], total);
                 const uint32_t key = score_key(sl);
                 if (pshift >= 32 || (key >> pshift) == prefix) {
@@ -209,59 +231,97 @@ __global__ void __launch_bounds__(BT) budget_kernel(const float* __restrict__ he
                     m = (unsigned long long)ldexp((double)sl, 62);
                 }
             }
+            // lanes of one bucket combine count and mass (three 21-bit limbs so
+            // the 32-lane sums cannot overflow) before one shared atomic
             const uint32_t grp = __match_any_sync(0xffffffffu, b);
             const uint32_t l0 = __reduce_add_sync(grp, (uint32_t)(m & 0x1FFFFFu));
             const uint32_t l1 = __reduce_add_sync(grp, (uint32_t)((m >> 21) & 0x1FFFFFu));
             const uint32_t l2 = __reduce_add_sync(grp, (uint32_t)(m >> 42));
-            if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (int)(tid & 31)) {
-                const unsigned long long sum = (unsigned long long)l0 +
-                                               ((unsigned long long)l1 << 21) +
-                                               ((unsigned long long)l2 << 42);
+            if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (tid & 31)) {
                 atomicAdd(&hist_cnt[b], (uint32_t)__popc(grp));
-                atomicAdd(&hist_mass[b], sum);
+                atomicAdd(&hist_mass[b], (unsigned long long)l0 + ((unsigned long long)l1 << 21) +
+                                             ((unsigned long long)l2 << 42));
             }
         }
-        __syncthreads();
-        // exclusive scan over buckets (2 buckets per thread, ascending)
-        const int b0 = 2 * tid, b1 = 2 * tid + 1;
-        unsigned long long m0 = b0 < nb ? hist_mass[b0] : 0, m1 = b1 < nb ? hist_mass[b1] : 0;
-        uint32_t c0 = b0 < nb ? hist_cnt[b0] : 0, c1 = b1 < nb ? hist_cnt[b1] : 0;
-        unsigned long long mtot;
-        uint32_t ctot;
-        const unsigned long long mex = block_excl_scan<unsigned long long>(m0 + m1, &mtot);
-        const uint32_t cex = block_excl_scan<uint32_t>(c0 + c1, &ctot);
-        const unsigned long long need = T - s_mass_below;  // > 0
-        __syncthreads();
-        if (lvl == 0 && mtot < need) {
-            // total mass never reaches tau: k_sparse = L
-            if (tid == 0) s_done = 1;
-        } else {
-            // bucket b with excl[b] < need <= excl[b] + mass[b]
-            if (b0 < nb && mex < need && need <= mex + m0) {
-                s_prefix = (prefix << kBits[lvl]) | (uint32_t)b0;
-                s_mass_below += mex;
-                s_cnt_below += cex;
+        cluster.sync();
+        // merge bucket range [rank*per, (rank+1)*per) over the cluster
+        uint32_t mc = 0;
+        unsigned long long mm = 0;
+        if (tid < per) {
+            const int b = rank * per + tid;
+            for (int r = 0; r < CL; ++r) {
+                mc += cluster.map_shared_rank(hist_cnt, r)[b];
+                mm += cluster.map_shared_rank(hist_mass, r)[b];
             }
-            if (b1 < nb && mex + m0 < need && need <= mex + m0 + m1) {
-                s_prefix = (prefix << kBits[lvl]) | (uint32_t)b1;
-                s_mass_below += mex + m0;
-                s_cnt_below += cex + c0;
+            m_cnt[tid] = mc;
+            m_mass[tid] = mm;
+        }
+        const uint32_t rc = block_sum<uint32_t>(mc);
+        const unsigned long long rmass = block_sum<unsigned long long>(mm);
+        if (tid == 0) {
+            range_cnt = rc;
+            range_mass = rmass;
+        }
+        cluster.sync();
+        const unsigned long long need = T - mass_below;  // > 0
+        if (tid == 0) {
+            unsigned long long below = 0;
+            uint32_t cbelow = 0;
+            int rstar = -1;
+            for (int r = 0; r < CL; ++r) {
+                const unsigned long long mr = *cluster.map_shared_rank(&range_mass, r);
+                const uint32_t cr = *cluster.map_shared_rank(&range_cnt, r);
+                if (below < need && need <= below + mr) {
+                    rstar = r;
+                    break;
+                }
+                below += mr;
+                cbelow += cr;
             }
+            s_rstar = rstar;
+            s_below_r = below;
+            s_cbelow_r = cbelow;
         }
         __syncthreads();
-        if (s_done) break;
+        if (s_rstar < 0) {  // only possible at level 0: total mass < tau
+            done = true;
+            cluster.sync();
+            break;
+        }
+        if (rank == s_rstar) {
+            // ascending exclusive scan inside this CTA's merged range
+            const unsigned long long m0 = tid < per ? m_mass[tid] : 0;
+            const uint32_t c0 = tid < per ? m_cnt[tid] : 0;
+            unsigned long long mtot;
+            uint32_t ctot;
+            const unsigned long long mex = block_excl_scan<unsigned long long>(m0, &mtot) + s_below_r;
+            const uint32_t cex = block_excl_scan<uint32_t>(c0, &ctot) + s_cbelow_r;
+            if (tid < per && mex < need && need <= mex + m0) {
+                for (int r = 0; r < CL; ++r) {
+                    *cluster.map_shared_rank(&res_bucket, r) = (uint32_t)(rank * per + tid);
+                    *cluster.map_shared_rank(&res_mass, r) = mex;
+                    *cluster.map_shared_rank(&res_cnt, r) = cex;
+                }
+            }
+        }
+        cluster.sync();
+        prefix = (prefix << bits) | res_bucket;
+        mass_below += res_mass;
+        cnt_below += res_cnt;
+        cluster.sync();  // everyone read res before the next level may overwrite it
     }
-    if (tid == 0) {
+    if (rank == 0 && tid == 0) {
         int k_sparse = L;
-        if (!s_done) {
-            const float v = __uint_as_float(s_prefix);
+        if (!done) {
+            const float v = __uint_as_float(prefix);
             const unsigned long long m = (unsigned long long)ldexp((double)v, 62);
-            const unsigned long long need = T - s_mass_below;
+            const unsigned long long need = T - mass_below;
             const unsigned long long c = (need + m - 1) / m;  // m > 0: bucket mass crossed
-            k_sparse = (int)(s_cnt_below + c);
+            k_sparse = (int)(cnt_below + c);
         }
         *k_keep = max(L - k_sparse, min_keep);
     }
+    (void)s_done;
 }
 
 // ---------------------------------------------------------------- select
@@ -276,37 +336,42 @@ __device__ __forceinline__ bool is_forced(int t, const int32_t* forced, int nf, 
     return lo < nf && forced[lo] == t;
 }
 
-__global__ void __launch_bounds__(BT) select_kernel(const float* __restrict__ s, int L,
-                                                    const int32_t* __restrict__ k_keep_p,
-                                                    const int32_t* __restrict__ forced, int nf,
-                                                    int fbegin, int head_begin,
-                                                    int32_t* __restrict__ idx,
-                                                    int32_t* __restrict__ inv) {
-    __shared__ uint32_t hist[2048];
-    __shared__ uint32_t s_prefix, s_cnt_gt, s_need;
-    const int h = head_begin + blockIdx.x;
+// One cluster of CL CTAs per head; CTA r owns tokens [r*S, (r+1)*S).  Radix
+// select of the (k - |F|)-th largest non-forced key as in budget_kernel
+// (descending), then an ordered compaction whose per-slice bases (kept count
+// and tie count before the slice) come from the lower-ranked CTAs via DSMEM.
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BT, 1)
+select_kernel(const float* __restrict__ s, int L, const int32_t* __restrict__ k_keep_p,
+              const int32_t* __restrict__ forced, int nf, int fbegin, int head_begin,
+              int32_t* __restrict__ idx, int32_t* __restrict__ inv) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
     const int tid = threadIdx.x;
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t m_cnt[2048 / CL];
+    __shared__ uint32_t range_cnt;
+    __shared__ uint32_t res_bucket, res_above;
+    __shared__ int s_rstar;
+    __shared__ uint32_t s_above_r;
+    __shared__ int slice_fg, slice_eq;  // forced-or-greater and tie counts of this slice
+    const int h = head_begin + blockIdx.y;
     const float* sh = s + (size_t)h * L;
+    const int S = (L + CL - 1) / CL;
+    const int t_begin = min(L, rank * S), t_end = min(L, t_begin + S);
     const int k_keep = *k_keep_p;
     const int n_free = k_keep - nf;
-    if (tid == 0) {
-        s_prefix = 0;
-        s_cnt_gt = 0;
-        s_need = (uint32_t)max(n_free, 0);
-    }
-    __syncthreads();
-    // ---- radix select of the n_free-th largest non-forced key ----
+    uint32_t prefix = 0, need = (uint32_t)max(n_free, 0);
     if (n_free > 0) {
         for (int lvl = 0; lvl < 3; ++lvl) {
-            const int shift = kShift[lvl], nb = 1 << kBits[lvl];
-            const int pshift = shift + kBits[lvl];
+            const int shift = kShift[lvl], bits = kBits[lvl], nb = 1 << bits, per = nb / CL;
+            const int pshift = shift + bits;
             for (int b = tid; b < nb; b += BT) hist[b] = 0;
             __syncthreads();
-            const uint32_t prefix = s_prefix;
-            for (int base = 0; base < L; base += BT) {
+            for (int base = t_begin; base < t_end; base += BT) {
                 const int t = base + tid;
                 uint32_t b = 0xFFFFFFFFu;
-                if (t < L && !is_forced(t, forced, nf, fbegin)) {
+                if (t < t_end && !is_forced(t, forced, nf, fbegin)) {
                     const uint32_t key = score_key(sh[t]);
                     if (pshift >= 32 || (key >> pshift) == prefix) b = (key >> shift) & (nb - 1);
                 }
@@ -314,37 +379,81 @@ __global__ void __launch_bounds__(BT) select_kernel(const float* __restrict__ s,
                 if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (tid & 31))
                     atomicAdd(&hist[b], (uint32_t)__popc(grp));
             }
-            __syncthreads();
-            // descending: count of keys in buckets above b = exclusive scan from the top
-            const int b0 = nb - 1 - 2 * tid, b1 = nb - 2 - 2 * tid;  // thread handles 2, top-down
-            const uint32_t c0 = b0 >= 0 ? hist[b0] : 0, c1 = b1 >= 0 ? hist[b1] : 0;
-            uint32_t ctot;
-            const uint32_t above = block_excl_scan<uint32_t>(c0 + c1, &ctot);
-            const uint32_t need = s_need;
-            __syncthreads();
-            if (b0 >= 0 && above < need && need <= above + c0) {
-                s_prefix = (prefix << kBits[lvl]) | (uint32_t)b0;
-                s_cnt_gt += above;
-                s_need = need - above;
+            cluster.sync();
+            uint32_t mc = 0;
+            if (tid < per) {
+                const int b = rank * per + tid;
+                for (int r = 0; r < CL; ++r) mc += cluster.map_shared_rank(hist, r)[b];
+                m_cnt[tid] = mc;
             }
-            if (b1 >= 0 && above + c0 < need && need <= above + c0 + c1) {
-                s_prefix = (prefix << kBits[lvl]) | (uint32_t)b1;
-                s_cnt_gt += above + c0;
-                s_need = need - above - c0;
+            const uint32_t rc = block_sum<uint32_t>(mc);
+            if (tid == 0) range_cnt = rc;
+            cluster.sync();
+            if (tid == 0) {  // descending over ranks: higher ranks hold higher buckets
+                uint32_t above = 0;
+                int rstar = -1;
+                for (int r = CL - 1; r >= 0; --r) {
+                    const uint32_t cr = *cluster.map_shared_rank(&range_cnt, r);
+                    if (above < need && need <= above + cr) {
+                        rstar = r;
+                        break;
+                    }
+                    above += cr;
+                }
+                s_rstar = rstar;
+                s_above_r = above;
             }
             __syncthreads();
+            if (rank == s_rstar) {
+                // descending exclusive scan: thread i handles bucket per-1-i
+                const int bi = per - 1 - tid;
+                const uint32_t c0 = (tid < per) ? m_cnt[bi] : 0;
+                uint32_t ctot;
+                const uint32_t above = block_excl_scan<uint32_t>(c0, &ctot) + s_above_r;
+                if (tid < per && above < need && need <= above + c0) {
+                    for (int r = 0; r < CL; ++r) {
+                        *cluster.map_shared_rank(&res_bucket, r) = (uint32_t)(rank * per + bi);
+                        *cluster.map_shared_rank(&res_above, r) = above;
+                    }
+                }
+            }
+            cluster.sync();
+            prefix = (prefix << bits) | res_bucket;
+            need -= res_above;
+            cluster.sync();  // everyone read res before the next level may overwrite it
         }
     }
-    const uint32_t vstar = s_prefix;
-    // ties to take at v* (lowest index first); with n_free == 0 none
-    const int take_eq = n_free > 0 ? (int)s_need : 0;
+    const uint32_t vstar = prefix;
     const bool has_thr = n_free > 0;
-    // ---- ordered compaction ----
+    const int take_eq = has_thr ? (int)need : 0;  // ties at v* to keep, lowest index first
+    // ---- slice counts -> bases from the lower-ranked CTAs ----
+    int fg = 0, eq = 0;
+    for (int t = t_begin + tid; t < t_end; t += BT) {
+        const bool f = is_forced(t, forced, nf, fbegin);
+        const uint32_t key = score_key(sh[t]);
+        if (f || (has_thr && key > vstar)) ++fg;
+        else if (has_thr && key == vstar) ++eq;
+    }
+    fg = block_sum<int>(fg);
+    eq = block_sum<int>(eq);
+    if (tid == 0) {
+        slice_fg = fg;
+        slice_eq = eq;
+    }
+    cluster.sync();
+    int base_pos = 0, base_eq = 0;
+    for (int r = 0; r < rank; ++r) {
+        const int fr = *cluster.map_shared_rank(&slice_fg, r);
+        const int er = *cluster.map_shared_rank(&slice_eq, r);
+        base_pos += fr + max(0, min(er, take_eq - base_eq));
+        base_eq += er;
+    }
+    cluster.sync();  // remote reads done before any CTA may exit
+    // ---- ordered compaction of this slice ----
     int32_t* idx_h = idx + (size_t)h * L;
     int32_t* inv_h = inv ? inv + (size_t)h * L : nullptr;
-    int base_pos = 0, base_eq = 0;
     constexpr int IPT = 4;
-    for (int t0 = 0; t0 < L; t0 += BT * IPT) {
+    for (int t0 = t_begin; t0 < t_end; t0 += BT * IPT) {
         int keep_flags = 0, eq_flags = 0, nkeep = 0, neq = 0;
         uint32_t keys[IPT];
         bool forced_f[IPT];
@@ -353,7 +462,7 @@ __global__ void __launch_bounds__(BT) select_kernel(const float* __restrict__ s,
             const int t = t0 + tid * IPT + i;
             forced_f[i] = false;
             keys[i] = 0;
-            if (t < L) {
+            if (t < t_end) {
                 forced_f[i] = is_forced(t, forced, nf, fbegin);
                 keys[i] = score_key(sh[t]);
                 if (!forced_f[i] && has_thr && keys[i] == vstar) {
@@ -368,7 +477,7 @@ __global__ void __launch_bounds__(BT) select_kernel(const float* __restrict__ s,
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const int t = t0 + tid * IPT + i;
-            if (t >= L) continue;
+            if (t >= t_end) continue;
             bool keep = forced_f[i];
             if (!keep && has_thr) {
                 if (keys[i] > vstar) keep = true;
@@ -384,7 +493,7 @@ __global__ void __launch_bounds__(BT) select_kernel(const float* __restrict__ s,
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const int t = t0 + tid * IPT + i;
-            if (t >= L) continue;
+            if (t >= t_end) continue;
             if (keep_flags & (1 << i)) {
                 idx_h[pos] = t;
                 if (inv_h) inv_h[t] = pos;
@@ -411,7 +520,7 @@ int launch_budget(const tsa_desc& d, const float* s, int32_t* k_keep, float* hea
     const int L = d.seq_len;
     headsum_kernel<<<(L + 255) / 256, 256, 0, st>>>(s, headsum, d.n_heads, L);
     TSA_LAUNCH_CHECK("headsum");
-    budget_kernel<<<1, BT, 0, st>>>(headsum, L, d.tau, min_keep, k_keep, status,
+    budget_kernel<<<CL, BT, 0, st>>>(headsum, L, d.tau, min_keep, k_keep, status,
                                     BUDGET_FROM_HEADSUM, nullptr,
                                     scoring_mode(d) == TSA_SCORING_REFERENCE ? 1 : 0);
     TSA_LAUNCH_CHECK("budget");
@@ -423,7 +532,7 @@ int launch_aggregate(const tsa_desc& d, const float* s, float* sl, float* headsu
     const int L = d.seq_len;
     headsum_kernel<<<(L + 255) / 256, 256, 0, st>>>(s, headsum, d.n_heads, L);
     TSA_LAUNCH_CHECK("headsum");
-    budget_kernel<<<1, BT, 0, st>>>(headsum, L, 0.0, 1, nullptr, status, AGGREGATE_ONLY, sl,
+    budget_kernel<<<CL, BT, 0, st>>>(headsum, L, 0.0, 1, nullptr, status, AGGREGATE_ONLY, sl,
                                     scoring_mode(d) == TSA_SCORING_REFERENCE ? 1 : 0);
     TSA_LAUNCH_CHECK("aggregate");
     return 0;
@@ -431,7 +540,7 @@ int launch_aggregate(const tsa_desc& d, const float* s, float* sl, float* headsu
 
 int launch_coverage_from_sl(const tsa_desc& d, const float* sl, int32_t* k_keep, int32_t* status,
                             int min_keep, cudaStream_t st) {
-    budget_kernel<<<1, BT, 0, st>>>(sl, d.seq_len, d.tau, min_keep, k_keep, status, BUDGET_FROM_SL,
+    budget_kernel<<<CL, BT, 0, st>>>(sl, d.seq_len, d.tau, min_keep, k_keep, status, BUDGET_FROM_SL,
                                     nullptr, 1);
     TSA_LAUNCH_CHECK("coverage_budget");
     return 0;
@@ -441,8 +550,8 @@ int launch_select(const tsa_desc& d, const float* s, const int32_t* k_keep, cons
                   int32_t n_forced, int32_t forced_begin, int32_t* idx, int32_t* inv,
                   cudaStream_t st) {
     const int nh = d.head_end - d.head_begin;
-    select_kernel<<<nh, BT, 0, st>>>(s, d.seq_len, k_keep, forced, n_forced, forced_begin,
-                                     d.head_begin, idx, inv);
+    select_kernel<<<dim3(CL, nh), BT, 0, st>>>(s, d.seq_len, k_keep, forced, n_forced,
+                                               forced_begin, d.head_begin, idx, inv);
     TSA_LAUNCH_CHECK("select");
     return 0;
 }
