@@ -249,7 +249,10 @@ def run_ours(args):
     b = 2
     hbm_rows = {}
     for name, nbytes in (
-            # K/V rows of the KV head per query head: read + write compressed, + idx
+            # K/V rows of the KV head per query head (read + write compressed, + idx)
+            # and the zero rows of the dropped tokens (+ inverse map), one launch
+            ("gather_zero", 4 * sh.h_per * k_keep * D * b + 4 * sh.h_per * k_keep
+             + sh.h_per * (L - k_keep) * D * b + 4 * sh.h_per * L),
             ("gather", 4 * sh.h_per * k_keep * D * b + 4 * sh.h_per * k_keep),
             # zero rows the selection dropped + read the inverse map
             ("zero_fill", sh.h_per * (L - k_keep) * D * b + 4 * sh.h_per * L),

@@ -145,6 +145,12 @@ TSA_API int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* kc,
                                const int32_t* idx, const int32_t* k_keep, void* out,
                                void* stream);
 
+/* K/V half of tsa_gather (kc, vc) and tsa_zero_unselected in one pass: the
+ * two independent HBM streams of the fused path share a launch. */
+TSA_API int tsa_gather_zero(const tsa_desc* d, const void* k, const void* v, const int32_t* idx,
+                            const int32_t* k_keep, void* kc, void* vc, const int32_t* inv,
+                            void* out, void* stream);
+
 /* out[h, t] = +0.0 for every t with inv[h, t] < 0 (scatter_rows' zero rows). */
 TSA_API int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream);
 

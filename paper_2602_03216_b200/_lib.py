@@ -21,7 +21,7 @@ TSA_OK, TSA_ERR_INVALID, TSA_ERR_CUDA = 0, 1, 2
 EXPORTS = (
     "tsa_desc_init", "tsa_last_error", "tsa_version", "tsa_kernel_launches", "tsa_workspace_size", "tsa_score",
     "tsa_budget", "tsa_aggregate_scores", "tsa_coverage_budget", "tsa_select", "tsa_gather",
-    "tsa_attend", "tsa_attend_indexed", "tsa_zero_unselected", "tsa_scatter",
+    "tsa_attend", "tsa_attend_indexed", "tsa_zero_unselected", "tsa_gather_zero", "tsa_scatter",
     "tsa_scatter_rows", "tsa_check", "tsa_token_sparse_attention",
     "tsa_dense_attention", "tsa_sparse_attention_layer",
 )
@@ -84,6 +84,7 @@ def load() -> C.CDLL:
         "tsa_scatter": (C.c_int, [D, P, P, P, P]),
         "tsa_attend_indexed": (C.c_int, [D, P, P, P, P, P, P, P]),
         "tsa_zero_unselected": (C.c_int, [D, P, P, P]),
+        "tsa_gather_zero": (C.c_int, [D, P, P, P, P, P, P, P, P, P]),
         "tsa_scatter_rows": (C.c_int, [D, P, P, P, P, P, P]),
         "tsa_check": (C.c_int, [D, P, P]),
         "tsa_token_sparse_attention": (C.c_int, [D, P, P, P, P, P, P, P, P]),

@@ -250,6 +250,14 @@ int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* kc, const v
     return launch_attend_indexed(*d, q, kc, vc, idx, k_keep, out, S(stream));
 }
 
+int tsa_gather_zero(const tsa_desc* d, const void* k, const void* v, const int32_t* idx,
+                    const int32_t* k_keep, void* kc, void* vc, const int32_t* inv, void* out,
+                    void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!kc || !vc || !inv || !out) return invalid("tsa_gather_zero: null buffer");
+    return launch_gather_zero(*d, nullptr, k, v, idx, k_keep, nullptr, kc, vc, inv, out, S(stream));
+}
+
 int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream) {
     if (int rc = check_desc(d)) return rc;
     return launch_zero_unselected(*d, inv, out, S(stream));
@@ -279,9 +287,8 @@ int tsa_token_sparse_attention(const tsa_desc* d, const void* q, const void* k, 
     int rc;
     if (attend_sm100_supported(*d)) {  // fused gather -> attend -> scatter
         if ((rc = launch_inverse(*d, idx, k_keep, at<int32_t>(ws, w.inv), st))) return rc;
-        if ((rc = launch_zero_unselected(*d, at<int32_t>(ws, w.inv), out, st))) return rc;
-        if ((rc = launch_gather(*d, q, k, v, idx, k_keep, nullptr, at<void>(ws, w.kc),
-                                at<void>(ws, w.vc), st)))
+        if ((rc = launch_gather_zero(*d, q, k, v, idx, k_keep, nullptr, at<void>(ws, w.kc),
+                                     at<void>(ws, w.vc), at<int32_t>(ws, w.inv), out, st)))
             return rc;
         return launch_attend_indexed(*d, q, at<void>(ws, w.kc), at<void>(ws, w.vc), idx, k_keep,
                                      out, st);
@@ -323,10 +330,9 @@ int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, 
         if ((rc = tsa_score(d, q, k, s, ws, stream))) return rc;
         if ((rc = budget_impl(*d, s, k_keep_out, ws, std::max(1, nf), st))) return rc;
         if ((rc = launch_select(*d, s, k_keep_out, nullptr, nf, fb, idx, inv, st))) return rc;
-        if (attend_sm100_supported(*d)) {  // K/V gather, then fused Q-gather/attend/scatter
-            if ((rc = launch_zero_unselected(*d, inv, out, st))) return rc;
-            if ((rc = launch_gather(*d, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
-                                    at<void>(ws, w.vc), st)))
+        if (attend_sm100_supported(*d)) {  // K/V gather + zero-fill, then fused Q-gather/attend/scatter
+            if ((rc = launch_gather_zero(*d, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
+                                         at<void>(ws, w.vc), inv, out, st)))
                 return rc;
             if ((rc = launch_attend_indexed(*d, q, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
                                             k_keep_out, out, st)))

@@ -96,6 +96,9 @@ int launch_write_int(int32_t* dst, int32_t value, cudaStream_t st);
 int launch_gather(const tsa_desc& d, const void* q, const void* k, const void* v,
                   const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
                   cudaStream_t st);
+int launch_gather_zero(const tsa_desc& d, const void* q, const void* k, const void* v,
+                       const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
+                       const int32_t* inv, void* out, cudaStream_t st);
 int launch_scatter(const tsa_desc& d, const void* oc, const int32_t* inv, void* out,
                    cudaStream_t st);
 int launch_inverse(const tsa_desc& d, const int32_t* idx, const int32_t* k_keep, int32_t* inv,

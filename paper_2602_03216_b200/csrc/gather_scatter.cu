@@ -32,13 +32,25 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
                                                      V* __restrict__ qc, V* __restrict__ kc,
                                                      V* __restrict__ vc, int L, int group,
                                                      int chunks /* access units per row */,
-                                                     int head_begin) {
+                                                     int head_begin,
+                                                     const int32_t* __restrict__ inv,
+                                                     V* __restrict__ out) {
     __shared__ int32_t rows[G_ROWS];
     const int h = head_begin + blockIdx.y;
     const int kv = h / group;
     const int n = *k_keep_p;
     const int r0 = blockIdx.x * G_ROWS;
     const int pad_end = min(L, (n + 127) / 128 * 128);
+    if (out) {
+        // fused zero-fill: output rows t in [r0, r0 + 64) the selection dropped
+        // (scatter_rows' zero rows, tensor_ops.cpp:107) -- a second independent
+        // HBM stream in the same launch
+        const int32_t* inv_h = inv + (size_t)h * L;
+        for (int e = threadIdx.x; e < G_ROWS * chunks; e += 256) {
+            const int t = r0 + e / chunks, c = e % chunks;
+            if (t < L && __ldg(inv_h + t) < 0) out[((size_t)h * L + t) * chunks + c] = V{};
+        }
+    }
     if (r0 >= pad_end) return;
     if (threadIdx.x < G_ROWS) {
         const int r = r0 + threadIdx.x;
@@ -170,26 +182,32 @@ int launch_zero_unselected(const tsa_desc& d, const int32_t* inv, void* out, cud
 template <typename V>
 static int gather_t(const tsa_desc& d, const void* q, const void* k, const void* v,
                     const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
-                    cudaStream_t st) {
+                    const int32_t* inv, void* out, cudaStream_t st) {
     const int L = d.seq_len;
     const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / sizeof(V));
     const int nh = d.head_end - d.head_begin;
     dim3 grid((L + 63) / 64, nh);
     gather_kernel<V><<<grid, 256, 0, st>>>((const V*)q, (const V*)k, (const V*)v, idx, k_keep,
                                            (V*)qc, (V*)kc, (V*)vc, L, d.n_heads / d.n_kv_heads,
-                                           chunks, d.head_begin);
+                                           chunks, d.head_begin, inv, (V*)out);
     TSA_LAUNCH_CHECK("gather");
     return 0;
+}
+
+int launch_gather_zero(const tsa_desc& d, const void* q, const void* k, const void* v,
+                       const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
+                       const int32_t* inv, void* out, cudaStream_t st) {
+    switch (unit_bytes(d)) {
+        case 16: return gather_t<uint4>(d, q, k, v, idx, k_keep, qc, kc, vc, inv, out, st);
+        case 4: return gather_t<uint32_t>(d, q, k, v, idx, k_keep, qc, kc, vc, inv, out, st);
+        default: return gather_t<uint16_t>(d, q, k, v, idx, k_keep, qc, kc, vc, inv, out, st);
+    }
 }
 
 int launch_gather(const tsa_desc& d, const void* q, const void* k, const void* v,
                   const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
                   cudaStream_t st) {
-    switch (unit_bytes(d)) {
-        case 16: return gather_t<uint4>(d, q, k, v, idx, k_keep, qc, kc, vc, st);
-        case 4: return gather_t<uint32_t>(d, q, k, v, idx, k_keep, qc, kc, vc, st);
-        default: return gather_t<uint16_t>(d, q, k, v, idx, k_keep, qc, kc, vc, st);
-    }
+    return launch_gather_zero(d, q, k, v, idx, k_keep, qc, kc, vc, nullptr, nullptr, st);
 }
 
 template <typename V>

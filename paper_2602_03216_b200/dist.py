@@ -111,6 +111,11 @@ class CudaBackend:
                                        _ptr(self.idx), _ptr(k_keep), None, _ptr(self.kc),
                                        _ptr(self.vc), _stream(self.device)))
 
+    def gather_kv_zero(self, k, v, k_keep, out_local):
+        _lib.check(self.lib.tsa_gather_zero(C.byref(self.local), _ptr(k), _ptr(v), _ptr(self.idx),
+                                            _ptr(k_keep), _ptr(self.kc), _ptr(self.vc),
+                                            _ptr(self.inv), _ptr(out_local), _stream(self.device)))
+
     def attend_indexed(self, q, k_keep, out_local):
         _lib.check(self.lib.tsa_attend_indexed(C.byref(self.local), _ptr(q), _ptr(self.kc),
                                                _ptr(self.vc), _ptr(self.idx), _ptr(k_keep),
@@ -191,12 +196,11 @@ class ShardedSparseAttention:
         b.select(self.s_local, k_keep)
         mark("select")
         if getattr(b, "fused", False):
-            # K/V compress, then attend with Q gathered by TMA gather4 and the
-            # output rows stored at their original positions; dropped rows zeroed
-            b.zero_unselected(self.out_local)
-            mark("zero_fill")
-            b.gather_kv(k, v, k_keep)
-            mark("gather")
+            # K/V compress + zero the dropped rows (one launch), then attend with
+            # Q gathered by TMA gather4 and the output rows stored at their
+            # original positions
+            b.gather_kv_zero(k, v, k_keep, self.out_local)
+            mark("gather_zero")
             b.attend_indexed(q, k_keep, self.out_local)
             mark("attend")
         else:

@@ -375,3 +375,25 @@ def test_heavy_tailed_layer_bf16_vs_oracle(cuda, port):
     o = host(out)
     for hh in (0, 3, 6):
         assert parity.rel_l2(o[hh], ref[hh]) <= parity.BF16_REL_L2
+
+
+@pytest.mark.parametrize("dtype,L", [(torch.bfloat16, 3000), (torch.float32, 1500)])
+def test_sharded_step_world1_matches_layer_bitwise(cuda, dtype, L):
+    """dist.ShardedSparseAttention (stage entry points: fused K/V gather +
+    zero-fill, indexed attend) equals tsa_sparse_attention_layer bit for bit,
+    and rows the selection dropped are +0."""
+    from paper_2602_03216_b200 import workloads
+    from paper_2602_03216_b200.dist import ShardedSparseAttention
+    q, k, v = workloads.heavy_tailed_heads(8, 2, L, 128, seed=4)
+    q, k, v = (t.to(dtype) for t in (q, k, v))
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.02)
+    out, st = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), plan)
+    lay = ShardedSparseAttention(8, 2, L, 128, dtype, plan, device=q.device)
+    o2 = lay.step(q, k, v)
+    torch.cuda.synchronize()
+    assert lay.k_keep == st.k_keep < L
+    assert torch.equal(o2.view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
+                       out.view(torch.int16 if dtype == torch.bfloat16 else torch.int32))
+    keep = torch.zeros(8, L, dtype=torch.bool, device=q.device)
+    keep.scatter_(1, st.selection.indices.long(), True)
+    assert bool((o2[~keep] == 0).all())
