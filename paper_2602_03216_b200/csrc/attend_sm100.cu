@@ -91,9 +91,49 @@ __device__ __forceinline__ void issue_pv_half(uint32_t t_o, uint32_t t_p, uint32
     }
 }
 
+// P = 2^(x*scale - m) for one 128-key S row held in registers: packed f32x2
+// scale (FFMA2), the exponential split between MUFU.EX2 and a polynomial on
+// the FMA pipe (pairs set in kPolyMask, per 32-key chunk; the diagonal tile,
+// which carries the -inf causal mask, uses kPolyMask = 0), 4 packed partial
+// row sums, bf16 pack into S columns [0, 64) (tcgen05.st) with P released to
+// the MMA warp in two 64-key halves (p_full[0], p_full[1]) so PV on keys 0..63
+// overlaps the exponentials of keys 64..127.
+template <uint32_t kPolyMask>
+__device__ __forceinline__ void exp_pack_row(const uint32_t (&r)[BN], uint64_t sc2, uint64_t nm2,
+                                             uint32_t t_s, uint64_t* p_full, uint64_t (&ps)[4]) {
+#pragma unroll
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            uint64_t x = fma2(f2(__uint_as_float(r[c0 + 2 * e]), __uint_as_float(r[c0 + 2 * e + 1])),
+                              sc2, nm2);
+            float x0, x1, p0, p1;
+            f2_split(x, x0, x1);
+            if (kPolyMask >> e & 1u) {
+                x = ex2_poly2(f2(fmaxf(x0, -127.0f), fmaxf(x1, -127.0f)));
+                f2_split(x, p0, p1);
+            } else {
+                p0 = ex2_approx(x0);
+                p1 = ex2_approx(x1);
+                x = f2(p0, p1);
+            }
+            ps[e & 3] = add2(ps[e & 3], x);
+            pk[e] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(t_s + c0 / 2, pk);
+        if (c0 == 32 || c0 == 96) {
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&p_full[c0 == 96]);
+        }
+    }
+}
+
 // Softmax / correction / epilogue for one 128-row query tile (tile 0 = A, 1 = B).
 // Output row of compressed row qi: the compressed buffer (row q_row0 + local
 // row) or, for the fused path, the original position h*L + idx[h, qi].
+template <uint32_t kPolyMask>
 __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32_t warp,
                                              uint32_t lane, int tA, int tB, bool hasB, int n,
                                              int q_row0, float scale_log2,
@@ -125,14 +165,19 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
                 for (int c = 0; c < BN; ++c)
                     if (c > lim) r[c] = __float_as_uint(-INFINITY);
             }
-            // row max with 8 independent partial maxima (ILP)
+            // row max: 8 independent partial maxima, 3-input FMNMX3
             float pm[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) pm[e] = __uint_as_float(r[e]);
+            for (int e = 0; e < 8; ++e)
+                pm[e] = max3f(__uint_as_float(r[e]), __uint_as_float(r[8 + e]),
+                              __uint_as_float(r[16 + e]));
 #pragma unroll
-            for (int c = 8; c < BN; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(r[c]));
-            const float tmax = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                                     fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) *
+            for (int c = 24; c < BN; c += 16)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    pm[e] = max3f(pm[e], __uint_as_float(r[c + e]), __uint_as_float(r[c + 8 + e]));
+            const float tmax = max3f(max3f(pm[0], pm[1], pm[2]), max3f(pm[3], pm[4], pm[5]),
+                                     fmaxf(pm[6], pm[7])) *
                                scale_log2;
             float m_use = m_run;
             bool rescale = false;
@@ -144,43 +189,35 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
             if (__any_sync(0xffffffffu, rescale)) {
                 // PV(j-1) is complete: S(j) was issued after it (commit semantics)
                 const float alpha = rescale ? ex2_approx(m_run - m_use) : 1.0f;
+                const uint64_t alpha2 = f2(alpha, alpha);
 #pragma unroll
                 for (int c0 = 0; c0 < HD; c0 += 32) {
                     uint32_t ro[32];
                     tmem_ld32(t_o + c0, ro);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        ro[e] = __float_as_uint(__uint_as_float(ro[e]) * alpha);
+                    for (int e = 0; e < 32; e += 2) {
+                        float a, b;
+                        f2_split(fma2(f2(__uint_as_float(ro[e]), __uint_as_float(ro[e + 1])),
+                                      alpha2, 0ull),
+                                 a, b);
+                        ro[e] = __float_as_uint(a);
+                        ro[e + 1] = __float_as_uint(b);
+                    }
                     tmem_st32(t_o + c0, ro);
                 }
                 if (rescale) l_run *= alpha;
             }
             m_run = m_use;
-            // P = 2^(x*scale - m), 8 partial row sums, packed bf16 into S columns [0, 64)
-            float ps[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) ps[e] = 0.0f;
-#pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                uint32_t pk[16];
-#pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    const float p0 = ex2_approx(fmaf(__uint_as_float(r[c0 + e]), scale_log2, -m_use));
-                    const float p1 = ex2_approx(fmaf(__uint_as_float(r[c0 + e + 1]), scale_log2, -m_use));
-                    ps[(e >> 1) & 7] += p0 + p1;
-                    pk[e / 2] = pack_bf16x2(p0, p1);
-                }
-                tmem_st16(t_s + c0 / 2, pk);
-                if (c0 == 32 || c0 == 96) {
-                    // release P in two 64-key halves: PV on keys 0..63 overlaps
-                    // the exponentials of keys 64..127
-                    tmem_wait_st();
-                    tc_fence_before();
-                    mbar_arrive(&sm.p_full[tile][c0 == 96]);
-                }
-            }
-            l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+            const uint64_t sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_use, -m_use);
+            uint64_t ps[4] = {0ull, 0ull, 0ull, 0ull};
+            if (j == my_t)
+                exp_pack_row<0u>(r, sc2, nm2, t_s, sm.p_full[tile], ps);
+            else
+                exp_pack_row<kPolyMask>(r, sc2, nm2, t_s, sm.p_full[tile], ps);
+            float l0, l1;
+            f2_split(add2(add2(ps[0], ps[1]), add2(ps[2], ps[3])), l0, l1);
+            l_run += l0 + l1;
         }
         // epilogue: wait for the last PV, O / l -> bf16 -> global
         mbar_wait(&sm.o_done[tile], my_t & 1);
@@ -216,7 +253,7 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
 // per-head buffers, and O rows are stored at their original positions.
 // (Gathering K/V with gather4 as well costs 128 TMA requests per KV step and
 // measured 2.3x slower on B200; see profiles/r1/README.md.)
-template <bool kIndexed>
+template <bool kIndexed, uint32_t kPolyMask>
 __global__ void __launch_bounds__(kThreads, 1)
 attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ n_dev,
@@ -268,7 +305,7 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (warp < 8) {
         // ------------------------------------------------------ softmax warps
         asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-        softmax_role(sm, tmem, warp, lane, tA, tB, hasB, n, q_row0, scale_log2, o,
+        softmax_role<kPolyMask>(sm, tmem, warp, lane, tA, tB, hasB, n, q_row0, scale_log2, o,
                      kIndexed ? idx + (size_t)h * rows_per_head : nullptr,
                      (size_t)h * rows_per_head);
         tc_fence_before();
@@ -443,6 +480,34 @@ bool attend_sm100_supported(const tsa_desc& d) { return d.dtype == TSA_BF16 && d
 
 namespace {
 
+// Which exponential pairs of each 32-key chunk run on the FMA pipe
+// (TSA_EXP_POLY = 0 / 25 / 37 / 50 percent; a tuning knob, default 37.5 %).
+uint32_t poly_mask() {
+    static const uint32_t m = [] {
+        const char* e = std::getenv("TSA_EXP_POLY");
+        const int pct = e ? std::atoi(e) : 37;
+        return pct <= 0 ? 0x0000u : pct <= 25 ? 0x1111u : pct <= 37 ? 0x2929u : 0x5555u;
+    }();
+    return m;
+}
+
+template <bool kIndexed, uint32_t kPolyMask>
+void run_kernel(dim3 grid, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                const CUtensorMap& mv, const int32_t* n_dev, int32_t n_const, int32_t kv_group,
+                int32_t rows_per_head, int32_t kv_rows_per_head, int head_begin, float scale_log2,
+                void* o, const int32_t* idx) {
+    const int smem = (int)sizeof(AttnSmem) + 1024;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(attend_sm100_kernel<kIndexed, kPolyMask>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_set = true;
+    }
+    attend_sm100_kernel<kIndexed, kPolyMask><<<grid, kThreads, smem, st>>>(
+        mq, mk, mv, n_dev, n_const, kv_group, rows_per_head, kv_rows_per_head, head_begin,
+        scale_log2, (__nv_bfloat16*)o, idx);
+}
+
 template <bool kIndexed>
 int launch_impl(const tsa_desc& d, const void* q, const void* k, const void* v,
                 const int32_t* idx, const int32_t* n_dev, int32_t n_const, int32_t kv_group,
@@ -458,19 +523,30 @@ int launch_impl(const tsa_desc& d, const void* q, const void* k, const void* v,
         return rc;
     if ((rc = make_bf16_map_2d(&mk, k, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
     if ((rc = make_bf16_map_2d(&mv, v, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
-    const int smem = (int)sizeof(AttnSmem) + 1024;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(attend_sm100_kernel<kIndexed>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_set = true;
-    }
     const int max_tiles = (rows_per_head + BM - 1) / BM;
     dim3 grid((max_tiles + 1) / 2, nh);
     const float scale_log2 = (1.0f / sqrtf((float)HD)) * 1.4426950408889634f;
-    attend_sm100_kernel<kIndexed><<<grid, kThreads, smem, st>>>(
-        mq, mk, mv, n_dev, n_const, kv_group, rows_per_head, kv_rows_per_head, d.head_begin,
-        scale_log2, (__nv_bfloat16*)o, idx);
+    switch (poly_mask()) {
+        case 0x0000u:
+            run_kernel<kIndexed, 0x0000u>(grid, st, mq, mk, mv, n_dev, n_const, kv_group,
+                                          rows_per_head, kv_rows_per_head, d.head_begin,
+                                          scale_log2, o, idx);
+            break;
+        case 0x1111u:
+            run_kernel<kIndexed, 0x1111u>(grid, st, mq, mk, mv, n_dev, n_const, kv_group,
+                                          rows_per_head, kv_rows_per_head, d.head_begin,
+                                          scale_log2, o, idx);
+            break;
+        case 0x5555u:
+            run_kernel<kIndexed, 0x5555u>(grid, st, mq, mk, mv, n_dev, n_const, kv_group,
+                                          rows_per_head, kv_rows_per_head, d.head_begin,
+                                          scale_log2, o, idx);
+            break;
+        default:
+            run_kernel<kIndexed, 0x2929u>(grid, st, mq, mk, mv, n_dev, n_const, kv_group,
+                                          rows_per_head, kv_rows_per_head, d.head_begin,
+                                          scale_log2, o, idx);
+    }
     TSA_LAUNCH_CHECK(kIndexed ? "attend_sm100_indexed" : "attend_sm100");
     return 0;
 }

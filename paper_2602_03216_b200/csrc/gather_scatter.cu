@@ -36,27 +36,27 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
                                                      const int32_t* __restrict__ inv,
                                                      V* __restrict__ out) {
     __shared__ int32_t rows[G_ROWS];
+    __shared__ bool drop[G_ROWS];
     const int h = head_begin + blockIdx.y;
     const int kv = h / group;
     const int n = *k_keep_p;
     const int r0 = blockIdx.x * G_ROWS;
     const int pad_end = min(L, (n + 127) / 128 * 128);
-    if (out) {
-        // fused zero-fill: output rows t in [r0, r0 + 64) the selection dropped
-        // (scatter_rows' zero rows, tensor_ops.cpp:107) -- a second independent
-        // HBM stream in the same launch
-        const int32_t* inv_h = inv + (size_t)h * L;
-        for (int e = threadIdx.x; e < G_ROWS * chunks; e += 256) {
-            const int t = r0 + e / chunks, c = e % chunks;
-            if (t < L && __ldg(inv_h + t) < 0) out[((size_t)h * L + t) * chunks + c] = V{};
-        }
-    }
-    if (r0 >= pad_end) return;
+    const bool gather = r0 < pad_end;
+    if (!gather && !out) return;
     if (threadIdx.x < G_ROWS) {
         const int r = r0 + threadIdx.x;
-        rows[threadIdx.x] = r < n ? idx[(size_t)h * L + r] : -1;
+        rows[threadIdx.x] = gather && r < n ? idx[(size_t)h * L + r] : -1;
+        // fused zero-fill: output rows the selection dropped (scatter_rows'
+        // zero rows, tensor_ops.cpp:107): fire-and-forget stores beside the gather
+        if (out) drop[threadIdx.x] = r < L && __ldg(inv + (size_t)h * L + r) < 0;
     }
     __syncthreads();
+    if (out) {
+        for (int e = threadIdx.x; e < G_ROWS * chunks; e += 256)
+            if (drop[e / chunks]) out[((size_t)h * L + r0) * chunks + e] = V{};
+    }
+    if (!gather) return;
     const int total = G_ROWS * chunks;
     constexpr int U = 4;
     for (int e0 = threadIdx.x; e0 < total; e0 += 256 * U) {

@@ -289,6 +289,57 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// ---- packed f32x2 arithmetic (FFMA2 / FADD2: two lanes of work per issue slot)
+// and 3-input max (FMNMX3).  Measured on B200 (tools/probes/pipe_probe.cu):
+// FFMA2/FADD2/FMNMX/FMNMX3/F2FP issue at 0.5 / clk / SM sub-partition, FFMA
+// at 1, MUFU.EX2 at 1/8 -- the exponential is the softmax's bottleneck pipe.
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_split(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t add2_rm(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// 2^x for a pair on the FMA pipe (Cody-Waite split + degree-3 minimax
+// polynomial on [0, 1), max relative error 8.6e-5 -- far below the bf16
+// rounding P is stored with).  x >= -127 (callers clamp), finite.
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
+    const uint64_t kMagic = 0x4B4000004B400000ull;     // 1.5 * 2^23: floor lands in the mantissa
+    const uint64_t kNegMagic = 0xCB400000CB400000ull;
+    const uint64_t t = add2_rm(x, kMagic);               // bits = magic + floor(x)
+    const uint64_t fl = add2(t, kNegMagic);              // floor(x), exact
+    const uint64_t fr = fma2(fl, 0xBF800000BF800000ull, x);  // x - floor(x) in [0, 1), exact
+    uint64_t p = fma2(f2(0.0770652f, 0.0770652f), fr, f2(0.227647f, 0.227647f));
+    p = fma2(p, fr, f2(0.69511634f, 0.69511634f));
+    p = fma2(p, fr, f2(1.0f, 1.0f));
+    // scale by 2^floor(x): add floor(x) to the exponent field (magic << 23 wraps to 0)
+    const uint32_t lo = (uint32_t)p + ((uint32_t)t << 23);
+    const uint32_t hi = (uint32_t)(p >> 32) + ((uint32_t)(t >> 32) << 23);
+    return ((uint64_t)hi << 32) | lo;
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
