@@ -165,14 +165,13 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
                 for (int c = 0; c < BN; ++c)
                     if (c > lim) r[c] = __float_as_uint(-INFINITY);
             }
-            // row max: 8 independent partial maxima, 3-input FMNMX3
+            // row max: 8 independent partial maxima, 3-input FMNMX3 (columns
+            // 0..15 seed them, then 7 steps of 16 columns cover 16..127)
             float pm[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-                pm[e] = max3f(__uint_as_float(r[e]), __uint_as_float(r[8 + e]),
-                              __uint_as_float(r[16 + e]));
+            for (int e = 0; e < 8; ++e) pm[e] = fmaxf(__uint_as_float(r[e]), __uint_as_float(r[8 + e]));
 #pragma unroll
-            for (int c = 24; c < BN; c += 16)
+            for (int c = 16; c < BN; c += 16)
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
                     pm[e] = max3f(pm[e], __uint_as_float(r[c + e]), __uint_as_float(r[c + 8 + e]));
@@ -349,6 +348,9 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 a3 = r0 + 3 < n ? __ldg(idx_h + r0 + 3) : last;
             };
             const int q_base_row = h * rows_per_head;  // original Q rows of head h
+            // post the byte count before any lane's copy can complete_tx
+            if (lane == 0) mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
+            __syncwarp();
             for (int t = 0; t < (hasB ? 2 : 1); ++t) {
                 int a0, a1, a2, a3;
                 rows4((tA + t) * BM + 4 * (int)lane, a0, a1, a2, a3);
@@ -358,7 +360,6 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 tma_gather4(dst + HALF_BYTES, &tm_q, &sm.q_full, 64, q_base_row + a0,
                             q_base_row + a1, q_base_row + a2, q_base_row + a3);
             }
-            if (lane == 0) mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
             // K/V: tiled loads of the compressed per-head buffers (kc/vc from the
             // gather kernel) -- 4 TMA requests per KV step instead of 128 gathers
             if (lane == 0) {
@@ -481,11 +482,11 @@ bool attend_sm100_supported(const tsa_desc& d) { return d.dtype == TSA_BF16 && d
 namespace {
 
 // Which exponential pairs of each 32-key chunk run on the FMA pipe
-// (TSA_EXP_POLY = 0 / 25 / 37 / 50 percent; a tuning knob, default 37.5 %).
+// (TSA_EXP_POLY = 0 / 25 / 37 / 50 percent; a tuning knob, default 0: measured slower on B200, profiles/r1/poly_sweep.log).
 uint32_t poly_mask() {
     static const uint32_t m = [] {
         const char* e = std::getenv("TSA_EXP_POLY");
-        const int pct = e ? std::atoi(e) : 37;
+        const int pct = e ? std::atoi(e) : 0;
         return pct <= 0 ? 0x0000u : pct <= 25 ? 0x1111u : pct <= 37 ? 0x2929u : 0x5555u;
     }();
     return m;

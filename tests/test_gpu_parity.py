@@ -361,6 +361,34 @@ def test_tcgen05_attention_running_max_rescales(cuda, port):
         assert parity.rel_l2(host(out[i]), ref) <= parity.BF16_REL_L2
 
 
+@pytest.mark.parametrize("indexed", [False, True])
+def test_tcgen05_attention_all_logits_very_negative(cuda, indexed):
+    """Every logit ~ -1100 (K = -Q, |q.k| large): softmax is shift-invariant, so
+    each row is the mean of its causal V prefix (test_attention.cpp:126-158's
+    Q = K = 0 case, shifted).  Guards the row max: a max that is not exactly
+    the largest unmasked logit (e.g. an extra 0 or stale column) underflows
+    every exponential and divides 0 by 0."""
+    H, L, d = 2, 384, 128
+    rng = np.random.default_rng(3)
+    u = np.where(rng.uniform(size=d) < 0.5, -1.0, 1.0)
+    q = np.broadcast_to(3.0 * u, (H, L, d)).astype(np.float32)
+    k = np.broadcast_to(-3.0 * u, (1, L, d)).astype(np.float32)
+    v = rng.uniform(-1, 1, (1, L, d)).astype(np.float32)
+    h = heads_of(q, k, v, torch.bfloat16)
+    vv = host(h.v)[0].astype(np.float64)
+    ref = np.cumsum(vv, axis=0) / np.arange(1, L + 1)[:, None]
+    if indexed:  # the fused path at tau = 0 (every token kept)
+        plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.0)
+        out, st = tsa.sparse_attention_layer(h, plan)
+        assert st.k_keep == L
+    else:
+        out = torch.stack([tsa.dense_causal_attention(h.q[i], h.k[0], h.v[0]) for i in range(H)])
+    o = host(out)
+    assert np.isfinite(o).all()
+    for i in range(H):
+        assert parity.rel_l2(o[i], ref) <= parity.BF16_REL_L2
+
+
 def test_heavy_tailed_layer_bf16_vs_oracle(cuda, port):
     from paper_2602_03216_b200 import workloads
     L = 8192
