@@ -58,6 +58,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-dense", action="store_true")
+    p.add_argument("--extra", type=str, default="cfg2,cfg5",
+                   help="other BASELINE configs measured after the headline (comma list: cfg2 = "
+                        "32K uniform tau sweep, cfg5 = Llama-3-70B heads at 128K; '' = none)")
     p.add_argument("--calibrate", action="store_true",
                    help="print k/L at the paper's tau levels for a sigma grid and exit")
     return p.parse_args()
@@ -178,9 +181,10 @@ def run_ours(args):
                   v[sh.kv0:sh.kv1].contiguous())
     stream = torch.cuda.current_stream(device)
 
-    def timed(obj, steps, warmup, dense=False, stage_events=False):
+    def timed(obj, steps, warmup, dense=False, stage_events=False, graph=False):
+        run = obj.step_graphed if graph else obj.step
         for _ in range(warmup):
-            obj.step(ql, kl, vl, dense=dense)
+            run(ql, kl, vl, dense=dense)
         torch.cuda.synchronize()
         barrier(world)
         names, evs = [], []
@@ -196,11 +200,16 @@ def run_ours(args):
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
         for _ in range(steps):
-            obj.step(ql, kl, vl, marks=mark if stage_events else None, dense=dense)
+            if graph:
+                run(ql, kl, vl, dense=dense)
+            else:
+                run(ql, kl, vl, marks=mark if stage_events else None, dense=dense)
         end.record(stream)
         torch.cuda.synchronize()
         barrier(world)
         launches = lib.tsa_kernel_launches() - launches0
+        if graph and obj.shard.world == 1:  # replays bypass the library's counter
+            launches = obj.graph_kernels * steps
         total = start.elapsed_time(end)
         stages = {}
         if stage_events:
@@ -212,22 +221,26 @@ def run_ours(args):
         ms = max_over_ranks(total / steps, world, device)
         return ms, stages, launches
 
+    # per-stage split: eager launches with CUDA events between the stages
+    eager_ms, stages, _ = timed(layer, args.steps, args.warmup, stage_events=True)
+    # the timed step: the whole chain replayed from a CUDA graph (world == 1;
+    # sharded runs launch eagerly around the NCCL all-gathers)
     with ClockSampler(local) as clk:
-        sparse_ms, stages, launches = timed(layer, args.steps, args.warmup, stage_events=True)
+        sparse_ms, _, launches = timed(layer, args.steps, args.warmup, graph=True)
     k_keep = layer.k_keep
     clocks = clk.summary()
     hbm, pk_burst, pk_sust, pk_kind = measured_peaks()
 
     dense_ms = None
     if not args.no_dense:
-        dense_ms, _, _ = timed(layer, args.steps, args.warmup, dense=True)
+        dense_ms, _, _ = timed(layer, args.steps, args.warmup, dense=True, graph=True)
     sweep = []
     for t in [float(x) for x in args.sweep.split(",") if x.strip()]:
         if t == args.tau:
             sweep.append({"tau": t, "k_keep": k_keep, "ms": round(sparse_ms, 3)})
             continue
         other = make(t)
-        ms_t, _, _ = timed(other, max(2, args.steps // 2), 2)
+        ms_t, _, _ = timed(other, max(2, args.steps // 2), 2, graph=True)
         sweep.append({"tau": t, "k_keep": other.k_keep, "ms": round(ms_t, 3)})
         del other
     if dense_ms:
@@ -263,6 +276,12 @@ def run_ours(args):
             hbm_rows[name] = {"ms": round(stages[name], 4), "GB/s": round(gbs, 1),
                               "frac": round(gbs / hbm, 4)}
 
+    extras = {}
+    for name in [x.strip() for x in args.extra.split(",") if x.strip()]:
+        extras[name] = run_extra(name, args, tsa, workloads, ShardedSparseAttention, rank, world,
+                                 device)
+        torch.cuda.empty_cache()
+
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, tsa, ql, kl, vl, rank, world, device, args.tau)
@@ -287,13 +306,81 @@ def run_ours(args):
             "tokens_per_s": round(L / (sparse_ms * 1e-3), 1),
             "dense_ms": round(dense_ms, 3) if dense_ms else None,
             "speedup_vs_dense": round(dense_ms / sparse_ms, 3) if dense_ms else None,
-            "tau_sweep": sweep, "stages_ms": {kk: round(vv, 4) for kk, vv in stages.items()},
+            "tau_sweep": sweep, "eager_ms": round(eager_ms, 3),
+            "stages_ms": {kk: round(vv, 4) for kk, vv in stages.items()},
             "hbm_stages": hbm_rows, "roofline": roofline, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
+            "other_configs": extras,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def time_layer(layer, ql, kl, vl, steps, warmup, world, device, dense=False):
+    """CUDA-event latency of the graph-replayed layer step (ms, max over ranks)."""
+    stream = torch.cuda.current_stream(device)
+    for _ in range(warmup):
+        layer.step_graphed(ql, kl, vl, dense=dense)
+    torch.cuda.synchronize()
+    barrier(world)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        layer.step_graphed(ql, kl, vl, dense=dense)
+    e.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(s.elapsed_time(e) / steps, world, device)
+
+
+EXTRA = {
+    # BASELINE configs[1]: L = 32K, uniform inputs (the reference's own generator
+    # family), tau sweep, dense vs sparse on one GPU
+    "cfg2": dict(workload="cfg2: one attention layer, Llama-3-8B heads (32 Q / 8 KV, d=128), "
+                          "L=32768, bf16, uniform[-1,1) inputs, tau sweep",
+                 H=32, Hkv=8, L=32768, gen="uniform", taus=[0.0, 0.25, 0.5, 0.75]),
+    # BASELINE configs[4]: Llama-3-70B heads at 128K (8 Q + 1 KV head per GPU at
+    # 8 GPUs); on N GPUs the heads are sharded N ways
+    "cfg5": dict(workload="cfg5: one attention layer, Llama-3-70B heads (64 Q / 8 KV, d=128), "
+                          "L=131072, bf16, heavy-tailed inputs, paper tau levels",
+                 H=64, Hkv=8, L=131072, gen="heavy", taus=[0.005, 0.01]),
+}
+
+
+def run_extra(name, args, tsa, workloads, Sharded, rank, world, device):
+    """Latency of another BASELINE config: dense and every tau of its sweep,
+    with the per-stage split of the sparse step at the last tau."""
+    c = EXTRA[name]
+    H_, Hkv_, L = c["H"], c["Hkv"], c["L"]
+    if c["gen"] == "uniform":
+        q, k, v = workloads.uniform_heads(H_, Hkv_, L, D, seed=2602, device=device)
+    else:
+        q, k, v = workloads.heavy_tailed_heads(H_, Hkv_, L, D, seed=2602, device=device)
+    steps, warm = max(3, args.steps), 3
+    rows, dense_ms, sh = [], None, None
+    for tau in c["taus"]:
+        plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
+        lay = Sharded(H_, Hkv_, L, D, torch.bfloat16, plan, rank=rank, world=world, device=device)
+        sh = lay.shard
+        ql, kl, vl = (q[sh.h0:sh.h1].contiguous(), k[sh.kv0:sh.kv1].contiguous(),
+                      v[sh.kv0:sh.kv1].contiguous())
+        if dense_ms is None and not args.no_dense:
+            dense_ms = time_layer(lay, ql, kl, vl, steps, warm, world, device, dense=True)
+        ms = time_layer(lay, ql, kl, vl, steps, warm, world, device)
+        kk = lay.k_keep
+        attn_tf = f_attn(kk, D, sh.h_per) / (ms * 1e-3) / 1e12
+        rows.append({"tau": tau, "k_keep": kk, "k_over_L": round(kk / L, 4), "ms": round(ms, 3),
+                     "speedup_vs_dense": round(dense_ms / ms, 3) if dense_ms else None,
+                     "layer_TFLOP_per_s": round(attn_tf, 1),
+                     "tokens_per_s": round(L / (ms * 1e-3), 1)})
+        del lay, ql, kl, vl
+    out = {"workload": c["workload"], "seq_len": L, "n_heads": H_, "n_kv_heads": Hkv_,
+           "heads_per_gpu": sh.h_per, "dense_ms": round(dense_ms, 3) if dense_ms else None,
+           "dense_TFLOP_per_s": round(f_attn(L, D, sh.h_per) / (dense_ms * 1e-3) / 1e12, 1)
+           if dense_ms else None, "tau_sweep": rows}
+    del q, k, v
+    return out
 
 
 def profile_traffic(kernel):

@@ -79,6 +79,10 @@ TSA_API const char* tsa_last_error(void);
 TSA_API const char* tsa_version(void);
 /* Number of kernels this library has launched in the process (all streams). */
 TSA_API uint64_t tsa_kernel_launches(void);
+/* Destroys the CUDA graphs tsa_sparse_attention_layer keeps (one per
+ * descriptor + buffer addresses, at most 16).  Call before freeing buffers a
+ * later allocation could reuse with a different meaning. */
+TSA_API void tsa_release_graphs(void);
 
 /* Bytes of scratch the calls below need for `d` (scores, index lists,
  * compressed Q/K/V/O buffers and selection scratch), 256-B aligned.
@@ -182,7 +186,11 @@ TSA_API int tsa_dense_attention(const tsa_desc* d, const void* q, const void* k,
  * (optional) receives the selection [H x L] int32, k_keep_out (device int32,
  * required) the budget; k_keep_host (optional, pinned) is filled
  * asynchronously for LayerStat.  Multi-GPU callers use the stage entry points
- * with an all-gather of s between tsa_score and tsa_budget. */
+ * with an all-gather of s between tsa_score and tsa_budget.
+ * The chain never waits on the host, so its launches are captured into a CUDA
+ * graph on the first call for a (descriptor, buffer addresses) key and
+ * replayed afterwards (TSA_GRAPHS=0 disables; calls on a capturing stream run
+ * eagerly into the caller's capture). */
 TSA_API int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, const void* v,
                                void* out, int32_t* idx_out, int32_t* k_keep_out,
                                int32_t* k_keep_host, void* ws, void* stream);

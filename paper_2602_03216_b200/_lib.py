@@ -19,7 +19,7 @@ TSA_OK, TSA_ERR_INVALID, TSA_ERR_CUDA = 0, 1, 2
 
 # Every symbol include/tsa_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "tsa_desc_init", "tsa_last_error", "tsa_version", "tsa_kernel_launches", "tsa_workspace_size", "tsa_score",
+    "tsa_desc_init", "tsa_last_error", "tsa_version", "tsa_kernel_launches", "tsa_release_graphs", "tsa_workspace_size", "tsa_score",
     "tsa_budget", "tsa_aggregate_scores", "tsa_coverage_budget", "tsa_select", "tsa_gather",
     "tsa_attend", "tsa_attend_indexed", "tsa_zero_unselected", "tsa_gather_zero", "tsa_scatter",
     "tsa_scatter_rows", "tsa_check", "tsa_token_sparse_attention",
@@ -73,6 +73,7 @@ def load() -> C.CDLL:
         "tsa_last_error": (C.c_char_p, []),
         "tsa_version": (C.c_char_p, []),
         "tsa_kernel_launches": (C.c_uint64, []),
+        "tsa_release_graphs": (None, []),
         "tsa_workspace_size": (C.c_int, [D, C.POINTER(C.c_size_t)]),
         "tsa_score": (C.c_int, [D, P, P, P, P, P]),
         "tsa_budget": (C.c_int, [D, P, P, P, P]),

@@ -14,6 +14,8 @@ static thread_local std::string g_error;
 static std::atomic<unsigned long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+unsigned long long launches_so_far() { return g_launches.load(); }
 
 void set_error(const std::string& msg) { g_error = msg; }
 
@@ -165,6 +167,8 @@ const char* tsa_last_error(void) { return tsa::g_error.c_str(); }
 
 uint64_t tsa_kernel_launches(void) { return tsa::g_launches.load(); }
 
+void tsa_release_graphs(void) { tsa::graph_cache_clear(); }
+
 const char* tsa_version(void) { return "tsa_b200 0.1 (sm_100a)"; }
 
 int tsa_workspace_size(const tsa_desc* d, size_t* bytes) {
@@ -310,12 +314,10 @@ int tsa_dense_attention(const tsa_desc* d, const void* q, const void* k, const v
                            d->seq_len, d->seq_len, out, S(stream));
 }
 
-int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, const void* v,
+static int layer_eager(const tsa_desc* d, const void* q, const void* k, const void* v,
                                void* out, int32_t* idx_out, int32_t* k_keep_out,
-                               int32_t* k_keep_host, void* ws, void* stream) {
-    if (int rc = check_desc(d)) return rc;
-    if (!k_keep_out) return invalid("tsa_sparse_attention_layer: k_keep_out is required");
-    cudaStream_t st = S(stream);
+                               int32_t* k_keep_host, void* ws, cudaStream_t st) {
+    void* stream = st;
     int rc;
     if (d->mode == TSA_MODE_DENSE) {
         if ((rc = launch_write_int(k_keep_out, d->seq_len, st))) return rc;
@@ -353,6 +355,18 @@ int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, 
         if (e != cudaSuccess) return cuda_check(e, "k_keep copy");
     }
     return 0;
+}
+
+int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, const void* v,
+                               void* out, int32_t* idx_out, int32_t* k_keep_out,
+                               int32_t* k_keep_host, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!k_keep_out) return invalid("tsa_sparse_attention_layer: k_keep_out is required");
+    return tsa::graph_launch(*d, {q, k, v, out, idx_out, k_keep_out, k_keep_host, ws}, S(stream),
+                             [&](cudaStream_t st) {
+                                 return layer_eager(d, q, k, v, out, idx_out, k_keep_out,
+                                                    k_keep_host, ws, st);
+                             });
 }
 
 }  // extern "C"

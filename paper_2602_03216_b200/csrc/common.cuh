@@ -4,7 +4,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
+#include <functional>
 #include <string>
 
 #include "../../include/tsa_b200.h"
@@ -19,6 +21,15 @@ int invalid(const std::string& msg);
 int cuda_check(cudaError_t e, const char* what);
 
 void count_launch();
+void add_launches(unsigned long long n);
+unsigned long long launches_so_far();
+
+// graph.cu: capture-once / replay of a launch sequence keyed by the
+// descriptor and the buffer addresses it touches.
+constexpr int kGraphPtrs = 8;
+int graph_launch(const tsa_desc& d, const std::array<const void*, kGraphPtrs>& ptrs,
+                 cudaStream_t st, const std::function<int(cudaStream_t)>& body);
+void graph_cache_clear();
 
 #define TSA_LAUNCH_CHECK(what)                                             \
     do {                                                                   \

@@ -176,6 +176,34 @@ class ShardedSparseAttention:
             parts = list(dst.chunk(self.shard.world, dim=0))
             dist.all_gather(parts, src.contiguous())
 
+    def step_graphed(self, q, k, v, dense: bool = False):
+        """``step`` replayed from a CUDA graph captured on the first call for
+        these input buffers: the chain never waits on the host (k_keep stays
+        on the device), so the launch sequence is fixed and one graph launch
+        replaces ~8 host launches and their gaps.  Single-process only (the
+        NCCL all-gathers of a sharded step run eagerly)."""
+        if self.shard.world > 1:
+            return self.step(q, k, v, dense=dense)
+        key = (q.data_ptr(), k.data_ptr(), v.data_ptr(), dense)
+        graphs = self.__dict__.setdefault("_graphs", {})
+        g = graphs.get(key)
+        if g is None:
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(side):  # warm once outside capture (attributes, maps)
+                self.step(q, k, v, dense=dense)
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            n0 = _lib.load().tsa_kernel_launches()
+            with torch.cuda.graph(g):
+                self.step(q, k, v, dense=dense)
+            # library kernels per replay (captured launches are counted at capture)
+            g.tsa_kernels = _lib.load().tsa_kernel_launches() - n0
+            graphs[key] = g
+        g.replay()
+        self.graph_kernels = g.tsa_kernels
+        return self.out_full
+
     def step(self, q, k, v, marks=None, dense: bool = False):
         mark = marks or (lambda name: None)
         b = self.backend

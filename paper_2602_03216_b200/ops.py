@@ -215,6 +215,9 @@ def _stream(device: torch.device):
     return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+_kd_cache = {}
+
+
 def _workspace(desc: _lib.TsaDesc, device: torch.device) -> torch.Tensor:
     nbytes = C.c_size_t()
     _lib.check(_lib.load().tsa_workspace_size(C.byref(desc), C.byref(nbytes)))
@@ -457,8 +460,14 @@ def sparse_attention_layer(heads: HeadTensors, plan: SparsePlan, layer: int = 0,
     ws = _workspace(desc, dev)
     if out is None:
         out = torch.empty_like(q)
-    idx = torch.empty((heads.n_heads, L), dtype=torch.int32, device=dev) if sparse else None
-    kd = torch.empty(1, dtype=torch.int32, device=dev)
+    if stat:  # the caller keeps the selection: fresh buffers
+        idx = torch.empty((heads.n_heads, L), dtype=torch.int32, device=dev) if sparse else None
+        kd = torch.empty(1, dtype=torch.int32, device=dev)
+    else:  # selection stays in the workspace; stable addresses keep the graph cache warm
+        idx = None
+        kd = _kd_cache.get((dev.type, dev.index))
+        if kd is None:
+            kd = _kd_cache[(dev.type, dev.index)] = torch.empty(1, dtype=torch.int32, device=dev)
     _lib.check(_lib.load().tsa_sparse_attention_layer(
         C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(idx), _ptr(kd), None,
         _ptr(ws), _stream(dev)))

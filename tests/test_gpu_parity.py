@@ -425,3 +425,33 @@ def test_sharded_step_world1_matches_layer_bitwise(cuda, dtype, L):
     keep = torch.zeros(8, L, dtype=torch.bool, device=q.device)
     keep.scatter_(1, st.selection.indices.long(), True)
     assert bool((o2[~keep] == 0).all())
+
+
+def test_graph_replay_matches_eager_bitwise(cuda):
+    """tsa_sparse_attention_layer replays a captured CUDA graph from the
+    second call on (same descriptor + buffers), and ShardedSparseAttention's
+    step_graphed replays a torch graph: both equal the eager stage-by-stage
+    step bit for bit, including after the inputs change in place."""
+    from paper_2602_03216_b200 import _lib, workloads
+    from paper_2602_03216_b200.dist import ShardedSparseAttention
+    L = 2500
+    q, k, v = workloads.heavy_tailed_heads(8, 2, L, 128, seed=9)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.02)
+    h = tsa.HeadTensors(q, k, v)
+    lay = ShardedSparseAttention(8, 2, L, 128, torch.bfloat16, plan, device=q.device)
+    for seed in (9, 10):  # second round: new values in the same buffers
+        if seed == 10:
+            q2, k2, v2 = workloads.heavy_tailed_heads(8, 2, L, 128, seed=seed, sigma=2.0)
+            q.copy_(q2), k.copy_(k2), v.copy_(v2)
+        eager = lay.step(q, k, v).clone()
+        out = torch.empty_like(q)
+        n0 = _lib.load().tsa_kernel_launches()
+        for _ in range(3):
+            tsa.sparse_attention_layer(h, plan, out=out, stat=False)
+            torch.cuda.synchronize()
+            assert torch.equal(out.view(torch.int16), eager.view(torch.int16))
+        assert _lib.load().tsa_kernel_launches() - n0 >= 3 * 5  # replays are counted
+        g = lay.step_graphed(q, k, v).clone()
+        g = lay.step_graphed(q, k, v).clone()
+        assert torch.equal(g.view(torch.int16), eager.view(torch.int16))
+        assert lay.graph_kernels >= 5
