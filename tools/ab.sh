@@ -1,0 +1,9 @@
+#!/bin/bash
+# A/B of two builds in alternating processes: bash tools/ab.sh <dirA> <dirB> [rounds]
+A=$1; B=$2; N=${3:-3}
+for i in $(seq $N); do
+  for d in $A $B; do
+    (cd $d && timeout 300 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --extra "" --sweep "" 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$d', d['value'], 'eager', d['eager_ms'], 'dense', d['dense_ms'], 'x%.3f'%d['speedup_vs_dense'], 'clk', d['clocks']['sm_mhz'], {k: round(v,3) for k,v in d['stages_ms'].items() if v > 0.01})")
+  done
+done
