@@ -37,10 +37,16 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
                                                      V* __restrict__ out) {
     __shared__ int32_t rows[G_ROWS];
     __shared__ bool drop[G_ROWS];
-    const int h = head_begin + blockIdx.y;
+    // block order: the `group` query heads sharing a KV head are adjacent and
+    // take the same 64-row block of their selections, whose token positions
+    // nearly coincide -- the K/V rows they read hit L2 after the first head
+    const int nrb = gridDim.x / group;  // row blocks per head
+    const int hg = blockIdx.x % group, rb = blockIdx.x / group;
+    const int h = head_begin + blockIdx.y * group + hg;
     const int kv = h / group;
     const int n = *k_keep_p;
-    const int r0 = blockIdx.x * G_ROWS;
+    const int r0 = rb * G_ROWS;
+    (void)nrb;
     const int pad_end = min(L, (n + 127) / 128 * 128);
     const bool gather = r0 < pad_end;
     if (!gather && !out) return;
@@ -186,7 +192,8 @@ static int gather_t(const tsa_desc& d, const void* q, const void* k, const void*
     const int L = d.seq_len;
     const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / sizeof(V));
     const int nh = d.head_end - d.head_begin;
-    dim3 grid((L + 63) / 64, nh);
+    const int group = d.n_heads / d.n_kv_heads;  // shards hold whole KV groups
+    dim3 grid((L + 63) / 64 * group, nh / group);
     gather_kernel<V><<<grid, 256, 0, st>>>((const V*)q, (const V*)k, (const V*)v, idx, k_keep,
                                            (V*)qc, (V*)kc, (V*)vc, L, d.n_heads / d.n_kv_heads,
                                            chunks, d.head_begin, inv, (V*)out);

@@ -41,8 +41,7 @@ constexpr int SF_MAX_CHUNKS = 512;
 struct __align__(1024) ScoreSmem {
     uint8_t q[SF_TILE];
     uint8_t k[SF_NS][SF_TILE];
-    float row_m[SF_BM];
-    float row_il[SF_BM];
+    alignas(16) float row_off[SF_BM];  // pass 2: -(m_r + log2 l_r), -inf for padding rows
     uint64_t q_full;
     uint64_t k_full[SF_NS];
     uint64_t k_empty[SF_NS];
@@ -185,23 +184,32 @@ score_pass1(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
                 for (int c = 0; c < SF_BN; ++c)
                     if (key0 + c > limit) x[c] = __float_as_uint(-INFINITY);
             }
+            // row max: 8 partial maxima seeded by columns 0..15, then 7 x 16 columns
             float pm[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) pm[e] = __uint_as_float(x[e]);
+            for (int e = 0; e < 8; ++e) pm[e] = fmaxf(__uint_as_float(x[e]), __uint_as_float(x[8 + e]));
 #pragma unroll
-            for (int c = 8; c < SF_BN; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(x[c]));
-            const float tmax = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                                     fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * scale_log2;
+            for (int c = 16; c < SF_BN; c += 16)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    pm[e] = max3f(pm[e], __uint_as_float(x[c + e]), __uint_as_float(x[c + 8 + e]));
+            const float tmax = max3f(max3f(pm[0], pm[1], pm[2]), max3f(pm[3], pm[4], pm[5]),
+                                     fmaxf(pm[6], pm[7])) * scale_log2;
             const float m_new = fmaxf(m_run, tmax);
             if (m_new != -INFINITY) {
-                float ps[8];
+                // packed f32x2 scale (FFMA2) and partial sums (FADD2)
+                const uint64_t sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_new, -m_new);
+                uint64_t ps[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-                for (int e = 0; e < 8; ++e) ps[e] = 0.0f;
-#pragma unroll
-                for (int c = 0; c < SF_BN; ++c)
-                    ps[c & 7] += ex2_approx(fmaf(__uint_as_float(x[c]), scale_log2, -m_new));
-                const float s = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-                l_run = l_run * ex2_approx(m_run - m_new) + s;
+                for (int c = 0; c < SF_BN; c += 2) {
+                    float y0, y1;
+                    f2_split(fma2(f2(__uint_as_float(x[c]), __uint_as_float(x[c + 1])), sc2, nm2), y0,
+                             y1);
+                    ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], f2(ex2_approx(y0), ex2_approx(y1)));
+                }
+                float s0, s1;
+                f2_split(add2(add2(ps[0], ps[1]), add2(ps[2], ps[3])), s0, s1);
+                l_run = l_run * ex2_approx(m_run - m_new) + (s0 + s1);
                 m_run = m_new;
             }
         }
@@ -236,9 +244,10 @@ score_pass2(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
             const float2 p = part[(size_t)c * SF_BM];
             if (p.y > 0.0f) Ls += p.y * ex2_approx(p.x - M);
         }
-        const bool valid = row / LQ < g.n_heads_tile;
-        sm.row_m[row] = valid ? M : 0.0f;
-        sm.row_il[row] = (valid && Ls > 0.0f) ? 1.0f / Ls : 0.0f;
+        const bool valid = row / LQ < g.n_heads_tile && Ls > 0.0f;
+        // p = 2^(x scale - m) / l = 2^(x scale - (m + log2 l)): the normaliser
+        // folds into the exponent offset (one FFMA per element, no multiply)
+        sm.row_off[row] = valid ? -(M + __log2f(Ls)) : -INFINITY;
     }
     setup(sm, warp);  // includes __syncthreads: row stats visible
     producer_roles<true>(sm, &tm_q, &tm_k, g, L, LQ, warp, lane);
@@ -255,28 +264,38 @@ score_pass2(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
             load_row128(sm.tmem_base + b * 128 + lane_off, x);
             tc_fence_before();
             mbar_arrive(&sm.s_free[b]);
-            // rows r may see this key iff key <= L - lq + r  <=>  r >= key - (L - lq)
+            // rows r may see this key iff key <= L - lq + r  <=>  r >= key - (L - lq);
+            // all but the last tile(s) are visible to every row (warp-uniform test)
             const int r_first = key - (L - LQ);
+            const bool tile_full = (g.kt0 + j) * SF_BN + SF_BN - 1 <= L - LQ;
+            const uint64_t sc2 = f2(scale_log2, scale_log2);
             float acc[HPT_MAX];
 #pragma unroll
             for (int i = 0; i < HPT_MAX; ++i) {
-                float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+                uint64_t a01 = 0ull, a23 = 0ull;
 #pragma unroll
                 for (int rr = 0; rr < LQ; rr += 4) {
                     const int c = i * LQ + rr;
-                    float p[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float e = ex2_approx(
-                            fmaf(__uint_as_float(x[c + u]), scale_log2, -sm.row_m[c + u]));
-                        p[u] = (rr + u >= r_first) ? e * sm.row_il[c + u] : 0.0f;
+                    const float4 off = *reinterpret_cast<const float4*>(&sm.row_off[c]);
+                    float y0, y1, y2, y3;
+                    f2_split(fma2(f2(__uint_as_float(x[c]), __uint_as_float(x[c + 1])), sc2,
+                                  f2(off.x, off.y)), y0, y1);
+                    f2_split(fma2(f2(__uint_as_float(x[c + 2]), __uint_as_float(x[c + 3])), sc2,
+                                  f2(off.z, off.w)), y2, y3);
+                    float p0 = ex2_approx(y0), p1 = ex2_approx(y1), p2 = ex2_approx(y2),
+                          p3 = ex2_approx(y3);
+                    if (!tile_full) {
+                        p0 = rr + 0 >= r_first ? p0 : 0.0f;
+                        p1 = rr + 1 >= r_first ? p1 : 0.0f;
+                        p2 = rr + 2 >= r_first ? p2 : 0.0f;
+                        p3 = rr + 3 >= r_first ? p3 : 0.0f;
                     }
-                    a0 += p[0];
-                    a1 += p[1];
-                    a2 += p[2];
-                    a3 += p[3];
+                    a01 = add2(a01, f2(p0, p1));
+                    a23 = add2(a23, f2(p2, p3));
                 }
-                acc[i] = (a0 + a1) + (a2 + a3);
+                float s0, s1;
+                f2_split(add2(a01, a23), s0, s1);
+                acc[i] = s0 + s1;
             }
             if (key < L) {
 #pragma unroll

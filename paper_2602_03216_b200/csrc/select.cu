@@ -52,9 +52,9 @@ __device__ __constant__ int kBits[3] = {11, 11, 10};
 
 // Block-wide exclusive scan of `v` (one value per thread) -> returns exclusive
 // prefix and writes the block total to *total (all threads).
-template <typename U>
+template <typename U, int NT = BT>
 __device__ U block_excl_scan(U v, U* total) {
-    __shared__ U warp_sums[BT / 32];
+    __shared__ U warp_sums[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     U incl = v;
 #pragma unroll
@@ -65,20 +65,20 @@ __device__ U block_excl_scan(U v, U* total) {
     if (lane == 31) warp_sums[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        U w = warp_sums[lane];
+        U w = lane < NT / 32 ? warp_sums[lane] : U(0);
         U wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const U n = __shfl_up_sync(0xffffffffu, wi, o);
             if (lane >= o) wi += n;
         }
-        warp_sums[lane] = wi - w;  // exclusive prefix of warp totals
+        if (lane < NT / 32) warp_sums[lane] = wi - w;  // exclusive prefix of warp totals
     }
     __syncthreads();
     const U excl = warp_sums[warp] + incl - v;
     // total = exclusive prefix of the last warp + its inclusive sum
     __shared__ U s_total;
-    if (threadIdx.x == BT - 1) s_total = excl + v;
+    if (threadIdx.x == NT - 1) s_total = excl + v;
     __syncthreads();
     *total = s_total;
     return excl;
@@ -91,13 +91,14 @@ __device__ U block_excl_scan(U v, U* total) {
 // mode AGGREGATE_ONLY:       write s_l = headsum / total to sl_out and stop.
 enum { BUDGET_FROM_HEADSUM = 0, BUDGET_FROM_SL = 1, AGGREGATE_ONLY = 2 };
 
+constexpr int BB = 512;  // threads per budget CTA
 constexpr int CL = 8;  // CTAs per cluster: the token axis of one head (or of s_l) is split 8 ways
 
 // Sum of `v` over the block (all threads get it).
-template <typename U>
+template <typename U, int NT = BT>
 __device__ U block_sum(U v) {
     U tot;
-    block_excl_scan<U>(v, &tot);
+    block_excl_scan<U, NT>(v, &tot);
     return tot;
 }
 
@@ -107,10 +108,14 @@ __device__ U block_sum(U v) {
 // cluster barrier, CTA r merges bucket range r across the cluster through
 // DSMEM, range totals decide which CTA holds the crossing, that CTA finds the
 // bucket and broadcasts it into every CTA's shared memory.
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BT, 1)
+template <bool kStaged>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BB, 1)
 budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep,
               int32_t* __restrict__ k_keep, int32_t* __restrict__ status, int mode,
               float* __restrict__ sl_out, int exact_total) {
+    // kStaged: this CTA's slice of headsum (then s_l) lives in shared memory,
+    // so the three histogram levels do not re-read global memory
+    extern __shared__ float staged[];
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
@@ -126,7 +131,7 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
     __shared__ float s_total;
     __shared__ uint32_t res_bucket, res_cnt;
     __shared__ unsigned long long res_mass;
-    __shared__ int s_done, s_rstar;
+    __shared__ int s_rstar;
     __shared__ unsigned long long s_below_r;
     __shared__ uint32_t s_cbelow_r;
     const int S = (L + CL - 1) / CL;
@@ -141,13 +146,13 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
             if (rank == 0) {
                 constexpr int CH = 2048;
                 const int nchunk = (L + CH - 1) / CH;
-                for (int i = tid; i < CH; i += BT) stage[0][i] = i < L ? headsum[i] : 0.0f;
+                for (int i = tid; i < CH; i += BB) stage[0][i] = i < L ? headsum[i] : 0.0f;
                 __syncthreads();
                 float acc = 0.0f;
                 for (int c = 0; c < nchunk; ++c) {
                     if (c + 1 < nchunk) {
                         const int base = (c + 1) * CH;
-                        for (int i = tid; i < CH; i += BT)
+                        for (int i = tid; i < CH; i += BB)
                             stage[(c + 1) & 1][i] = base + i < L ? headsum[base + i] : 0.0f;
                     }
                     if (tid == 0) {
@@ -170,14 +175,20 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
                 if (tid == 0)
                     for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(&s_total, r) = acc;
             }
+            if (kStaged)
+                for (int t = t_begin + tid; t < t_end; t += BB) staged[t - t_begin] = headsum[t];
             cluster.sync();
             total = s_total;
         } else {
             // deterministic parallel f64 reduction (FAST scoring mode): fixed
             // per-CTA partials combined in rank order by every CTA
             double acc = 0.0;
-            for (int t = t_begin + tid; t < t_end; t += BT) acc += (double)headsum[t];
-            acc = block_sum<double>(acc);
+            for (int t = t_begin + tid; t < t_end; t += BB) {
+                const float x = headsum[t];
+                acc += (double)x;
+                if (kStaged) staged[t - t_begin] = x;
+            }
+            acc = block_sum<double, BB>(acc);
             if (tid == 0) part_total = acc;
             cluster.sync();
             double tot = 0.0;
@@ -193,11 +204,16 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
             return;
         }
         if (mode == AGGREGATE_ONLY) {
-            for (int t = t_begin + tid; t < t_end; t += BT) sl_out[t] = __fdiv_rn(headsum[t], total);
+            for (int t = t_begin + tid; t < t_end; t += BB) sl_out[t] = __fdiv_rn(headsum[t], total);
             cluster.sync();
             return;
         }
+        if (kStaged)  // s_l = headsum / total in place (token_coverage.cpp:65)
+            for (int i = tid; i < t_end - t_begin; i += BB) staged[i] = __fdiv_rn(staged[i], total);
+    } else if (kStaged) {
+        for (int t = t_begin + tid; t < t_end; t += BB) staged[t - t_begin] = headsum[t];
     }
+    __syncthreads();
     // ---- coverage crossing ----
     // T = ceil(tau * 2^62); tau = 0 -> k_sparse = 0 (prefix 0 >= 0, :82).
     const double tscaled = ldexp(tau, 62);
@@ -214,17 +230,17 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
     for (int lvl = 0; lvl < 3; ++lvl) {
         const int shift = kShift[lvl], bits = kBits[lvl], nb = 1 << bits, per = nb / CL;
         const int pshift = shift + bits;
-        for (int b = tid; b < nb; b += BT) {
+        for (int b = tid; b < nb; b += BB) {
             hist_cnt[b] = 0;
             hist_mass[b] = 0;
         }
         __syncthreads();
-        for (int base = t_begin; base < t_end; base += BT) {
+        for (int base = t_begin; base < t_end; base += BB) {
             const int t = base + tid;
             uint32_t b = 0xFFFFFFFFu;
             unsigned long long m = 0;
             if (t < t_end) {
-                const float sl = __fdiv_rn(headsum[t], total);
+                const float sl = kStaged ? staged[t - t_begin] : __fdiv_rn(headsum[t], total);
                 const uint32_t key = score_key(sl);
                 if (pshift >= 32 || (key >> pshift) == prefix) {
                     b = (key >> shift) & (nb - 1);
@@ -256,8 +272,8 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
             m_cnt[tid] = mc;
             m_mass[tid] = mm;
         }
-        const uint32_t rc = block_sum<uint32_t>(mc);
-        const unsigned long long rmass = block_sum<unsigned long long>(mm);
+        const uint32_t rc = block_sum<uint32_t, BB>(mc);
+        const unsigned long long rmass = block_sum<unsigned long long, BB>(mm);
         if (tid == 0) {
             range_cnt = rc;
             range_mass = rmass;
@@ -294,8 +310,8 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
             const uint32_t c0 = tid < per ? m_cnt[tid] : 0;
             unsigned long long mtot;
             uint32_t ctot;
-            const unsigned long long mex = block_excl_scan<unsigned long long>(m0, &mtot) + s_below_r;
-            const uint32_t cex = block_excl_scan<uint32_t>(c0, &ctot) + s_cbelow_r;
+            const unsigned long long mex = block_excl_scan<unsigned long long, BB>(m0, &mtot) + s_below_r;
+            const uint32_t cex = block_excl_scan<uint32_t, BB>(c0, &ctot) + s_cbelow_r;
             if (tid < per && mex < need && need <= mex + m0) {
                 for (int r = 0; r < CL; ++r) {
                     *cluster.map_shared_rank(&res_bucket, r) = (uint32_t)(rank * per + tid);
@@ -321,7 +337,6 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
         }
         *k_keep = max(L - k_sparse, min_keep);
     }
-    (void)s_done;
 }
 
 // ---------------------------------------------------------------- select
@@ -507,7 +522,206 @@ select_kernel(const float* __restrict__ s, int L, const int32_t* __restrict__ k_
     }
 }
 
+// ------------------------------------------------ select, slice in shared memory
+// Same algorithm as select_kernel, with each CTA's slice of the head's scores
+// staged once into shared memory as radix keys (forced tokens as the
+// kForcedKey sentinel): the three histogram levels and the two compaction
+// passes then read shared memory instead of re-reading L2 five times, and 512
+// threads per CTA let two clusters share an SM.  Used when a slice fits
+// (ceil(L / CL) <= kSliceMax).
+constexpr int BS = 512;
+constexpr int kSliceMax = 16384;
+constexpr uint32_t kForcedKey = 0xFFFFFFFFu;
+
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(BS, 2)
+select_smem_kernel(const float* __restrict__ s, int L, const int32_t* __restrict__ k_keep_p,
+                   const int32_t* __restrict__ forced, int nf, int fbegin, int head_begin,
+                   int32_t* __restrict__ idx, int32_t* __restrict__ inv) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ uint32_t keys[];  // this CTA's slice
+    const int rank = (int)cluster.block_rank();
+    const int tid = threadIdx.x;
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t m_cnt[2048 / CL];
+    __shared__ uint32_t range_cnt;
+    __shared__ uint32_t res_bucket, res_above;
+    __shared__ int s_rstar;
+    __shared__ uint32_t s_above_r;
+    __shared__ int slice_fg, slice_eq;
+    const int h = head_begin + blockIdx.y;
+    const float* sh = s + (size_t)h * L;
+    const int S = (L + CL - 1) / CL;
+    const int t_begin = min(L, rank * S), t_end = min(L, t_begin + S);
+    const int n_loc = t_end - t_begin;
+    const int k_keep = *k_keep_p;
+    const int n_free = k_keep - nf;
+    // ---- stage keys (8 independent loads in flight per thread) ----
+    for (int i0 = 0; i0 < n_loc; i0 += BS * 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * BS + tid;
+            v[u] = i < n_loc ? __ldg(sh + t_begin + i) : 0.0f;
+        }
+#pragma unroll 4
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * BS + tid;
+            if (i < n_loc)
+                keys[i] = is_forced(t_begin + i, forced, nf, fbegin) ? kForcedKey : score_key(v[u]);
+        }
+    }
+    __syncthreads();
+    uint32_t prefix = 0, need = (uint32_t)max(n_free, 0);
+    if (n_free > 0) {
+        for (int lvl = 0; lvl < 3; ++lvl) {
+            const int shift = kShift[lvl], bits = kBits[lvl], nb = 1 << bits, per = nb / CL;
+            const int pshift = shift + bits;
+            for (int b = tid; b < nb; b += BS) hist[b] = 0;
+            __syncthreads();
+            for (int i0 = 0; i0 < n_loc; i0 += BS) {  // whole warps iterate together
+                const int i = i0 + tid;
+                const uint32_t key = i < n_loc ? keys[i] : kForcedKey;
+                uint32_t b = 0xFFFFFFFFu;
+                if (key != kForcedKey && (pshift >= 32 || (key >> pshift) == prefix))
+                    b = (key >> shift) & (nb - 1);
+                if (__any_sync(0xffffffffu, b != 0xFFFFFFFFu)) {
+                    const uint32_t grp = __match_any_sync(0xffffffffu, b);  // warp-aggregated
+                    if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (tid & 31))
+                        atomicAdd(&hist[b], (uint32_t)__popc(grp));
+                }
+            }
+            cluster.sync();
+            uint32_t mc = 0;
+            if (tid < per) {
+                const int b = rank * per + tid;
+                for (int r = 0; r < CL; ++r) mc += cluster.map_shared_rank(hist, r)[b];
+                m_cnt[tid] = mc;
+            }
+            const uint32_t rc = block_sum<uint32_t, BS>(mc);
+            if (tid == 0) range_cnt = rc;
+            cluster.sync();
+            if (tid == 0) {  // descending over ranks: higher ranks hold higher buckets
+                uint32_t above = 0;
+                int rstar = -1;
+                for (int r = CL - 1; r >= 0; --r) {
+                    const uint32_t cr = *cluster.map_shared_rank(&range_cnt, r);
+                    if (above < need && need <= above + cr) {
+                        rstar = r;
+                        break;
+                    }
+                    above += cr;
+                }
+                s_rstar = rstar;
+                s_above_r = above;
+            }
+            __syncthreads();
+            if (rank == s_rstar) {
+                const int bi = per - 1 - tid;
+                const uint32_t c0 = (tid < per) ? m_cnt[bi] : 0;
+                uint32_t ctot;
+                const uint32_t above = block_excl_scan<uint32_t, BS>(c0, &ctot) + s_above_r;
+                if (tid < per && above < need && need <= above + c0) {
+                    for (int r = 0; r < CL; ++r) {
+                        *cluster.map_shared_rank(&res_bucket, r) = (uint32_t)(rank * per + bi);
+                        *cluster.map_shared_rank(&res_above, r) = above;
+                    }
+                }
+            }
+            cluster.sync();
+            prefix = (prefix << bits) | res_bucket;
+            need -= res_above;
+            cluster.sync();
+        }
+    }
+    const uint32_t vstar = prefix;
+    const bool has_thr = n_free > 0;
+    const int take_eq = has_thr ? (int)need : 0;
+    int fg = 0, eq = 0;
+    for (int i = tid; i < n_loc; i += BS) {
+        const uint32_t key = keys[i];
+        if (key == kForcedKey || (has_thr && key > vstar)) ++fg;
+        else if (has_thr && key == vstar) ++eq;
+    }
+    fg = block_sum<int, BS>(fg);
+    eq = block_sum<int, BS>(eq);
+    if (tid == 0) {
+        slice_fg = fg;
+        slice_eq = eq;
+    }
+    cluster.sync();
+    int base_pos = 0, base_eq = 0;
+    for (int r = 0; r < rank; ++r) {
+        const int fr = *cluster.map_shared_rank(&slice_fg, r);
+        const int er = *cluster.map_shared_rank(&slice_eq, r);
+        base_pos += fr + max(0, min(er, take_eq - base_eq));
+        base_eq += er;
+    }
+    cluster.sync();  // remote reads done before any CTA may exit
+    // ---- ordered compaction: warp ballots + one block scan per 8-item chunk ----
+    int32_t* idx_h = idx + (size_t)h * L;
+    int32_t* inv_h = inv ? inv + (size_t)h * L : nullptr;
+    constexpr int IPT = 8;
+    for (int c0 = 0; c0 < n_loc; c0 += BS * IPT) {
+        uint32_t kbits = 0, ebits = 0;
+        int neq = 0;
+#pragma unroll
+        for (int u = 0; u < IPT; ++u) {
+            const int i = c0 + tid * IPT + u;
+            if (i < n_loc) {
+                const uint32_t key = keys[i];
+                if (key == kForcedKey || (has_thr && key > vstar)) kbits |= 1u << u;
+                else if (has_thr && key == vstar) {
+                    ebits |= 1u << u;
+                    ++neq;
+                }
+            }
+        }
+        int eq_total;
+        int running_eq = block_excl_scan<int, BS>(neq, &eq_total) + base_eq;
+#pragma unroll
+        for (int u = 0; u < IPT; ++u)
+            if ((ebits >> u & 1u) && running_eq++ < take_eq) kbits |= 1u << u;
+        int keep_total;
+        int pos = block_excl_scan<int, BS>(__popc(kbits), &keep_total) + base_pos;
+#pragma unroll
+        for (int u = 0; u < IPT; ++u) {
+            const int i = c0 + tid * IPT + u;
+            if (i >= n_loc) break;
+            const int t = t_begin + i;
+            if (kbits >> u & 1u) {
+                idx_h[pos] = t;
+                if (inv_h) inv_h[t] = pos;
+                ++pos;
+            } else if (inv_h) {
+                inv_h[t] = -1;
+            }
+        }
+        base_pos += keep_total;
+        base_eq += eq_total;
+    }
+}
+
 }  // namespace
+
+static void launch_budget_kernel(const float* v, int L, double tau, int min_keep, int32_t* k_keep,
+                                 int32_t* status, int mode, float* sl_out, int exact_total,
+                                 cudaStream_t st) {
+    const int slice = (L + CL - 1) / CL;
+    if (slice <= kSliceMax) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(budget_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSliceMax * 4);
+            attr = true;
+        }
+        budget_kernel<true><<<CL, BB, slice * 4, st>>>(v, L, tau, min_keep, k_keep, status, mode,
+                                                       sl_out, exact_total);
+    } else {
+        budget_kernel<false><<<CL, BB, 0, st>>>(v, L, tau, min_keep, k_keep, status, mode, sl_out,
+                                                exact_total);
+    }
+}
 
 int launch_write_int(int32_t* dst, int32_t value, cudaStream_t st) {
     write_int_kernel<<<1, 1, 0, st>>>(dst, value);
@@ -520,9 +734,8 @@ int launch_budget(const tsa_desc& d, const float* s, int32_t* k_keep, float* hea
     const int L = d.seq_len;
     headsum_kernel<<<(L + 255) / 256, 256, 0, st>>>(s, headsum, d.n_heads, L);
     TSA_LAUNCH_CHECK("headsum");
-    budget_kernel<<<CL, BT, 0, st>>>(headsum, L, d.tau, min_keep, k_keep, status,
-                                    BUDGET_FROM_HEADSUM, nullptr,
-                                    scoring_mode(d) == TSA_SCORING_REFERENCE ? 1 : 0);
+    launch_budget_kernel(headsum, L, d.tau, min_keep, k_keep, status, BUDGET_FROM_HEADSUM, nullptr,
+                         scoring_mode(d) == TSA_SCORING_REFERENCE ? 1 : 0, st);
     TSA_LAUNCH_CHECK("budget");
     return 0;
 }
@@ -532,16 +745,16 @@ int launch_aggregate(const tsa_desc& d, const float* s, float* sl, float* headsu
     const int L = d.seq_len;
     headsum_kernel<<<(L + 255) / 256, 256, 0, st>>>(s, headsum, d.n_heads, L);
     TSA_LAUNCH_CHECK("headsum");
-    budget_kernel<<<CL, BT, 0, st>>>(headsum, L, 0.0, 1, nullptr, status, AGGREGATE_ONLY, sl,
-                                    scoring_mode(d) == TSA_SCORING_REFERENCE ? 1 : 0);
+    launch_budget_kernel(headsum, L, 0.0, 1, nullptr, status, AGGREGATE_ONLY, sl,
+                         scoring_mode(d) == TSA_SCORING_REFERENCE ? 1 : 0, st);
     TSA_LAUNCH_CHECK("aggregate");
     return 0;
 }
 
 int launch_coverage_from_sl(const tsa_desc& d, const float* sl, int32_t* k_keep, int32_t* status,
                             int min_keep, cudaStream_t st) {
-    budget_kernel<<<CL, BT, 0, st>>>(sl, d.seq_len, d.tau, min_keep, k_keep, status, BUDGET_FROM_SL,
-                                    nullptr, 1);
+    launch_budget_kernel(sl, d.seq_len, d.tau, min_keep, k_keep, status, BUDGET_FROM_SL, nullptr, 1,
+                         st);
     TSA_LAUNCH_CHECK("coverage_budget");
     return 0;
 }
@@ -550,8 +763,21 @@ int launch_select(const tsa_desc& d, const float* s, const int32_t* k_keep, cons
                   int32_t n_forced, int32_t forced_begin, int32_t* idx, int32_t* inv,
                   cudaStream_t st) {
     const int nh = d.head_end - d.head_begin;
-    select_kernel<<<dim3(CL, nh), BT, 0, st>>>(s, d.seq_len, k_keep, forced, n_forced,
-                                               forced_begin, d.head_begin, idx, inv);
+    const int slice = (d.seq_len + CL - 1) / CL;
+    if (slice <= kSliceMax) {
+        const int smem = slice * 4;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(select_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSliceMax * 4);
+            attr = true;
+        }
+        select_smem_kernel<<<dim3(CL, nh), BS, smem, st>>>(s, d.seq_len, k_keep, forced, n_forced,
+                                                           forced_begin, d.head_begin, idx, inv);
+    } else {
+        select_kernel<<<dim3(CL, nh), BT, 0, st>>>(s, d.seq_len, k_keep, forced, n_forced,
+                                                   forced_begin, d.head_begin, idx, inv);
+    }
     TSA_LAUNCH_CHECK("select");
     return 0;
 }

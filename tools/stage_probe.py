@@ -12,10 +12,15 @@ from paper_2602_03216_b200 import workloads  # noqa: E402
 from paper_2602_03216_b200.dist import ShardedSparseAttention  # noqa: E402
 
 L = int(sys.argv[1])
-q, k, v = workloads.heavy_tailed_heads(32, 8, L, 128, seed=2602)
+gen = sys.argv[3] if len(sys.argv) > 3 else "heavy"
+tau = float(sys.argv[4]) if len(sys.argv) > 4 else 0.01
+if gen == "uniform":
+    q, k, v = workloads.uniform_heads(32, 8, L, 128, seed=2602)
+else:
+    q, k, v = workloads.heavy_tailed_heads(32, 8, L, 128, seed=2602)
 dev = torch.device("cuda")
 for scoring in (2, 1):
-    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.01)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
     lay = ShardedSparseAttention(32, 8, L, 128, torch.bfloat16, plan, device=dev, scoring=scoring)
     for it in range(3):
         names, evs = [], []
