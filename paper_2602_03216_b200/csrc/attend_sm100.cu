@@ -67,27 +67,39 @@ __device__ __forceinline__ uint32_t opaque(uint32_t x) {
     return x;
 }
 
+// Shared-memory descriptors differ between the K-steps of one operand only in
+// the start-address field (bits 0-13, address >> 4), which never carries into
+// the LBO field for shared-memory addresses: build the low word once per
+// operand base and add the K-step offset, the high word (SBO = 1 KiB, version,
+// SW128 layout) is a constant.
+__device__ __forceinline__ uint64_t sdesc_from_lo(uint32_t lo) {
+    return (static_cast<uint64_t>(0x40004040u) << 32) | lo;
+}
+__device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr, uint32_t lbo_bytes) {
+    return ((saddr >> 4) & 0x3FFFu) | (((lbo_bytes >> 4) & 0x3FFFu) << 16);
+}
+
 __device__ __forceinline__ void issue_s(uint32_t t_s, uint32_t q_base, uint32_t k_base,
-                                        uint32_t idesc) {
-    q_base = opaque(q_base);
-    k_base = opaque(k_base);
+                                        uint32_t idesc, uint32_t leader) {
+    const uint32_t qlo = sdesc_lo(q_base, 16), klo = sdesc_lo(k_base, 16);
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t off = (kk >> 2) * HALF_BYTES + (kk & 3) * 32;
-        mma_bf16_ss(t_s, sdesc_kmajor_sw128(q_base + off), sdesc_kmajor_sw128(k_base + off), idesc,
-                    kk > 0 ? 1u : 0u);
+        const uint32_t off = ((kk >> 2) * HALF_BYTES + (kk & 3) * 32) >> 4;
+        mma_bf16_ss_p(t_s, sdesc_from_lo(qlo + off), sdesc_from_lo(klo + off), idesc,
+                      kk > 0 ? 1u : 0u, leader);
     }
 }
 
 // O += P[:, 64h .. 64h+63] V[64h .. 64h+63, :] (half h of the 128-key tile).
 __device__ __forceinline__ void issue_pv_half(uint32_t t_o, uint32_t t_p, uint32_t v_base,
-                                              uint32_t idesc, bool accumulate, int half) {
-    v_base = opaque(v_base);
+                                              uint32_t idesc, bool accumulate, int half,
+                                              uint32_t leader) {
+    const uint32_t vlo = sdesc_lo(v_base, HALF_BYTES);
 #pragma unroll
     for (int k2 = 0; k2 < BN / 32; ++k2) {
         const int kk = half * (BN / 32) + k2;
-        mma_bf16_ts(t_o, t_p + kk * 8, sdesc_mnmajor_sw128(v_base + kk * 2048, HALF_BYTES), idesc,
-                    (accumulate || kk > 0) ? 1u : 0u);
+        mma_bf16_ts_p(t_o, t_p + kk * 8, sdesc_from_lo(vlo + ((kk * 2048) >> 4)), idesc,
+                      (accumulate || kk > 0) ? 1u : 0u, leader);
     }
 }
 
@@ -379,7 +391,8 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
     } else if (warp == 9) {
         // ------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        {  // the whole warp runs the loop (warp-uniform state); the elected lane issues
+            const uint32_t L1 = elect_one() ? 1u : 0u;
             const uint32_t idesc_s = idesc_bf16_f32(BM, BN, 0, 0);
             const uint32_t idesc_o = idesc_bf16_f32(BM, HD, 0, 1);
             const uint32_t qa = smem_u32(sm.q[0]), qb = smem_u32(sm.q[1]);
@@ -391,13 +404,13 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // prologue: S(0) for both tiles
             mbar_wait(&sm.k_full[0], 0);
             tc_fence_after();
-            issue_s(tS[0], qa, smem_u32(sm.k[0]), idesc_s);
-            mma_commit(&sm.s_full[0]);
+            issue_s(tS[0], qa, smem_u32(sm.k[0]), idesc_s, L1);
+            mma_commit_p(&sm.s_full[0], L1);
             if (hasB) {
-                issue_s(tS[1], qb, smem_u32(sm.k[0]), idesc_s);
-                mma_commit(&sm.s_full[1]);
+                issue_s(tS[1], qb, smem_u32(sm.k[0]), idesc_s, L1);
+                mma_commit_p(&sm.s_full[1], L1);
             }
-            mma_commit(&sm.k_empty[0]);
+            mma_commit_p(&sm.k_empty[0], L1);
             for (int j = 0; j < nkv; ++j) {
                 const int st = j % NS;
                 const int j1 = j + 1, st1 = j1 % NS;
@@ -407,35 +420,35 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 if (doA(j)) {
                     mbar_wait(&sm.p_full[0][0], j & 1);
                     tc_fence_after();
-                    issue_pv_half(tO[0], tS[0], v_base, idesc_o, j > 0, 0);
+                    issue_pv_half(tO[0], tS[0], v_base, idesc_o, j > 0, 0, L1);
                     mbar_wait(&sm.p_full[0][1], j & 1);
                     tc_fence_after();
-                    issue_pv_half(tO[0], tS[0], v_base, idesc_o, j > 0, 1);
-                    mma_commit(&sm.o_done[0]);
+                    issue_pv_half(tO[0], tS[0], v_base, idesc_o, j > 0, 1, L1);
+                    mma_commit_p(&sm.o_done[0], L1);
                     if (doA(j1)) {
                         mbar_wait(&sm.k_full[st1], (j1 / NS) & 1);
                         tc_fence_after();
-                        issue_s(tS[0], qa, smem_u32(sm.k[st1]), idesc_s);
-                        mma_commit(&sm.s_full[0]);
+                        issue_s(tS[0], qa, smem_u32(sm.k[st1]), idesc_s, L1);
+                        mma_commit_p(&sm.s_full[0], L1);
                     }
                 }
                 if (doB(j)) {
                     mbar_wait(&sm.p_full[1][0], j & 1);
                     tc_fence_after();
-                    issue_pv_half(tO[1], tS[1], v_base, idesc_o, j > 0, 0);
+                    issue_pv_half(tO[1], tS[1], v_base, idesc_o, j > 0, 0, L1);
                     mbar_wait(&sm.p_full[1][1], j & 1);
                     tc_fence_after();
-                    issue_pv_half(tO[1], tS[1], v_base, idesc_o, j > 0, 1);
-                    mma_commit(&sm.o_done[1]);
+                    issue_pv_half(tO[1], tS[1], v_base, idesc_o, j > 0, 1, L1);
+                    mma_commit_p(&sm.o_done[1], L1);
                     if (doB(j1)) {
                         mbar_wait(&sm.k_full[st1], (j1 / NS) & 1);
                         tc_fence_after();
-                        issue_s(tS[1], qb, smem_u32(sm.k[st1]), idesc_s);
-                        mma_commit(&sm.s_full[1]);
+                        issue_s(tS[1], qb, smem_u32(sm.k[st1]), idesc_s, L1);
+                        mma_commit_p(&sm.s_full[1], L1);
                     }
                 }
-                if (k1_needed) mma_commit(&sm.k_empty[st1]);
-                mma_commit(&sm.v_empty[st]);
+                if (k1_needed) mma_commit_p(&sm.k_empty[st1], L1);
+                mma_commit_p(&sm.v_empty[st], L1);
             }
         }
         // teardown: wait for the softmax warps' last TMEM reads, then free TMEM
