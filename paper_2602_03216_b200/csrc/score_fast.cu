@@ -95,26 +95,27 @@ __device__ __forceinline__ void producer_roles(ScoreSmem& sm, const CUtensorMap*
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t idesc = idesc_bf16_f32(SF_BM, SF_BN, 0, 0);
-            const uint32_t q_base = smem_u32(sm.q);
-            mbar_wait(&sm.q_full, 0);
-            for (int j = 0; j < g.nt; ++j) {
-                const int st = j % SF_NS, b = j & 1;
-                mbar_wait(&sm.k_full[st], (j / SF_NS) & 1);
-                if (j >= 2) mbar_wait(&sm.s_free[b], ((j - 2) >> 1) & 1);
-                tc_fence_after();
-                const uint32_t k_base = smem_u32(sm.k[st]);
+        // converged warp, elected issue: the MMAs go out back to back from
+        // uniform registers (see attend_sm100.cu)
+        const uint32_t L1 = elect_one() ? 1u : 0u;
+        const uint32_t idesc = idesc_bf16_f32(SF_BM, SF_BN, 0, 0);
+        const uint32_t q_base = smem_u32(sm.q);
+        mbar_wait(&sm.q_full, 0);
+        for (int j = 0; j < g.nt; ++j) {
+            const int st = j % SF_NS, b = j & 1;
+            mbar_wait(&sm.k_full[st], (j / SF_NS) & 1);
+            if (j >= 2) mbar_wait(&sm.s_free[b], ((j - 2) >> 1) & 1);
+            tc_fence_after();
+            const uint32_t k_base = smem_u32(sm.k[st]);
 #pragma unroll
-                for (int kk = 0; kk < SF_HD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * SF_HALF + (kk & 3) * 32;
-                    const uint64_t da = sdesc_kmajor_sw128((kTransposed ? k_base : q_base) + off);
-                    const uint64_t db = sdesc_kmajor_sw128((kTransposed ? q_base : k_base) + off);
-                    mma_bf16_ss(t_s[b], da, db, idesc, kk > 0 ? 1u : 0u);
-                }
-                mma_commit(&sm.s_full[b]);
-                mma_commit(&sm.k_empty[st]);
+            for (int kk = 0; kk < SF_HD / 16; ++kk) {
+                const uint32_t off = (kk >> 2) * SF_HALF + (kk & 3) * 32;
+                const uint64_t da = sdesc_kmajor_sw128((kTransposed ? k_base : q_base) + off);
+                const uint64_t db = sdesc_kmajor_sw128((kTransposed ? q_base : k_base) + off);
+                mma_bf16_ss_p(t_s[b], da, db, idesc, kk > 0 ? 1u : 0u, L1);
             }
+            mma_commit_p(&sm.s_full[b], L1);
+            mma_commit_p(&sm.k_empty[st], L1);
         }
     }
 }
