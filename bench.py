@@ -221,12 +221,12 @@ def run_ours(args):
         ms = max_over_ranks(total / steps, world, device)
         return ms, stages, launches
 
-    # per-stage split: eager launches with CUDA events between the stages
-    eager_ms, stages, _ = timed(layer, args.steps, args.warmup, stage_events=True)
     # the timed step: the whole chain replayed from a CUDA graph (world == 1;
     # sharded runs launch eagerly around the NCCL all-gathers)
     with ClockSampler(local) as clk:
         sparse_ms, _, launches = timed(layer, args.steps, args.warmup, graph=True)
+    # per-stage split: eager launches with CUDA events between the stages
+    eager_ms, stages, _ = timed(layer, args.steps, args.warmup, stage_events=True)
     k_keep = layer.k_keep
     clocks = clk.summary()
     hbm, pk_burst, pk_sust, pk_kind = measured_peaks()
