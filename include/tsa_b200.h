@@ -195,6 +195,32 @@ TSA_API int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const v
                                void* out, int32_t* idx_out, int32_t* k_keep_out,
                                int32_t* k_keep_host, void* ws, void* stream);
 
+/* ---- Attention-branch producer / consumer (layer_forward, model.cpp:169-201) ----
+ * The kernels cfg4's 32-layer prefill stack runs around the path; the
+ * projections themselves (x W_q|k|v, cat W_o) are plain GEMMs for the caller's
+ * BLAS (cuBLAS).  Row-major, dtype TSA_F32 or TSA_BF16 (compute in f32). */
+
+/* rms_norm (model.cpp:81-94): out[r] = (x[r] * inv_r) * gain, inv_r =
+ * 1 / sqrt(sum_j x[r, j]^2 / cols + eps), the sum taken sequentially in f32 as
+ * the reference does (f32 inputs match it bit for bit). */
+TSA_API int tsa_rms_norm(const void* x, const float* gain, int64_t rows, int32_t cols, float eps,
+                         int32_t dtype, void* out, void* stream);
+
+/* RoPE angles of apply_rope (model.cpp:107-116) at positions 0..seq_len-1:
+ * table[t][i] = {(float)cos(t w_i), (float)sin(t w_i)}, w_i = theta^(-2i/d)
+ * (double, host libm), f32 [seq_len][d_head/2][2]. */
+TSA_API int tsa_rope_table(int32_t seq_len, int32_t d_head, float theta, float* table,
+                           void* stream);
+
+/* split_heads + apply_rope of project_qkv (model.cpp:128-158): projection rows
+ * qkv [L][(H + 2 Hkv) d] (q heads, then k heads, then v heads) -> q [H][L][d],
+ * k / v [Hkv][L][d]; q and k rotated in f32 (x0 c - x1 s, x0 s + x1 c). */
+TSA_API int tsa_split_heads_rope(const tsa_desc* d, const void* qkv, const float* table, void* q,
+                                 void* k, void* v, void* stream);
+
+/* Head concat before W_o (model.cpp:196-200): heads [H][L][d] -> cat [L][H d]. */
+TSA_API int tsa_heads_concat(const tsa_desc* d, const void* heads, void* cat, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,10 @@ class Oracle:
             L.tsa_oracle_token_sparse_attention_sampled.argtypes = [
                 _f32p, _f32p, _f32p, _I, _I, _I, _I, _i32p, _I, _I, _I, _I, _f32p, _I]
             L.tsa_oracle_avg_pool_1d.argtypes = [_f32p, _I, _I, _f32p]
+            L.tsa_oracle_rms_norm.argtypes = [_f32p, _f32p, _I, _I, C.c_float, _f32p]
+            L.tsa_oracle_apply_rope.argtypes = [_f32p, _I, _I, C.c_float, _f32p]
+            L.tsa_oracle_project_qkv.argtypes = [_f32p, _f32p, _f32p, _f32p, _I, _I, _I, _I, _I,
+                                                 C.c_float, _f32p, _f32p, _f32p]
             L.tsa_oracle_rng_new.restype = C.c_void_p
             L.tsa_oracle_rng_new.argtypes = [C.c_uint64]
             L.tsa_oracle_rng_free.argtypes = [C.c_void_p]
@@ -101,6 +105,10 @@ class Oracle:
                                                          _i32p, _I, _i32p, _I, _f32p]
             L.tsa_ref_tsa_head_prefix.argtypes = [_f32p, _f32p, _f32p, _I, _I, _I, _I, _i32p, _I,
                                                   _I, _I, _f32p]
+            L.tsa_ref_rms_norm.argtypes = [_f32p, _f32p, _I, _I, C.c_float, _f32p]
+            L.tsa_ref_apply_rope.argtypes = [_f32p, _I, _I, C.c_float, _f32p]
+            L.tsa_ref_project_qkv.argtypes = [_f32p, _f32p, _f32p, _f32p, _I, _I, _I, _I, _I,
+                                              C.c_float, _f32p, _f32p, _f32p]
 
     def _check(self, rc: int):
         if rc != 0:
@@ -222,6 +230,34 @@ class Oracle:
         self._check(self.lib.tsa_ref_tsa_head_prefix(q, k, v, H, k.shape[0], L, d, idx,
                                                      idx.shape[1], h, m, out))
         return out
+
+    # ------------------------------------------- attention-branch producer
+    def _fn(self, name):
+        return getattr(self.lib, ("tsa_oracle_" if self.kind == "port" else "tsa_ref_") + name)
+
+    def rms_norm(self, x, gain, eps):
+        """model.cpp:81-94 -> [rows, cols] f32."""
+        x, gain = _f32(x), _f32(gain)
+        out = np.empty_like(x)
+        self._check(self._fn("rms_norm")(x, gain, x.shape[0], x.shape[1], eps, out))
+        return out
+
+    def apply_rope(self, x, theta):
+        """model.cpp:96-123 at positions 0..rows-1 -> [rows, cols] f32."""
+        x = _f32(x)
+        out = np.empty_like(x)
+        self._check(self._fn("apply_rope")(x, x.shape[0], x.shape[1], theta, out))
+        return out
+
+    def project_qkv(self, x_norm, wq, wk, wv, H, Hkv, d, theta):
+        """model.cpp:139-158 -> q [H, L, d], k [Hkv, L, d], v [Hkv, L, d] f32."""
+        x_norm, wq, wk, wv = _f32(x_norm), _f32(wq), _f32(wk), _f32(wv)
+        L, D = x_norm.shape
+        q = np.empty((H, L, d), np.float32)
+        k = np.empty((Hkv, L, d), np.float32)
+        v = np.empty((Hkv, L, d), np.float32)
+        self._check(self._fn("project_qkv")(x_norm, wq, wk, wv, L, D, H, Hkv, d, theta, q, k, v))
+        return q, k, v
 
     def avg_pool_1d(self, v, kernel):
         assert self.kind == "port"

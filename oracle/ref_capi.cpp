@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "tsa/attention.hpp"
+#include "tsa/model.hpp"
 #include "tsa/tensor_ops.hpp"
 #include "tsa/token_coverage.hpp"
 
@@ -195,6 +196,48 @@ int tsa_ref_tsa_head_prefix(const float* q, const float* k, const float* v, int 
         const Matrix kc = gather_rows(to_mat(k + size_t(kv) * L * d, L, d), s);
         const Matrix vc = gather_rows(to_mat(v + size_t(kv) * L * d, L, d), s);
         from_mat(dense_causal_attention(qc, kc, vc), out);
+    });
+}
+
+// ---- attention-branch producer (model.cpp:81-158): rms_norm, apply_rope,
+// project_qkv.  Row-major f32 arrays; positions are 0..rows-1 (project_qkv).
+int tsa_ref_rms_norm(const float* x, const float* gain, int rows, int cols, float eps, float* out) {
+    return guarded([&] {
+        Vector g(cols);
+        for (int j = 0; j < cols; ++j) g(j) = gain[j];
+        from_mat(rms_norm(to_mat(x, rows, cols), g, eps), out);
+    });
+}
+
+int tsa_ref_apply_rope(const float* x, int rows, int cols, float theta, float* out) {
+    return guarded([&] {
+        IndexList pos(static_cast<size_t>(rows));
+        for (int i = 0; i < rows; ++i) pos[size_t(i)] = i;
+        from_mat(apply_rope(to_mat(x, rows, cols), pos, theta), out);
+    });
+}
+
+// q_out [H x L x d], k_out / v_out [Hkv x L x d]; wq [D x H*d], wk / wv [D x Hkv*d].
+int tsa_ref_project_qkv(const float* x_norm, const float* wq, const float* wk, const float* wv,
+                        int L, int D, int H, int Hkv, int d, float theta, float* q_out,
+                        float* k_out, float* v_out) {
+    return guarded([&] {
+        ModelConfig cfg;
+        cfg.n_heads = H;
+        cfg.n_kv_heads = Hkv;
+        cfg.d_head = d;
+        cfg.d_model = D;
+        cfg.rope_theta = theta;
+        LayerWeights w;
+        w.wq = to_mat(wq, D, H * d);
+        w.wk = to_mat(wk, D, Hkv * d);
+        w.wv = to_mat(wv, D, Hkv * d);
+        const HeadTensors ht = project_qkv(to_mat(x_norm, L, D), w, cfg);
+        for (int h = 0; h < H; ++h) from_mat(ht.q[size_t(h)], q_out + size_t(h) * L * d);
+        for (int h = 0; h < Hkv; ++h) {
+            from_mat(ht.k[size_t(h)], k_out + size_t(h) * L * d);
+            from_mat(ht.v[size_t(h)], v_out + size_t(h) * L * d);
+        }
     });
 }
 

@@ -632,3 +632,85 @@ EXPORT int tsa_oracle_token_sparse_attention_sampled(const float* q, const float
     parallel_for((H + head_stride - 1) / head_stride, n_threads, tsa_one_head, &c);
     return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * Attention-branch producer (callers upstream of the path).
+ * rms_norm      model.cpp:81-94   ss = sum_j x^2 (f32, j ascending), inv = 1 / sqrt(ss / D + eps),
+ *                                 out = (x * inv) * gain
+ * apply_rope    model.cpp:96-123  pairs (2i, 2i+1) rotated by pos * theta^(-2i/d): angle in
+ *                                 double, (float)cos / (float)sin, x0 c - x1 s, x0 s + x1 c (f32)
+ * project_qkv   model.cpp:139-158 matmul (tensor_ops.cpp:12-25, p ascending, no FMA), split
+ *                                 into heads, RoPE on q and k at positions 0..L-1
+ */
+EXPORT int tsa_oracle_rms_norm(const float* x, const float* gain, int rows, int cols, float eps,
+                               float* out) {
+    if (rows < 0 || cols < 1) return fail("rms_norm: bad shape %ld x %ld", rows, cols, 0);
+    for (int i = 0; i < rows; ++i) {
+        const float* xr = x + (size_t)i * cols;
+        float ss = 0.0f;
+        for (int j = 0; j < cols; ++j) ss += xr[j] * xr[j];
+        const float inv = 1.0f / sqrtf(ss / (float)cols + eps);
+        for (int j = 0; j < cols; ++j) out[(size_t)i * cols + j] = xr[j] * inv * gain[j];
+    }
+    return 0;
+}
+
+EXPORT int tsa_oracle_apply_rope(const float* x, int rows, int cols, float theta, float* out) {
+    if (cols % 2 != 0) return fail("apply_rope: odd head dimension %ld", cols, 0, 0);
+    const int half = cols / 2;
+    for (int r = 0; r < rows; ++r) {
+        for (int i = 0; i < half; ++i) {
+            const double freq = pow((double)theta, -2.0 * (double)i / (double)cols);
+            const double angle = (double)r * freq;
+            const float c = (float)cos(angle), s = (float)sin(angle);
+            const float x0 = x[(size_t)r * cols + 2 * i], x1 = x[(size_t)r * cols + 2 * i + 1];
+            out[(size_t)r * cols + 2 * i] = x0 * c - x1 * s;
+            out[(size_t)r * cols + 2 * i + 1] = x0 * s + x1 * c;
+        }
+    }
+    return 0;
+}
+
+/* C[n x m] = A[n x k] B[k x m], reference order: C(i, :) += A(i, p) B(p, :), p ascending. */
+static void matmul_ref(const float* A, const float* B, int n, int k, int m, float* Cm) {
+    for (size_t i = 0; i < (size_t)n * m; ++i) Cm[i] = 0.0f;
+    for (int i = 0; i < n; ++i)
+        for (int p = 0; p < k; ++p) {
+            const float a = A[(size_t)i * k + p];
+            const float* b = B + (size_t)p * m;
+            float* c = Cm + (size_t)i * m;
+            for (int j = 0; j < m; ++j) c[j] += a * b[j];
+        }
+}
+
+/* q_out [H x L x d]; k_out / v_out [Hkv x L x d]; wq [D x H d], wk / wv [D x Hkv d]. */
+EXPORT int tsa_oracle_project_qkv(const float* x_norm, const float* wq, const float* wk,
+                                  const float* wv, int L, int D, int H, int Hkv, int d,
+                                  float theta, float* q_out, float* k_out, float* v_out) {
+    if (H < 1 || Hkv < 1 || d < 2 || d % 2) return fail("project_qkv: bad heads %ld/%ld d %ld", H, Hkv, d);
+    const int widths[3] = {H * d, Hkv * d, Hkv * d};
+    const float* ws[3] = {wq, wk, wv};
+    float* outs[3] = {q_out, k_out, v_out};
+    const int nh[3] = {H, Hkv, Hkv};
+    float* proj = (float*)malloc(sizeof(float) * (size_t)L * H * d);
+    float* head = (float*)malloc(sizeof(float) * (size_t)L * d);
+    if (!proj || !head) {
+        free(proj);
+        free(head);
+        return fail("project_qkv: out of memory", 0, 0, 0);
+    }
+    for (int t = 0; t < 3; ++t) {
+        matmul_ref(x_norm, ws[t], L, D, widths[t], proj);
+        for (int h = 0; h < nh[t]; ++h) {
+            for (int r = 0; r < L; ++r)
+                memcpy(head + (size_t)r * d, proj + (size_t)r * widths[t] + (size_t)h * d,
+                       sizeof(float) * d);
+            float* dst = outs[t] + (size_t)h * L * d;
+            if (t < 2) tsa_oracle_apply_rope(head, L, d, theta, dst);
+            else memcpy(dst, head, sizeof(float) * (size_t)L * d);
+        }
+    }
+    free(proj);
+    free(head);
+    return 0;
+}

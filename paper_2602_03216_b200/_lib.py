@@ -23,7 +23,8 @@ EXPORTS = (
     "tsa_budget", "tsa_aggregate_scores", "tsa_coverage_budget", "tsa_select", "tsa_gather",
     "tsa_attend", "tsa_attend_indexed", "tsa_zero_unselected", "tsa_gather_zero", "tsa_scatter",
     "tsa_scatter_rows", "tsa_check", "tsa_token_sparse_attention",
-    "tsa_dense_attention", "tsa_sparse_attention_layer",
+    "tsa_dense_attention", "tsa_sparse_attention_layer", "tsa_rms_norm", "tsa_rope_table",
+    "tsa_split_heads_rope", "tsa_heads_concat",
 )
 
 
@@ -74,6 +75,10 @@ def load() -> C.CDLL:
         "tsa_version": (C.c_char_p, []),
         "tsa_kernel_launches": (C.c_uint64, []),
         "tsa_release_graphs": (None, []),
+        "tsa_rms_norm": (C.c_int, [P, P, C.c_int64, I, C.c_float, I, P, P]),
+        "tsa_rope_table": (C.c_int, [I, I, C.c_float, P, P]),
+        "tsa_split_heads_rope": (C.c_int, [D, P, P, P, P, P, P]),
+        "tsa_heads_concat": (C.c_int, [D, P, P, P]),
         "tsa_workspace_size": (C.c_int, [D, C.POINTER(C.c_size_t)]),
         "tsa_score": (C.c_int, [D, P, P, P, P, P]),
         "tsa_budget": (C.c_int, [D, P, P, P, P]),

@@ -369,4 +369,36 @@ int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, 
                              });
 }
 
+// ---- attention-branch producer / consumer (cfg4 stack) ----
+int tsa_rms_norm(const void* x, const float* gain, int64_t rows, int32_t cols, float eps,
+                 int32_t dtype, void* out, void* stream) {
+    if (rows < 0 || cols < 1) return invalid("rms_norm: bad shape");
+    if (dtype != TSA_F32 && dtype != TSA_BF16) return invalid("rms_norm: unknown dtype");
+    if (!x || !gain || !out) return invalid("rms_norm: null pointer");
+    if (rows == 0) return 0;
+    return launch_rms_norm(x, gain, rows, cols, eps, dtype, out, S(stream));
+}
+
+int tsa_rope_table(int32_t seq_len, int32_t d_head, float theta, float* table, void* stream) {
+    if (d_head % 2 != 0)
+        return invalid("apply_rope: odd head dimension " + std::to_string(d_head));
+    if (seq_len < 1 || !table) return invalid("rope_table: bad arguments");
+    return launch_rope_table(seq_len, d_head, theta, table, S(stream));
+}
+
+int tsa_split_heads_rope(const tsa_desc* d, const void* qkv, const float* table, void* q, void* k,
+                         void* v, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (d->d_head % 2 != 0)
+        return invalid("apply_rope: odd head dimension " + std::to_string(d->d_head));
+    if (!qkv || !table || !q || !k || !v) return invalid("split_heads_rope: null pointer");
+    return launch_split_heads_rope(*d, qkv, table, q, k, v, S(stream));
+}
+
+int tsa_heads_concat(const tsa_desc* d, const void* heads, void* cat, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!heads || !cat) return invalid("heads_concat: null pointer");
+    return launch_heads_concat(*d, heads, cat, S(stream));
+}
+
 }  // extern "C"

@@ -118,6 +118,13 @@ int launch_zero_unselected(const tsa_desc& d, const int32_t* inv, void* out, cud
 int launch_attend_indexed(const tsa_desc& d, const void* q, const void* k, const void* v,
                           const int32_t* idx, const int32_t* k_keep, void* out, cudaStream_t st);
 int launch_colsum_pool(const tsa_desc& d, const float* probs, float* s, cudaStream_t st);
+// producer.cu (attention-branch producer / consumer, model.cpp:81-158, 196-200)
+int launch_rms_norm(const void* x, const float* gain, int64_t rows, int cols, float eps, int dtype,
+                    void* out, cudaStream_t st);
+int launch_rope_table(int seq_len, int d_head, float theta, float* table, cudaStream_t st);
+int launch_split_heads_rope(const tsa_desc& d, const void* qkv, const float* table, void* q,
+                            void* k, void* v, cudaStream_t st);
+int launch_heads_concat(const tsa_desc& d, const void* heads, void* cat, cudaStream_t st);
 // attend_simt.cu / attend_sm100.cu
 int launch_attend_simt(const tsa_desc& d, const void* q, const void* k, const void* v,
                        const int32_t* n_dev, int32_t n_const, int32_t kv_group, int32_t rows_per_head,

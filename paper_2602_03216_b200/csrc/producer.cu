@@ -1,0 +1,180 @@
+// Producer / consumer of the attention branch (layer_forward, model.cpp:169-201):
+// the kernels around the path that cfg4's 32-layer prefill stack needs.
+//
+//   rms_norm          model.cpp:81-94   one thread per row sums x^2 sequentially
+//                                       (f32, j ascending, FMUL then FADD -- the
+//                                       reference's order, so f32 inputs match it
+//                                       bit for bit); a warp per row scales
+//   rope table        model.cpp:107-116 angle = pos * theta^(-2i/d) in double (the
+//                                       frequencies come from the host's pow, as in
+//                                       the reference), cos/sin in double -> f32
+//   split_heads_rope  model.cpp:128-158 projection rows [L, (H + 2 Hkv) d] -> q
+//                                       [H, L, d], k / v [Hkv, L, d], RoPE on q and
+//                                       k in f32 (x0 c - x1 s, x0 s + x1 c, no FMA)
+//   heads_concat      model.cpp:196-200 [H, L, d] -> [L, H d] for the W_O GEMM
+//
+// The projections themselves (x W_q, x W_k, x W_v, cat W_o) are plain GEMMs and
+// go to cuBLAS through the host; everything here is HBM-bound byte movement.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace tsa {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float ld_f32(const T* p) {
+    return Elem<T>::to_f32(*p);
+}
+
+// A CTA owns 128 rows: each thread first sums x^2 of its own row
+// sequentially (the reference's order), then each warp scales 32 of the rows
+// with coalesced accesses: out = (x * inv) * gain.
+constexpr int RMS_ROWS = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(RMS_ROWS) rms_norm_kernel(const T* __restrict__ x,
+                                                           const float* __restrict__ gain,
+                                                           int64_t rows, int cols, float eps,
+                                                           T* __restrict__ out) {
+    __shared__ float inv_s[RMS_ROWS];
+    const int64_t r0 = (int64_t)blockIdx.x * RMS_ROWS;
+    const int64_t r = r0 + threadIdx.x;
+    if (r < rows) {
+        const T* xr = x + r * cols;
+        float ss = 0.0f;
+        for (int j = 0; j < cols; ++j) {
+            const float v = ld_f32(xr + j);
+            ss = __fadd_rn(ss, __fmul_rn(v, v));
+        }
+        // inv = 1 / sqrt(ss / cols + eps) (model.cpp:89), each step correctly rounded
+        inv_s[threadIdx.x] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)cols), eps)));
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int rr = warp; rr < RMS_ROWS; rr += RMS_ROWS / 32) {
+        const int64_t row = r0 + rr;
+        if (row >= rows) break;
+        const float iv = inv_s[rr];
+        const T* xr = x + row * cols;
+        T* o = out + row * cols;
+        for (int j = lane; j < cols; j += 32)
+            o[j] = Elem<T>::from_f32(__fmul_rn(__fmul_rn(ld_f32(xr + j), iv), gain[j]));
+    }
+}
+
+struct RopeFreqs {
+    double f[128];  // theta^(-2i/d), i < d/2 <= 128
+};
+
+__global__ void rope_table_kernel(const __grid_constant__ RopeFreqs freq, int seq_len, int half,
+                                  float2* __restrict__ table) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)seq_len * half) return;
+    const int t = (int)(e / half), i = (int)(e % half);
+    const double angle = (double)t * freq.f[i];
+    double s, c;
+    sincos(angle, &s, &c);
+    table[e] = make_float2((float)c, (float)s);
+}
+
+// One thread per (row, head-slot, pair).  Slots [0, H) are q heads, [H, H+Hkv)
+// k heads, [H+Hkv, H+2Hkv) v heads of the projection row.
+template <typename T>
+__global__ void __launch_bounds__(256) split_heads_rope_kernel(
+    const T* __restrict__ qkv, const float2* __restrict__ table, int L, int H, int Hkv, int d,
+    T* __restrict__ q, T* __restrict__ k, T* __restrict__ v) {
+    const int half = d / 2, slots = H + 2 * Hkv;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)L * slots * half) return;
+    const int i = (int)(e % half);
+    const int slot = (int)((e / half) % slots);
+    const int t = (int)(e / ((int64_t)half * slots));
+    const T* src = qkv + ((int64_t)t * slots + slot) * d + 2 * i;
+    const float x0 = ld_f32(src), x1 = ld_f32(src + 1);
+    T* dst;
+    float y0 = x0, y1 = x1;
+    if (slot < H + Hkv) {
+        const float2 cs = table[(int64_t)t * half + i];
+        y0 = __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
+        y1 = __fadd_rn(__fmul_rn(x0, cs.y), __fmul_rn(x1, cs.x));
+        dst = slot < H ? q + ((int64_t)slot * L + t) * d : k + ((int64_t)(slot - H) * L + t) * d;
+    } else {
+        dst = v + ((int64_t)(slot - H - Hkv) * L + t) * d;
+    }
+    dst[2 * i] = Elem<T>::from_f32(y0);
+    dst[2 * i + 1] = Elem<T>::from_f32(y1);
+}
+
+// cat[t, h d + c] = heads[h, t, c]; 16-byte units.
+__global__ void __launch_bounds__(256) heads_concat_kernel(const uint4* __restrict__ heads, int L,
+                                                          int H, int units_per_row,
+                                                          uint4* __restrict__ cat) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)L * H * units_per_row;
+    if (e >= total) return;
+    const int c = (int)(e % units_per_row);
+    const int h = (int)((e / units_per_row) % H);
+    const int64_t t = e / ((int64_t)units_per_row * H);
+    cat[e] = heads[((int64_t)h * L + t) * units_per_row + c];
+}
+
+}  // namespace
+
+int launch_rms_norm(const void* x, const float* gain, int64_t rows, int cols, float eps, int dtype,
+                    void* out, cudaStream_t st) {
+    const unsigned grid = (unsigned)((rows + RMS_ROWS - 1) / RMS_ROWS);
+    if (dtype == TSA_BF16)
+        rms_norm_kernel<__nv_bfloat16><<<grid, RMS_ROWS, 0, st>>>(
+            (const __nv_bfloat16*)x, gain, rows, cols, eps, (__nv_bfloat16*)out);
+    else
+        rms_norm_kernel<float><<<grid, RMS_ROWS, 0, st>>>((const float*)x, gain, rows, cols, eps,
+                                                          (float*)out);
+    TSA_LAUNCH_CHECK("rms_norm");
+    return 0;
+}
+
+int launch_rope_table(int seq_len, int d_head, float theta, float* table, cudaStream_t st) {
+    const int half = d_head / 2;
+    if (half < 1 || half > 128) return invalid("rope_table: d_head must be in [2, 256]");
+    // theta^(-2i/d) in double on the host: the reference's own expression and libm
+    RopeFreqs f{};
+    for (int i = 0; i < half; ++i)
+        f.f[i] = std::pow(static_cast<double>(theta), -2.0 * static_cast<double>(i) /
+                                                          static_cast<double>(d_head));
+    const int64_t n = (int64_t)seq_len * half;
+    rope_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(f, seq_len, half,
+                                                                  reinterpret_cast<float2*>(table));
+    TSA_LAUNCH_CHECK("rope_table");
+    return 0;
+}
+
+int launch_split_heads_rope(const tsa_desc& d, const void* qkv, const float* table, void* q,
+                            void* k, void* v, cudaStream_t st) {
+    const int L = d.seq_len, H = d.n_heads, Hkv = d.n_kv_heads, D = d.d_head;
+    const int64_t n = (int64_t)L * (H + 2 * Hkv) * (D / 2);
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    const float2* tb = reinterpret_cast<const float2*>(table);
+    if (d.dtype == TSA_BF16)
+        split_heads_rope_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+            (const __nv_bfloat16*)qkv, tb, L, H, Hkv, D, (__nv_bfloat16*)q, (__nv_bfloat16*)k,
+            (__nv_bfloat16*)v);
+    else
+        split_heads_rope_kernel<float><<<grid, 256, 0, st>>>((const float*)qkv, tb, L, H, Hkv, D,
+                                                             (float*)q, (float*)k, (float*)v);
+    TSA_LAUNCH_CHECK("split_heads_rope");
+    return 0;
+}
+
+int launch_heads_concat(const tsa_desc& d, const void* heads, void* cat, cudaStream_t st) {
+    const size_t row_bytes = (size_t)d.d_head * elem_bytes(d.dtype);
+    if (row_bytes % 16) return invalid("heads_concat: head rows must be a multiple of 16 bytes");
+    const int upr = (int)(row_bytes / 16);
+    const int64_t n = (int64_t)d.seq_len * d.n_heads * upr;
+    heads_concat_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        (const uint4*)heads, d.seq_len, d.n_heads, upr, (uint4*)cat);
+    TSA_LAUNCH_CHECK("heads_concat");
+    return 0;
+}
+
+}  // namespace tsa

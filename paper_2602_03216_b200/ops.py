@@ -44,6 +44,7 @@ __all__ = [
     "SparsePlan", "LayerStat", "score_tokens", "aggregate_scores", "coverage_budget",
     "fixed_budget", "select_tokens", "validate", "dense_causal_attention",
     "token_sparse_attention", "sparse_attention_layer", "InvalidArgument", "NativeLibraryError",
+    "rms_norm", "rope_table", "split_heads_rope", "heads_concat",
 ]
 
 
@@ -481,3 +482,63 @@ def sparse_attention_layer(heads: HeadTensors, plan: SparsePlan, layer: int = 0,
                                       tau=plan.tau if plan.mode == SparseMode.kDynamic else 0.0,
                                       forced=plan.forced_set(L), _full=idx, _k_dev=kd)
     return out, st
+
+
+# ------------------------------------------- attention-branch producer / consumer
+def rms_norm(x: torch.Tensor, gain: torch.Tensor, eps: float,
+             out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """model.cpp:81-94 over the rows of x [rows, cols] (f32 or bf16, CUDA)."""
+    _require_cuda(x, gain)
+    if x.dim() != 2:
+        raise InvalidArgument("rms_norm: x must be [rows, cols]")
+    if gain.numel() != x.shape[1]:
+        raise InvalidArgument(f"rms_norm: gain size {gain.numel()} != width of "
+                              f"[{x.shape[0]} x {x.shape[1]}]")
+    x = x.contiguous()
+    g = gain.to(torch.float32).contiguous()
+    if out is None:
+        out = torch.empty_like(x)
+    _lib.check(_lib.load().tsa_rms_norm(_ptr(x), _ptr(g), x.shape[0], x.shape[1], eps,
+                                        _dtype_code(x), _ptr(out), _stream(x.device)))
+    return out
+
+
+def rope_table(seq_len: int, d_head: int, theta: float, device) -> torch.Tensor:
+    """apply_rope's (cos, sin) at positions 0..L-1 (model.cpp:107-116): f32 [L, d/2, 2]."""
+    t = torch.empty((seq_len, d_head // 2, 2), dtype=torch.float32, device=device)
+    _lib.check(_lib.load().tsa_rope_table(seq_len, d_head, theta, _ptr(t),
+                                          _stream(torch.device(device))))
+    return t
+
+
+def split_heads_rope(qkv: torch.Tensor, table: torch.Tensor, n_heads: int, n_kv_heads: int,
+                     d_head: int, out: Optional[HeadTensors] = None) -> HeadTensors:
+    """split_heads + apply_rope of project_qkv (model.cpp:128-158): projection rows
+    [L, (H + 2 Hkv) d] -> HeadTensors with RoPE on q and k."""
+    _require_cuda(qkv, table)
+    L = qkv.shape[0]
+    if qkv.shape[1] != (n_heads + 2 * n_kv_heads) * d_head:
+        raise InvalidArgument("split_heads_rope: projection width != (H + 2 Hkv) d")
+    if out is None:
+        out = HeadTensors(torch.empty((n_heads, L, d_head), dtype=qkv.dtype, device=qkv.device),
+                          torch.empty((n_kv_heads, L, d_head), dtype=qkv.dtype, device=qkv.device),
+                          torch.empty((n_kv_heads, L, d_head), dtype=qkv.dtype, device=qkv.device))
+    desc = _desc_for(n_heads, n_kv_heads, L, d_head, _dtype_code(qkv))
+    qkv = qkv.contiguous()
+    _lib.check(_lib.load().tsa_split_heads_rope(C.byref(desc), _ptr(qkv), _ptr(table),
+                                                _ptr(out.q), _ptr(out.k), _ptr(out.v),
+                                                _stream(qkv.device)))
+    return out
+
+
+def heads_concat(heads: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """model.cpp:196-200: [H, L, d] -> [L, H d]."""
+    _require_cuda(heads)
+    H, L, d = heads.shape
+    heads = heads.contiguous()
+    if out is None:
+        out = torch.empty((L, H * d), dtype=heads.dtype, device=heads.device)
+    desc = _desc_for(H, H, L, d, _dtype_code(heads))
+    _lib.check(_lib.load().tsa_heads_concat(C.byref(desc), _ptr(heads), _ptr(out),
+                                            _stream(heads.device)))
+    return out

@@ -1,0 +1,136 @@
+"""cfg4: a multi-layer prefill attention stack around the sparse path.
+
+Each layer is the attention branch of the reference's ``layer_forward``
+(model.cpp:169-201) on the residual stream x [L, d_model]:
+
+    xn  = rms_norm(x, attn_norm, eps)                 tsa_rms_norm       (model.cpp:81-94)
+    qkv = xn [W_q | W_k | W_v]                        cuBLAS GEMM        (model.cpp:139-158)
+    q, k, v = split_heads + RoPE at 0..L-1            tsa_split_heads_rope
+    o   = sparse attention layer (score -> budget -> select -> gather -> attend)
+                                                      the path (this package)
+    x  += concat_h(o_h) W_o                           tsa_heads_concat + cuBLAS GEMM
+
+The FFN half of layer_forward (SwiGLU) is outside the attention stack.  Only
+one B200 is in this build, so the stack runs single-process (``world`` = 1);
+each layer's attention is a ``ShardedSparseAttention`` and shards by heads
+like the single-layer path.
+
+Weights are random-init like ``init_random`` (model.cpp:243-268): xavier
+uniform, gain vectors of ones.  With xavier W_q/W_k the logits q.k/sqrt(d) are
+O(1) and every attention map is near-uniform (k/L ~ 0.98 at tau = 0.01, so no
+layer would be sparse); trained models have sharper logits.  The stack
+therefore scales W_q and W_k by a per-layer gain (``qk_gain``, default spread
+over [2.5, 4.0]) and the synthetic hidden state mixes a shared direction into
+each row with block-constant weights (``structured_hidden``) -- structure that
+survives RMSNorm -- so the selection varies per layer and per head the way the
+paper's does.  Both are stated in the bench line's config.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import List, Optional
+
+import torch
+
+from . import ops
+from .dist import ShardedSparseAttention
+from .ops import SparsePlan
+
+
+@dataclass
+class StackLayer:
+    attn_norm: torch.Tensor   # [D] f32 (ones)
+    wqkv: torch.Tensor        # [D, (H + 2 Hkv) d]: W_q | W_k | W_v
+    wo: torch.Tensor          # [H d, D]
+    qk_gain: float
+
+
+def _xavier(rows: int, cols: int, gen: torch.Generator, device, gain: float = 1.0) -> torch.Tensor:
+    a = gain * math.sqrt(6.0 / (rows + cols))  # model.cpp:246-249
+    return (torch.rand((rows, cols), generator=gen, device=device) * 2 - 1) * a
+
+
+def structured_hidden(L: int, D: int, seed: int = 0, block: int = 32, spread: float = 1.5,
+                      dtype=torch.bfloat16, device="cuda") -> torch.Tensor:
+    """Rows x_t = sqrt(D) (c_t e + sqrt(1 - c_t^2) n_t): a shared unit direction e
+    with block-constant weights c_t = tanh(spread z) and unit noise n_t."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    e = torch.randn(D, generator=g, device=device)
+    e = e / e.norm()
+    nb = (L + block - 1) // block
+    c = torch.tanh(spread * torch.randn(nb, generator=g, device=device)).repeat_interleave(block)[:L]
+    x = torch.empty((L, D), dtype=dtype, device=device)
+    step = 8192
+    for r0 in range(0, L, step):  # bounded f32 temporaries
+        r1 = min(L, r0 + step)
+        n = torch.randn((r1 - r0, D), generator=g, device=device)
+        n = n / n.norm(dim=1, keepdim=True)
+        cc = c[r0:r1, None]
+        x[r0:r1] = (math.sqrt(D) * (cc * e[None] + torch.sqrt(1 - cc * cc) * n)).to(dtype)
+    return x
+
+
+class PrefillAttentionStack:
+    """n_layers attention branches over one residual stream (see module doc)."""
+
+    def __init__(self, n_layers: int, n_heads: int, n_kv_heads: int, d_head: int, d_model: int,
+                 seq_len: int, plan: SparsePlan, seed: int = 0, device=None,
+                 dtype=torch.bfloat16, rope_theta: float = 500000.0, norm_eps: float = 1e-5,
+                 qk_gain: Optional[List[float]] = None, scoring: int = 0):
+        device = torch.device(device or "cuda")
+        self.n_layers, self.H, self.Hkv, self.d, self.D, self.L = (
+            n_layers, n_heads, n_kv_heads, d_head, d_model, seq_len)
+        self.plan, self.eps, self.device, self.dtype = plan, norm_eps, device, dtype
+        if qk_gain is None:
+            qk_gain = [2.5 + 1.5 * (i % 7) / 6 for i in range(n_layers)]
+        g = torch.Generator(device=device).manual_seed(seed)
+        Wq, Wkv = n_heads * d_head, n_kv_heads * d_head
+        self.layers: List[StackLayer] = []
+        for i in range(n_layers):
+            wq = _xavier(d_model, Wq, g, device, qk_gain[i])
+            wk = _xavier(d_model, Wkv, g, device, qk_gain[i])
+            wv = _xavier(d_model, Wkv, g, device)
+            wo = _xavier(Wq, d_model, g, device)
+            self.layers.append(StackLayer(
+                attn_norm=torch.ones(d_model, dtype=torch.float32, device=device),
+                wqkv=torch.cat([wq, wk, wv], dim=1).to(dtype).contiguous(),
+                wo=wo.to(dtype).contiguous(), qk_gain=qk_gain[i]))
+            del wq, wk, wv, wo
+        self.attn = ShardedSparseAttention(n_heads, n_kv_heads, seq_len, d_head, dtype, plan,
+                                           device=device, scoring=scoring)
+        # persistent buffers: the whole forward is a fixed launch sequence
+        self.table = ops.rope_table(seq_len, d_head, rope_theta, device)
+        self.xn = torch.empty((seq_len, d_model), dtype=dtype, device=device)
+        self.qkv = torch.empty((seq_len, Wq + 2 * Wkv), dtype=dtype, device=device)
+        self.heads = ops.HeadTensors(
+            torch.empty((n_heads, seq_len, d_head), dtype=dtype, device=device),
+            torch.empty((n_kv_heads, seq_len, d_head), dtype=dtype, device=device),
+            torch.empty((n_kv_heads, seq_len, d_head), dtype=dtype, device=device))
+        self.cat = torch.empty((seq_len, Wq), dtype=dtype, device=device)
+        self.k_keep = torch.zeros(n_layers, dtype=torch.int32, device=device)
+
+    def layer(self, i: int, x: torch.Tensor, dense: bool = False, marks=None) -> torch.Tensor:
+        """One attention branch in place on the residual stream x [L, D]."""
+        mark = marks or (lambda name: None)
+        w = self.layers[i]
+        ops.rms_norm(x, w.attn_norm, self.eps, out=self.xn)
+        torch.matmul(self.xn, w.wqkv, out=self.qkv)
+        ops.split_heads_rope(self.qkv, self.table, self.H, self.Hkv, self.d, out=self.heads)
+        mark("producer")
+        o = self.attn.step(self.heads.q, self.heads.k, self.heads.v, dense=dense)
+        if dense:
+            self.k_keep[i].fill_(self.L)
+        else:
+            self.k_keep[i].copy_(self.attn.backend.k_keep[0])
+        mark("attention")
+        ops.heads_concat(o, out=self.cat)
+        x.addmm_(self.cat, w.wo)
+        mark("consumer")
+        return x
+
+    def forward(self, x: torch.Tensor, dense: bool = False, marks=None) -> torch.Tensor:
+        """All layers in place on x [L, D] (the residual stream)."""
+        for i in range(self.n_layers):
+            self.layer(i, x, dense=dense, marks=marks)
+        return x

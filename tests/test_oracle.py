@@ -195,3 +195,50 @@ def test_rel_l2_metric():
     a = np.array([[1.0, 2.0]], np.float32)
     assert rel_l2(a, a) == 0.0
     assert abs(rel_l2(np.array([[1.0, 0.0]]), np.array([[0.0, 0.0]])) - 1.0) < 1e-12
+
+
+# ------------------------------------- attention-branch producer (model.cpp)
+def test_producer_port_bit_exact_vs_reference(port, ref):
+    """rms_norm / apply_rope / project_qkv: the C restatement against the
+    reference's model.cpp compiled from /root/reference."""
+    rng = RefRng(31)
+    x = rng.random_matrix(37, 96, 2.0)
+    g = rng.random_matrix(1, 96, 1.0).reshape(-1)
+    for eps in (0.0, 1e-5):
+        assert np.array_equal(bits(port.rms_norm(x, g, eps)), bits(ref.rms_norm(x, g, eps)))
+    y = rng.random_matrix(300, 64, 1.0)
+    for theta in (10000.0, 500000.0):
+        assert np.array_equal(bits(port.apply_rope(y, theta)), bits(ref.apply_rope(y, theta)))
+    xn = rng.random_matrix(50, 64, 1.0)
+    wq, wk, wv = (rng.random_matrix(64, w, 0.2) for w in (4 * 16, 2 * 16, 2 * 16))
+    a = port.project_qkv(xn, wq, wk, wv, 4, 2, 16, 10000.0)
+    b = ref.project_qkv(xn, wq, wk, wv, 4, 2, 16, 10000.0)
+    for p, r in zip(a, b):
+        assert np.array_equal(bits(p), bits(r))
+
+
+def test_producer_kats(port):
+    """test_model.cpp:75-155: unit-gain rows have unit RMS; gain scales columns;
+    eps keeps zero rows finite; position 0 is the identity; rotation preserves
+    pair norms; q.k depends only on the relative position; odd widths throw."""
+    rng = RefRng(32)
+    x = rng.random_matrix(3, 16, 3.0)
+    y = port.rms_norm(x, np.ones(16, np.float32), 0.0)
+    assert np.allclose(np.sqrt((y.astype(np.float64) ** 2).mean(axis=1)), 1.0, atol=1e-6)
+    g = np.arange(1, 17, dtype=np.float32)
+    assert np.allclose(port.rms_norm(x, g, 0.0), y * g, rtol=1e-6)
+    assert np.all(np.isfinite(port.rms_norm(np.zeros((2, 4), np.float32), np.ones(4, np.float32),
+                                            1e-5)))
+    r = rng.random_matrix(64, 8, 1.0)
+    ro = port.apply_rope(r, 10000.0)
+    assert np.array_equal(bits(ro[0]), bits(r[0]))
+    n0 = np.hypot(r[:, 0::2], r[:, 1::2])
+    assert np.allclose(np.hypot(ro[:, 0::2], ro[:, 1::2]), n0, rtol=1e-5)
+    q = np.tile(rng.random_matrix(1, 8, 1.0), (64, 1))
+    k = np.tile(rng.random_matrix(1, 8, 1.0), (64, 1))
+    rq, rk = port.apply_rope(q, 10000.0), port.apply_rope(k, 10000.0)
+    d1 = float(rq[20] @ rk[15])   # relative offset 5
+    d2 = float(rq[40] @ rk[35])
+    assert abs(d1 - d2) < 1e-4 * max(1.0, abs(d1))
+    with pytest.raises(OracleError):
+        port.apply_rope(np.zeros((1, 3), np.float32), 1e4)

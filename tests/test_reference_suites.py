@@ -34,3 +34,15 @@ def test_reference_suites_link_the_b200_library():
         syms = subprocess.run(["nm", "-C", str(exe)], capture_output=True, text=True).stdout
         # the operator definitions come from the adapter, not the reference's sources
         assert "tsa::score_tokens" in syms and "ref_cpu_token_sparse_attention" in syms
+
+
+def test_reference_model_suite_pins_the_shim():
+    """proj/tests/test_model.cpp (rms_norm, apply_rope, project_qkv, layer_forward,
+    init_random, checkpoints) compiled unmodified against the Eigen/doctest shim:
+    pins model.cpp's arithmetic that the producer oracle restates (CPU)."""
+    exe = ROOT / "oracle" / "_ref" / "test_model"
+    if not exe.exists():
+        pytest.skip("reference suites not built")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "failed: 0" in r.stdout
