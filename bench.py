@@ -39,6 +39,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "attention prefill latency (ms) & speedup vs dense at 128K over tau sweep, 1/2/4/8 B200"
 H, HKV, D = 32, 8, 128
+D_HEAD = D
 
 
 def parse():
@@ -58,9 +59,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-dense", action="store_true")
-    p.add_argument("--extra", type=str, default="cfg2,cfg5",
+    p.add_argument("--extra", type=str, default="cfg2,cfg5,cfg4",
                    help="other BASELINE configs measured after the headline (comma list: cfg2 = "
-                        "32K uniform tau sweep, cfg5 = Llama-3-70B heads at 128K; '' = none)")
+                        "32K uniform tau sweep, cfg5 = Llama-3-70B heads at 128K, cfg4 = 32-layer "
+                        "prefill attention stack at 64K; '' = none)")
     p.add_argument("--calibrate", action="store_true",
                    help="print k/L at the paper's tau levels for a sigma grid and exit")
     return p.parse_args()
@@ -348,9 +350,77 @@ EXTRA = {
 }
 
 
+def run_cfg4(args, tsa, rank, world, device):
+    """BASELINE configs[3]: the full 32-layer prefill attention stack at L = 64K
+    (Llama-3-8B heads, d_model 4096, random-init layers, paper_2602_03216_b200/
+    stack.py): latency of the whole stack sparse (tau = 0.01) and dense, the
+    producer / attention / consumer split, and the per-layer budgets."""
+    from paper_2602_03216_b200.stack import PrefillAttentionStack, structured_hidden
+    if world > 1:
+        return {"skipped": "the stack runs single-process in this build"}
+    L, D, n_layers = 65536, 4096, 32
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=args.tau)
+    st = PrefillAttentionStack(n_layers, H, HKV, D_HEAD, D, L, plan, seed=4, device=device)
+    x0 = structured_hidden(L, D, seed=5, device=device)
+    x = torch.empty_like(x0)
+    stream = torch.cuda.current_stream(device)
+
+    def run(dense, marks=None):
+        x.copy_(x0)
+        st.forward(x, dense=dense, marks=marks)
+
+    out = {}
+    for dense in (False, True):
+        run(dense)  # warm-up
+        torch.cuda.synchronize()
+        steps = 1 if dense else 2
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(steps):
+            run(dense)
+        e.record(stream)
+        torch.cuda.synchronize()
+        out["dense_ms" if dense else "ms"] = round(s.elapsed_time(e) / steps, 1)
+    # producer / attention / consumer split of one sparse forward
+    names, evs = [], []
+
+    def mark(name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        names.append(name)
+        evs.append(ev)
+    mark("start")
+    run(False, marks=mark)
+    torch.cuda.synchronize()
+    split = {}
+    for i in range(1, len(evs)):
+        split[names[i]] = split.get(names[i], 0.0) + evs[i - 1].elapsed_time(evs[i])
+    split.pop("start", None)
+    kk = st.k_keep.cpu().tolist()
+    F = sum(f_attn(k, D_HEAD, H) for k in kk)
+    out.update({
+        "workload": "cfg4: 32-layer prefill attention stack (rms_norm -> QKV GEMM -> RoPE -> "
+                    "sparse attention -> W_o GEMM + residual), Llama-3-8B heads (32 Q / 8 KV, "
+                    "d=128, d_model 4096), L=65536, bf16, random-init layers (xavier; W_q, W_k "
+                    "x per-layer gain 2.5-4.0) on a structured synthetic hidden state",
+        "seq_len": L, "n_layers": n_layers, "tau": args.tau,
+        "speedup_vs_dense": round(out["dense_ms"] / out["ms"], 3),
+        "split_ms": {k2: round(v2, 1) for k2, v2 in split.items()},
+        "attention_TFLOP_per_s": round(F / (split.get("attention", 1.0) * 1e-3) / 1e12, 1),
+        "k_keep_per_layer": kk,
+        "k_over_L_mean": round(sum(kk) / (len(kk) * L), 4),
+        "tokens_per_s": round(L / (out["ms"] * 1e-3), 1),
+        "gemm": "cuBLAS (torch.matmul / addmm): x W_qkv and cat W_o",
+    })
+    del st, x, x0
+    return out
+
+
 def run_extra(name, args, tsa, workloads, Sharded, rank, world, device):
     """Latency of another BASELINE config: dense and every tau of its sweep,
     with the per-stage split of the sparse step at the last tau."""
+    if name == "cfg4":
+        return run_cfg4(args, tsa, rank, world, device)
     c = EXTRA[name]
     H_, Hkv_, L = c["H"], c["Hkv"], c["L"]
     if c["gen"] == "uniform":

@@ -27,38 +27,56 @@ __device__ __forceinline__ float ld_f32(const T* p) {
     return Elem<T>::to_f32(*p);
 }
 
-// A CTA owns 128 rows: each thread first sums x^2 of its own row
-// sequentially (the reference's order), then each warp scales 32 of the rows
-// with coalesced accesses: out = (x * inv) * gain.
-constexpr int RMS_ROWS = 128;
+// A CTA owns 32 rows.  Pass 1 streams the rows through shared memory in
+// 128-column chunks (all 256 threads load, coalesced, double-buffered) while
+// warp 0 -- one lane per row -- accumulates x^2 sequentially in the
+// reference's order; pass 2 scales the rows with coalesced 16-byte accesses:
+// out = (x * inv) * gain.
+constexpr int RMS_ROWS = 32;
+constexpr int RMS_CHUNK = 128;
+constexpr int RMS_THREADS = 256;
 
 template <typename T>
-__global__ void __launch_bounds__(RMS_ROWS) rms_norm_kernel(const T* __restrict__ x,
-                                                           const float* __restrict__ gain,
-                                                           int64_t rows, int cols, float eps,
-                                                           T* __restrict__ out) {
+__global__ void __launch_bounds__(RMS_THREADS) rms_norm_kernel(const T* __restrict__ x,
+                                                              const float* __restrict__ gain,
+                                                              int64_t rows, int cols, float eps,
+                                                              T* __restrict__ out) {
+    __shared__ float chunk[2][RMS_ROWS][RMS_CHUNK + 1];  // +1: conflict-free row walks
     __shared__ float inv_s[RMS_ROWS];
     const int64_t r0 = (int64_t)blockIdx.x * RMS_ROWS;
-    const int64_t r = r0 + threadIdx.x;
-    if (r < rows) {
-        const T* xr = x + r * cols;
-        float ss = 0.0f;
-        for (int j = 0; j < cols; ++j) {
-            const float v = ld_f32(xr + j);
-            ss = __fadd_rn(ss, __fmul_rn(v, v));
+    const int nrows = rows - r0 < RMS_ROWS ? (int)(rows - r0) : RMS_ROWS;
+    const int tid = threadIdx.x;
+    const int n_chunks = (cols + RMS_CHUNK - 1) / RMS_CHUNK;
+    auto load = [&](int c, int buf) {
+        const int c0 = c * RMS_CHUNK;
+        for (int e = tid; e < RMS_ROWS * RMS_CHUNK; e += RMS_THREADS) {
+            const int rr = e / RMS_CHUNK, j = e % RMS_CHUNK;
+            float v = 0.0f;
+            if (rr < nrows && c0 + j < cols) v = ld_f32(x + (r0 + rr) * cols + c0 + j);
+            chunk[buf][rr][j] = v;
         }
-        // inv = 1 / sqrt(ss / cols + eps) (model.cpp:89), each step correctly rounded
-        inv_s[threadIdx.x] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)cols), eps)));
-    }
+    };
+    float ss = 0.0f;
+    load(0, 0);
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int rr = warp; rr < RMS_ROWS; rr += RMS_ROWS / 32) {
-        const int64_t row = r0 + rr;
-        if (row >= rows) break;
+    for (int c = 0; c < n_chunks; ++c) {
+        if (c + 1 < n_chunks) load(c + 1, (c + 1) & 1);  // overlaps warp 0's sums
+        if (tid < RMS_ROWS) {
+            const float* row = chunk[c & 1][tid];
+            const int n = min(RMS_CHUNK, cols - c * RMS_CHUNK);
+            for (int j = 0; j < n; ++j) ss = __fadd_rn(ss, __fmul_rn(row[j], row[j]));
+        }
+        __syncthreads();
+    }
+    // inv = 1 / sqrt(ss / cols + eps) (model.cpp:89), each step correctly rounded
+    if (tid < RMS_ROWS)
+        inv_s[tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)cols), eps)));
+    __syncthreads();
+    for (int rr = tid >> 5; rr < nrows; rr += RMS_THREADS / 32) {
         const float iv = inv_s[rr];
-        const T* xr = x + row * cols;
-        T* o = out + row * cols;
-        for (int j = lane; j < cols; j += 32)
+        const T* xr = x + (r0 + rr) * cols;
+        T* o = out + (r0 + rr) * cols;
+        for (int j = tid & 31; j < cols; j += 32)
             o[j] = Elem<T>::from_f32(__fmul_rn(__fmul_rn(ld_f32(xr + j), iv), gain[j]));
     }
 }
@@ -78,32 +96,72 @@ __global__ void rope_table_kernel(const __grid_constant__ RopeFreqs freq, int se
     table[e] = make_float2((float)c, (float)s);
 }
 
-// One thread per (row, head-slot, pair).  Slots [0, H) are q heads, [H, H+Hkv)
-// k heads, [H+Hkv, H+2Hkv) v heads of the projection row.
+// One thread per (row, head slot, group of 4 pairs).  Slots [0, H) are q
+// heads, [H, H+Hkv) k heads, [H+Hkv, H+2Hkv) v heads of the projection row.
+constexpr int ROPE_PAIRS = 4;
+
 template <typename T>
 __global__ void __launch_bounds__(256) split_heads_rope_kernel(
     const T* __restrict__ qkv, const float2* __restrict__ table, int L, int H, int Hkv, int d,
     T* __restrict__ q, T* __restrict__ k, T* __restrict__ v) {
-    const int half = d / 2, slots = H + 2 * Hkv;
+    const int half = d / 2, groups = half / ROPE_PAIRS, slots = H + 2 * Hkv;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= (int64_t)L * slots * half) return;
-    const int i = (int)(e % half);
-    const int slot = (int)((e / half) % slots);
-    const int t = (int)(e / ((int64_t)half * slots));
-    const T* src = qkv + ((int64_t)t * slots + slot) * d + 2 * i;
-    const float x0 = ld_f32(src), x1 = ld_f32(src + 1);
+    if (e >= (int64_t)L * slots * groups) return;
+    const int g = (int)(e % groups);
+    const int slot = (int)((e / groups) % slots);
+    const int t = (int)(e / ((int64_t)groups * slots));
+    const int i0 = g * ROPE_PAIRS;
+    const T* src = qkv + ((int64_t)t * slots + slot) * d + 2 * i0;
+    // 8 elements: one 16-B load for bf16, two for f32
+    float xv[2 * ROPE_PAIRS];
+    if constexpr (sizeof(T) == 2) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(src);
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int u = 0; u < ROPE_PAIRS; ++u) {
+            const float2 f = __bfloat1622float2(p2[u]);
+            xv[2 * u] = f.x;
+            xv[2 * u + 1] = f.y;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const float4 f = reinterpret_cast<const float4*>(src)[u];
+            xv[4 * u] = f.x;
+            xv[4 * u + 1] = f.y;
+            xv[4 * u + 2] = f.z;
+            xv[4 * u + 3] = f.w;
+        }
+    }
     T* dst;
-    float y0 = x0, y1 = x1;
     if (slot < H + Hkv) {
-        const float2 cs = table[(int64_t)t * half + i];
-        y0 = __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
-        y1 = __fadd_rn(__fmul_rn(x0, cs.y), __fmul_rn(x1, cs.x));
+        const float4* tb4 = reinterpret_cast<const float4*>(table + (int64_t)t * half + i0);
+        const float4 cs01 = tb4[0], cs23 = tb4[1];
+        const float2 tb[ROPE_PAIRS] = {make_float2(cs01.x, cs01.y), make_float2(cs01.z, cs01.w),
+                                       make_float2(cs23.x, cs23.y), make_float2(cs23.z, cs23.w)};
+#pragma unroll
+        for (int u = 0; u < ROPE_PAIRS; ++u) {
+            const float2 cs = tb[u];
+            const float x0 = xv[2 * u], x1 = xv[2 * u + 1];
+            xv[2 * u] = __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
+            xv[2 * u + 1] = __fadd_rn(__fmul_rn(x0, cs.y), __fmul_rn(x1, cs.x));
+        }
         dst = slot < H ? q + ((int64_t)slot * L + t) * d : k + ((int64_t)(slot - H) * L + t) * d;
     } else {
         dst = v + ((int64_t)(slot - H - Hkv) * L + t) * d;
     }
-    dst[2 * i] = Elem<T>::from_f32(y0);
-    dst[2 * i + 1] = Elem<T>::from_f32(y1);
+    if constexpr (sizeof(T) == 2) {
+        uint4 raw;
+        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int u = 0; u < ROPE_PAIRS; ++u) p2[u] = __floats2bfloat162_rn(xv[2 * u], xv[2 * u + 1]);
+        *reinterpret_cast<uint4*>(dst + 2 * i0) = raw;
+    } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            reinterpret_cast<float4*>(dst + 2 * i0)[u] =
+                make_float4(xv[4 * u], xv[4 * u + 1], xv[4 * u + 2], xv[4 * u + 3]);
+    }
 }
 
 // cat[t, h d + c] = heads[h, t, c]; 16-byte units.
@@ -125,11 +183,11 @@ int launch_rms_norm(const void* x, const float* gain, int64_t rows, int cols, fl
                     void* out, cudaStream_t st) {
     const unsigned grid = (unsigned)((rows + RMS_ROWS - 1) / RMS_ROWS);
     if (dtype == TSA_BF16)
-        rms_norm_kernel<__nv_bfloat16><<<grid, RMS_ROWS, 0, st>>>(
+        rms_norm_kernel<__nv_bfloat16><<<grid, RMS_THREADS, 0, st>>>(
             (const __nv_bfloat16*)x, gain, rows, cols, eps, (__nv_bfloat16*)out);
     else
-        rms_norm_kernel<float><<<grid, RMS_ROWS, 0, st>>>((const float*)x, gain, rows, cols, eps,
-                                                          (float*)out);
+        rms_norm_kernel<float><<<grid, RMS_THREADS, 0, st>>>((const float*)x, gain, rows, cols,
+                                                             eps, (float*)out);
     TSA_LAUNCH_CHECK("rms_norm");
     return 0;
 }
@@ -152,7 +210,10 @@ int launch_rope_table(int seq_len, int d_head, float theta, float* table, cudaSt
 int launch_split_heads_rope(const tsa_desc& d, const void* qkv, const float* table, void* q,
                             void* k, void* v, cudaStream_t st) {
     const int L = d.seq_len, H = d.n_heads, Hkv = d.n_kv_heads, D = d.d_head;
-    const int64_t n = (int64_t)L * (H + 2 * Hkv) * (D / 2);
+    if ((D / 2) % ROPE_PAIRS != 0)
+        return invalid("split_heads_rope: d_head must be a multiple of " +
+                       std::to_string(2 * ROPE_PAIRS));
+    const int64_t n = (int64_t)L * (H + 2 * Hkv) * (D / 2 / ROPE_PAIRS);
     const unsigned grid = (unsigned)((n + 255) / 256);
     const float2* tb = reinterpret_cast<const float2*>(table);
     if (d.dtype == TSA_BF16)

@@ -53,7 +53,7 @@ def test_rms_norm_zero_rows_and_gain_mismatch(cuda):
 
 
 @pytest.mark.parametrize("L,H,Hkv,d,theta", [(300, 4, 2, 64, 10000.0), (2048, 8, 2, 128, 500000.0),
-                                             (1, 2, 1, 8, 10000.0)])
+                                             (1, 2, 1, 16, 10000.0)])
 def test_split_heads_rope_vs_oracle(cuda, port, L, H, Hkv, d, theta):
     """split_heads + apply_rope (model.cpp:128-158): v copied exactly, q and k
     rotated with the reference's f32 arithmetic; cos/sin are the double libm
