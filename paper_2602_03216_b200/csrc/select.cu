@@ -114,8 +114,11 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
               int32_t* __restrict__ k_keep, int32_t* __restrict__ status, int mode,
               float* __restrict__ sl_out, int exact_total) {
     // kStaged: this CTA's slice of headsum (then s_l) lives in shared memory,
-    // so the three histogram levels do not re-read global memory
+    // so the three histogram levels do not re-read global memory; the four
+    // 16-bit mass-limb histograms follow it
     extern __shared__ float staged[];
+    uint32_t(*hist_limb)[2048] = reinterpret_cast<uint32_t(*)[2048]>(
+        staged + ((L + CL - 1) / CL + 3) / 4 * 4);
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
@@ -233,6 +236,8 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
         for (int b = tid; b < nb; b += BB) {
             hist_cnt[b] = 0;
             hist_mass[b] = 0;
+            if (kStaged)
+                for (int l = 0; l < 4; ++l) hist_limb[l][b] = 0;
         }
         __syncthreads();
         for (int base = t_begin; base < t_end; base += BB) {
@@ -247,17 +252,39 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
                     m = (unsigned long long)ldexp((double)sl, 62);
                 }
             }
-            // lanes of one bucket combine count and mass (three 21-bit limbs so
-            // the 32-lane sums cannot overflow) before one shared atomic
-            const uint32_t grp = __match_any_sync(0xffffffffu, b);
-            const uint32_t l0 = __reduce_add_sync(grp, (uint32_t)(m & 0x1FFFFFu));
-            const uint32_t l1 = __reduce_add_sync(grp, (uint32_t)((m >> 21) & 0x1FFFFFu));
-            const uint32_t l2 = __reduce_add_sync(grp, (uint32_t)(m >> 42));
-            if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (tid & 31)) {
-                atomicAdd(&hist_cnt[b], (uint32_t)__popc(grp));
-                atomicAdd(&hist_mass[b], (unsigned long long)l0 + ((unsigned long long)l1 << 21) +
-                                             ((unsigned long long)l2 << 42));
+            if (kStaged) {
+                // native 32-bit shared atomics per lane: the count and the mass in
+                // four 16-bit limbs (a slice has <= 16384 tokens, so a limb sum
+                // stays below 2^30); the group reductions of the general path
+                // serialise over the distinct buckets of a warp
+                if (b != 0xFFFFFFFFu) {
+                    atomicAdd(&hist_cnt[b], 1u);
+#pragma unroll
+                    for (int l = 0; l < 4; ++l)
+                        atomicAdd(&hist_limb[l][b], (uint32_t)((m >> (16 * l)) & 0xFFFFu));
+                }
+            } else {
+                // lanes of one bucket combine count and mass (three 21-bit limbs so
+                // the 32-lane sums cannot overflow) before one shared atomic
+                const uint32_t grp = __match_any_sync(0xffffffffu, b);
+                const uint32_t l0 = __reduce_add_sync(grp, (uint32_t)(m & 0x1FFFFFu));
+                const uint32_t l1 = __reduce_add_sync(grp, (uint32_t)((m >> 21) & 0x1FFFFFu));
+                const uint32_t l2 = __reduce_add_sync(grp, (uint32_t)(m >> 42));
+                if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (tid & 31)) {
+                    atomicAdd(&hist_cnt[b], (uint32_t)__popc(grp));
+                    atomicAdd(&hist_mass[b], (unsigned long long)l0 +
+                                                 ((unsigned long long)l1 << 21) +
+                                                 ((unsigned long long)l2 << 42));
+                }
             }
+        }
+        if (kStaged) {
+            __syncthreads();
+            for (int b = tid; b < nb; b += BB)
+                hist_mass[b] = (unsigned long long)hist_limb[0][b] +
+                               ((unsigned long long)hist_limb[1][b] << 16) +
+                               ((unsigned long long)hist_limb[2][b] << 32) +
+                               ((unsigned long long)hist_limb[3][b] << 48);
         }
         cluster.sync();
         // merge bucket range [rank*per, (rank+1)*per) over the cluster
@@ -712,11 +739,12 @@ static void launch_budget_kernel(const float* v, int L, double tau, int min_keep
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(budget_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSliceMax * 4);
+                                 kSliceMax * 4 + 4 * 2048 * 4);
             attr = true;
         }
-        budget_kernel<true><<<CL, BB, slice * 4, st>>>(v, L, tau, min_keep, k_keep, status, mode,
-                                                       sl_out, exact_total);
+        const int smem = (slice + 3) / 4 * 4 * 4 + 4 * 2048 * 4;  // slice + mass limbs
+        budget_kernel<true><<<CL, BB, smem, st>>>(v, L, tau, min_keep, k_keep, status, mode,
+                                                  sl_out, exact_total);
     } else {
         budget_kernel<false><<<CL, BB, 0, st>>>(v, L, tau, min_keep, k_keep, status, mode, sl_out,
                                                 exact_total);
