@@ -464,21 +464,16 @@ def profile_traffic(kernel):
 
 
 def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau):
-    """Through the public API (sparse_attention_layer / the C-ABI layer call)
-    with host buffers: pinned H2D of this rank's q/k/v, D2H of its output."""
+    """Through the public host-tensor API (sparse_attention_layer_host -> the
+    C-ABI tsa_sparse_attention_layer_host): every step copies this rank's q/k/v
+    from pinned host memory and its output back, pipelined with the compute."""
     hq, hk, hv = (t.cpu().pin_memory() for t in (ql, kl, vl))
     hout = torch.empty(ql.shape, dtype=ql.dtype).pin_memory()
     plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
-    dq, dk, dv = (torch.empty_like(t) for t in (ql, kl, vl))
-    out = torch.empty_like(ql)
     stream = torch.cuda.current_stream(device)
 
     def step():
-        dq.copy_(hq, non_blocking=True)
-        dk.copy_(hk, non_blocking=True)
-        dv.copy_(hv, non_blocking=True)
-        tsa.sparse_attention_layer(tsa.HeadTensors(dq, dk, dv), plan, out=out, stat=False)
-        hout.copy_(out, non_blocking=True)
+        tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan, device=device)
 
     for _ in range(args.warmup):
         step()
@@ -495,6 +490,9 @@ def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau):
     return {"value": round(ms, 3), "unit": "ms",
             "h2d_bytes_per_step": (nb(ql) + nb(kl) + nb(vl)) * world,
             "d2h_bytes_per_step": nb(ql) * world,
+            "api": "sparse_attention_layer_host (tsa_sparse_attention_layer_host): H2D of K/V/Q "
+                   "tails, then Q by head group, and D2H of each finished head group overlap the "
+                   "compute",
             "note": "per-rank head shard; world>1 runs the single-GPU layer call per rank"}
 
 

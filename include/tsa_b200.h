@@ -195,6 +195,23 @@ TSA_API int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const v
                                void* out, int32_t* idx_out, int32_t* k_keep_out,
                                int32_t* k_keep_host, void* ws, void* stream);
 
+/* The layer on HOST tensors (the reference's calling convention: its operators
+ * take host matrices): q/k/v/out_host [H|Hkv][L][d] in host memory (pinned for
+ * asynchronous copies), q/k/v/out device staging buffers of the same shapes.
+ * The transfers are pipelined with the compute: K, V and the Q tail rows are
+ * copied first (scoring needs them), the remaining Q rows follow in n_groups
+ * head groups (0 = one per KV head) while the compute stream scores, selects
+ * and compresses; the attention runs per head group as its Q rows arrive and
+ * each group's output rows are copied back while the next group computes.
+ * Completion on `stream` covers every copy.  f32 / d != 128 / dense mode: one
+ * copy in, the layer, one copy out. */
+TSA_API int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host,
+                                            const void* k_host, const void* v_host,
+                                            void* out_host, void* q, void* k, void* v, void* out,
+                                            int32_t* idx_out, int32_t* k_keep_out,
+                                            int32_t* k_keep_host, void* ws, int32_t n_groups,
+                                            void* stream);
+
 /* ---- Attention-branch producer / consumer (layer_forward, model.cpp:169-201) ----
  * The kernels cfg4's 32-layer prefill stack runs around the path; the
  * projections themselves (x W_q|k|v, cat W_o) are plain GEMMs for the caller's

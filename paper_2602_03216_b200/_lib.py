@@ -24,7 +24,7 @@ EXPORTS = (
     "tsa_attend", "tsa_attend_indexed", "tsa_zero_unselected", "tsa_gather_zero", "tsa_scatter",
     "tsa_scatter_rows", "tsa_check", "tsa_token_sparse_attention",
     "tsa_dense_attention", "tsa_sparse_attention_layer", "tsa_rms_norm", "tsa_rope_table",
-    "tsa_split_heads_rope", "tsa_heads_concat",
+    "tsa_split_heads_rope", "tsa_heads_concat", "tsa_sparse_attention_layer_host",
 )
 
 
@@ -79,6 +79,7 @@ def load() -> C.CDLL:
         "tsa_rope_table": (C.c_int, [I, I, C.c_float, P, P]),
         "tsa_split_heads_rope": (C.c_int, [D, P, P, P, P, P, P]),
         "tsa_heads_concat": (C.c_int, [D, P, P, P]),
+        "tsa_sparse_attention_layer_host": (C.c_int, [D, P, P, P, P, P, P, P, P, P, P, P, P, I, P]),
         "tsa_workspace_size": (C.c_int, [D, C.POINTER(C.c_size_t)]),
         "tsa_score": (C.c_int, [D, P, P, P, P, P]),
         "tsa_budget": (C.c_int, [D, P, P, P, P]),

@@ -1,6 +1,7 @@
 // C ABI (include/tsa_b200.h): host-side validation with the reference's
 // error wording, workspace layout, and the stage orchestration of the sparse
 // layer branch (model.cpp:169-183).
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -367,6 +368,142 @@ int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, 
                                  return layer_eager(d, q, k, v, out, idx_out, k_keep_out,
                                                     k_keep_host, ws, st);
                              });
+}
+
+// ---- host-buffer entry point: the layer with its transfers pipelined ----
+// q/k/v/out_host are the caller's host tensors (pinned for asynchronous copies);
+// q/k/v/out are device staging buffers of the same shapes.  K, V and the Q
+// tail rows go first (scoring needs them), the rest of Q follows in head
+// groups on a copy stream while the compute stream scores, selects and
+// compresses; the attention then runs per head group, each group waiting only
+// for its own Q rows, and every finished group's output rows are copied back
+// on a second copy stream while the next group computes.
+namespace {
+struct HostPipe {
+    cudaStream_t in = nullptr, out = nullptr;
+    cudaEvent_t start = nullptr, kvq = nullptr, q[64] = {}, done[64] = {}, fin = nullptr;
+};
+HostPipe* host_pipe(int device) {
+    static HostPipe pipes[16];
+    static bool init[16] = {};
+    if (device < 0 || device >= 16) return nullptr;
+    HostPipe& p = pipes[device];
+    if (!init[device]) {
+        const unsigned f = cudaEventDisableTiming;
+        if (cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&p.out, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p.start, f) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p.kvq, f) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p.fin, f) != cudaSuccess)
+            return nullptr;
+        for (int g = 0; g < 64; ++g)
+            if (cudaEventCreateWithFlags(&p.q[g], f) != cudaSuccess ||
+                cudaEventCreateWithFlags(&p.done[g], f) != cudaSuccess)
+                return nullptr;
+        init[device] = true;
+    }
+    return &p;
+}
+}  // namespace
+
+int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const void* k_host,
+                                    const void* v_host, void* out_host, void* q, void* k, void* v,
+                                    void* out, int32_t* idx_out, int32_t* k_keep_out,
+                                    int32_t* k_keep_host, void* ws, int32_t n_groups,
+                                    void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!q_host || !k_host || !v_host || !out_host || !q || !k || !v || !out || !k_keep_out)
+        return invalid("tsa_sparse_attention_layer_host: null pointer");
+    if (d->head_begin != 0 || d->head_end != d->n_heads)
+        return invalid("tsa_sparse_attention_layer_host: the whole layer (no head shard)");
+    cudaStream_t st = S(stream);
+    const size_t eb = elem_bytes(d->dtype), L = d->seq_len, D = d->d_head;
+    const size_t head_bytes = L * D * eb;
+    const int H = d->n_heads, Hkv = d->n_kv_heads, g = H / Hkv;
+    cudaError_t e;
+#define TSA_HCK(x)                                                          \
+    do {                                                                    \
+        if ((e = (x)) != cudaSuccess) return cuda_check(e, "layer_host");   \
+    } while (0)
+    const bool pipelined = attend_sm100_supported(*d) && d->mode != TSA_MODE_DENSE;
+    if (!pipelined) {  // one copy in, the layer, one copy out
+        TSA_HCK(cudaMemcpyAsync(q, q_host, H * head_bytes, cudaMemcpyHostToDevice, st));
+        TSA_HCK(cudaMemcpyAsync(k, k_host, Hkv * head_bytes, cudaMemcpyHostToDevice, st));
+        TSA_HCK(cudaMemcpyAsync(v, v_host, Hkv * head_bytes, cudaMemcpyHostToDevice, st));
+        if (int rc = tsa_sparse_attention_layer(d, q, k, v, out, idx_out, k_keep_out, k_keep_host,
+                                                ws, stream))
+            return rc;
+        TSA_HCK(cudaMemcpyAsync(out_host, out, H * head_bytes, cudaMemcpyDeviceToHost, st));
+        return 0;
+    }
+    int dev = 0;
+    TSA_HCK(cudaGetDevice(&dev));
+    HostPipe* p = host_pipe(dev);
+    if (!p) return cuda_check(cudaGetLastError(), "layer_host: streams");
+    // groups of whole KV groups
+    int G = n_groups > 0 ? n_groups : Hkv;
+    G = std::max(1, std::min({G, Hkv, 64}));
+    while (Hkv % G) --G;
+    const int hpg = H / G;  // query heads per group
+    const size_t lq = lq_of(*d);
+    auto* qd = static_cast<uint8_t*>(q);
+    auto* qh = static_cast<const uint8_t*>(q_host);
+    TSA_HCK(cudaEventRecord(p->start, st));  // the device buffers are free after prior work
+    TSA_HCK(cudaStreamWaitEvent(p->in, p->start, 0));
+    TSA_HCK(cudaStreamWaitEvent(p->out, p->start, 0));
+    // scoring inputs: K, V (compress needs them too) and the Q tail rows of every head
+    TSA_HCK(cudaMemcpyAsync(k, k_host, Hkv * head_bytes, cudaMemcpyHostToDevice, p->in));
+    TSA_HCK(cudaMemcpyAsync(v, v_host, Hkv * head_bytes, cudaMemcpyHostToDevice, p->in));
+    const size_t tail_off = (L - lq) * D * eb;
+    TSA_HCK(cudaMemcpy2DAsync(qd + tail_off, head_bytes, qh + tail_off, head_bytes, lq * D * eb, H,
+                              cudaMemcpyHostToDevice, p->in));
+    TSA_HCK(cudaEventRecord(p->kvq, p->in));
+    // the rest of Q, group by group
+    for (int gi = 0; gi < G; ++gi) {
+        const size_t h0 = (size_t)gi * hpg;
+        if (L > lq)
+            TSA_HCK(cudaMemcpy2DAsync(qd + h0 * head_bytes, head_bytes, qh + h0 * head_bytes,
+                                      head_bytes, (L - lq) * D * eb, hpg, cudaMemcpyHostToDevice,
+                                      p->in));
+        TSA_HCK(cudaEventRecord(p->q[gi], p->in));
+    }
+    // score -> budget -> select -> compress K/V (+ zero the dropped rows) on the compute stream
+    TSA_HCK(cudaStreamWaitEvent(st, p->kvq, 0));
+    const Workspace w = workspace_layout(*d);
+    float* s = at<float>(ws, w.scores);
+    int32_t* idx = idx_out ? idx_out : at<int32_t>(ws, w.idx);
+    int32_t* inv = at<int32_t>(ws, w.inv);
+    const int fb = forced_begin(*d);
+    const int nf = d->seq_len - fb;
+    int rc;
+    if ((rc = tsa_score(d, q, k, s, ws, stream))) return rc;
+    if ((rc = budget_impl(*d, s, k_keep_out, ws, std::max(1, nf), st))) return rc;
+    if ((rc = launch_select(*d, s, k_keep_out, nullptr, nf, fb, idx, inv, st))) return rc;
+    if ((rc = launch_gather_zero(*d, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
+                                 at<void>(ws, w.vc), inv, out, st)))
+        return rc;
+    // attention per head group, output rows streamed back as groups finish
+    for (int gi = 0; gi < G; ++gi) {
+        tsa_desc dg = *d;
+        dg.head_begin = gi * hpg;
+        dg.head_end = (gi + 1) * hpg;
+        TSA_HCK(cudaStreamWaitEvent(st, p->q[gi], 0));
+        if ((rc = launch_attend_indexed(dg, q, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
+                                        k_keep_out, out, st)))
+            return rc;
+        TSA_HCK(cudaEventRecord(p->done[gi], st));
+        TSA_HCK(cudaStreamWaitEvent(p->out, p->done[gi], 0));
+        TSA_HCK(cudaMemcpyAsync(static_cast<uint8_t*>(out_host) + (size_t)dg.head_begin * head_bytes,
+                                static_cast<uint8_t*>(out) + (size_t)dg.head_begin * head_bytes,
+                                (size_t)hpg * head_bytes, cudaMemcpyDeviceToHost, p->out));
+    }
+    if (k_keep_host)
+        TSA_HCK(cudaMemcpyAsync(k_keep_host, k_keep_out, 4, cudaMemcpyDeviceToHost, st));
+    TSA_HCK(cudaEventRecord(p->fin, p->out));
+    TSA_HCK(cudaStreamWaitEvent(st, p->fin, 0));  // completion on `stream` covers the copies
+#undef TSA_HCK
+    (void)g;
+    return 0;
 }
 
 // ---- attention-branch producer / consumer (cfg4 stack) ----

@@ -44,7 +44,7 @@ __all__ = [
     "SparsePlan", "LayerStat", "score_tokens", "aggregate_scores", "coverage_budget",
     "fixed_budget", "select_tokens", "validate", "dense_causal_attention",
     "token_sparse_attention", "sparse_attention_layer", "InvalidArgument", "NativeLibraryError",
-    "rms_norm", "rope_table", "split_heads_rope", "heads_concat",
+    "rms_norm", "rope_table", "split_heads_rope", "heads_concat", "sparse_attention_layer_host",
 ]
 
 
@@ -542,3 +542,37 @@ def heads_concat(heads: torch.Tensor, out: Optional[torch.Tensor] = None) -> tor
     _lib.check(_lib.load().tsa_heads_concat(C.byref(desc), _ptr(heads), _ptr(out),
                                             _stream(heads.device)))
     return out
+
+
+_staging: dict = {}
+
+
+def sparse_attention_layer_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                                out: torch.Tensor, plan: SparsePlan, device=None,
+                                n_groups: int = 0, scoring: int = 0) -> torch.Tensor:
+    """The sparse layer on HOST tensors (the reference's calling convention):
+    q [H, L, d], k / v [Hkv, L, d] and out [H, L, d] in (pinned) host memory.
+    Transfers are pipelined with the compute (tsa_sparse_attention_layer_host);
+    returns the device k_keep (int32[1]); ``out`` is complete once the current
+    stream of ``device`` has drained."""
+    device = torch.device(device or "cuda")
+    for t in (q, k, v, out):
+        if t.is_cuda:
+            raise InvalidArgument("sparse_attention_layer_host: q, k, v, out must be host tensors")
+    H, L, d = q.shape
+    Hkv = k.shape[0]
+    desc = _desc_for(H, Hkv, L, d, _dtype_code(q), mode=int(plan.mode), tau=plan.tau,
+                     s_fixed=plan.s_fixed, last_q=plan.last_q, kernel=plan.kernel,
+                     forced_policy=int(plan.forced), scoring=scoring)
+    key = (device.index, q.dtype, H, Hkv, L, d)
+    bufs = _staging.get(key)
+    if bufs is None:
+        bufs = _staging[key] = (torch.empty_like(q, device=device), torch.empty_like(k, device=device),
+                                torch.empty_like(v, device=device), torch.empty_like(out, device=device),
+                                torch.empty(1, dtype=torch.int32, device=device))
+    qd, kd, vd, od, kk = bufs
+    ws = _workspace(desc, device)
+    _lib.check(_lib.load().tsa_sparse_attention_layer_host(
+        C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(qd), _ptr(kd), _ptr(vd),
+        _ptr(od), None, _ptr(kk), None, _ptr(ws), n_groups, _stream(device)))
+    return kk

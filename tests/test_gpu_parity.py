@@ -455,3 +455,22 @@ def test_graph_replay_matches_eager_bitwise(cuda):
         g = lay.step_graphed(q, k, v).clone()
         assert torch.equal(g.view(torch.int16), eager.view(torch.int16))
         assert lay.graph_kernels >= 5
+
+
+@pytest.mark.parametrize("dtype,L", [(torch.bfloat16, 3000), (torch.float32, 700)])
+def test_host_api_equals_device_layer_bitwise(cuda, dtype, L):
+    """tsa_sparse_attention_layer_host (pipelined copies, attention per head
+    group) returns exactly the device-resident layer's output and budget."""
+    from paper_2602_03216_b200 import workloads
+    q, k, v = workloads.heavy_tailed_heads(8, 2, L, 128, seed=12)
+    q, k, v = (t.to(dtype) for t in (q, k, v))
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.02)
+    ref, st = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), plan)
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    hout = torch.full(q.shape, 7.0, dtype=dtype).pin_memory()
+    for groups in (0, 1, 2):
+        kk = tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan, n_groups=groups)
+        torch.cuda.synchronize()
+        assert int(kk.item()) == st.k_keep
+        assert torch.equal(hout.view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
+                           ref.cpu().view(torch.int16 if dtype == torch.bfloat16 else torch.int32))
