@@ -372,12 +372,12 @@ int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, 
 
 // ---- host-buffer entry point: the layer with its transfers pipelined ----
 // q/k/v/out_host are the caller's host tensors (pinned for asynchronous copies);
-// q/k/v/out are device staging buffers of the same shapes.  K, V and the Q
-// tail rows go first (scoring needs them), the rest of Q follows in head
-// groups on a copy stream while the compute stream scores, selects and
-// compresses; the attention then runs per head group, each group waiting only
-// for its own Q rows, and every finished group's output rows are copied back
-// on a second copy stream while the next group computes.
+// q/k/v/out are device staging buffers of the same shapes.  K and the Q tail
+// rows go first (scoring needs all of them), then each head group's V heads
+// and remaining Q rows on a copy stream while the compute stream scores and
+// selects; compress + attention then run per head group, each waiting only for
+// its own rows, and every finished group's output rows are copied back on a
+// second copy stream while the next group computes.
 namespace {
 struct HostPipe {
     cudaStream_t in = nullptr, out = nullptr;
@@ -451,23 +451,26 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
     TSA_HCK(cudaEventRecord(p->start, st));  // the device buffers are free after prior work
     TSA_HCK(cudaStreamWaitEvent(p->in, p->start, 0));
     TSA_HCK(cudaStreamWaitEvent(p->out, p->start, 0));
-    // scoring inputs: K, V (compress needs them too) and the Q tail rows of every head
+    // scoring inputs first: all of K and the Q tail rows of every head
     TSA_HCK(cudaMemcpyAsync(k, k_host, Hkv * head_bytes, cudaMemcpyHostToDevice, p->in));
-    TSA_HCK(cudaMemcpyAsync(v, v_host, Hkv * head_bytes, cudaMemcpyHostToDevice, p->in));
     const size_t tail_off = (L - lq) * D * eb;
     TSA_HCK(cudaMemcpy2DAsync(qd + tail_off, head_bytes, qh + tail_off, head_bytes, lq * D * eb, H,
                               cudaMemcpyHostToDevice, p->in));
     TSA_HCK(cudaEventRecord(p->kvq, p->in));
-    // the rest of Q, group by group
+    // then, group by group, the group's V heads and the rest of its Q rows
+    const int kvpg = Hkv / G;
     for (int gi = 0; gi < G; ++gi) {
-        const size_t h0 = (size_t)gi * hpg;
+        const size_t h0 = (size_t)gi * hpg, kv0 = (size_t)gi * kvpg;
+        TSA_HCK(cudaMemcpyAsync(static_cast<uint8_t*>(v) + kv0 * head_bytes,
+                                static_cast<const uint8_t*>(v_host) + kv0 * head_bytes,
+                                (size_t)kvpg * head_bytes, cudaMemcpyHostToDevice, p->in));
         if (L > lq)
             TSA_HCK(cudaMemcpy2DAsync(qd + h0 * head_bytes, head_bytes, qh + h0 * head_bytes,
                                       head_bytes, (L - lq) * D * eb, hpg, cudaMemcpyHostToDevice,
                                       p->in));
         TSA_HCK(cudaEventRecord(p->q[gi], p->in));
     }
-    // score -> budget -> select -> compress K/V (+ zero the dropped rows) on the compute stream
+    // score -> budget -> select on the compute stream
     TSA_HCK(cudaStreamWaitEvent(st, p->kvq, 0));
     const Workspace w = workspace_layout(*d);
     float* s = at<float>(ws, w.scores);
@@ -479,15 +482,16 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
     if ((rc = tsa_score(d, q, k, s, ws, stream))) return rc;
     if ((rc = budget_impl(*d, s, k_keep_out, ws, std::max(1, nf), st))) return rc;
     if ((rc = launch_select(*d, s, k_keep_out, nullptr, nf, fb, idx, inv, st))) return rc;
-    if ((rc = launch_gather_zero(*d, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
-                                 at<void>(ws, w.vc), inv, out, st)))
-        return rc;
-    // attention per head group, output rows streamed back as groups finish
+    // per head group: compress K/V (+ zero the dropped rows), attend, and stream
+    // the group's output rows back while the next group computes
     for (int gi = 0; gi < G; ++gi) {
         tsa_desc dg = *d;
         dg.head_begin = gi * hpg;
         dg.head_end = (gi + 1) * hpg;
         TSA_HCK(cudaStreamWaitEvent(st, p->q[gi], 0));
+        if ((rc = launch_gather_zero(dg, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
+                                     at<void>(ws, w.vc), inv, out, st)))
+            return rc;
         if ((rc = launch_attend_indexed(dg, q, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
                                         k_keep_out, out, st)))
             return rc;
