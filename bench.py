@@ -59,8 +59,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-dense", action="store_true")
-    p.add_argument("--extra", type=str, default="cfg2,cfg5,cfg4",
-                   help="other BASELINE configs measured after the headline (comma list: cfg2 = "
+    p.add_argument("--extra", type=str, default="cfg1,cfg2,cfg5,cfg4",
+                   help="other BASELINE configs measured after the headline (comma list: cfg1 = "
+                        "4K fp32 vs the CPU oracle, cfg2 = "
                         "32K uniform tau sweep, cfg5 = Llama-3-70B heads at 128K, cfg4 = 32-layer "
                         "prefill attention stack at 64K; '' = none)")
     p.add_argument("--calibrate", action="store_true",
@@ -416,11 +417,61 @@ def run_cfg4(args, tsa, rank, world, device):
     return out
 
 
+def run_cfg1(args, tsa, rank, world, device):
+    """BASELINE configs[0]: one layer, Llama-3-8B heads, L = 4K, fp32 inputs,
+    tau = 0.5, on one GPU next to the CPU oracle (reference-order arithmetic:
+    REFERENCE scoring, f32 attention), with the parity of the two."""
+    if world > 1 or rank != 0:
+        return {"skipped": "single-GPU config"}
+    from oracle.oracle import Oracle, n_threads_default
+    from paper_2602_03216_b200 import workloads
+    L, tau = 4096, 0.5
+    q, k, v = workloads.uniform_heads(H, HKV, L, D, seed=11, dtype=torch.float32, device=device)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
+    heads = tsa.HeadTensors(q, k, v)
+    out = torch.empty_like(q)
+    for _ in range(3):
+        tsa.sparse_attention_layer(heads, plan, out=out, stat=False)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(device)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = max(3, args.steps)
+    s.record(stream)
+    for _ in range(n):
+        tsa.sparse_attention_layer(heads, plan, out=out, stat=False)
+    e.record(stream)
+    torch.cuda.synchronize()
+    gpu_ms = s.elapsed_time(e) / n
+    o_gpu, st = tsa.sparse_attention_layer(heads, plan)
+    res = {"workload": "cfg1: one attention layer, Llama-3-8B heads (32 Q / 8 KV, d=128), "
+                       "L=4096, fp32 uniform inputs, tau=0.5", "gpu_ms": round(gpu_ms, 3),
+           "k_keep": st.k_keep, "dtype": "f32 (REFERENCE-order scoring, SIMT f32 attention)"}
+    if not args.no_cpu_baseline:
+        ora = Oracle("port")
+        T = n_threads_default()
+        qn, kn, vn = (t.cpu().numpy() for t in (q, k, v))
+        t0 = time.perf_counter()
+        sc = ora.score_tokens(qn, kn, 64, 7, n_threads=T)
+        kk = ora.coverage_budget(ora.aggregate_scores(sc), tau, 1)
+        idx = ora.select_tokens(sc, kk, [L - 1], n_threads=T)
+        o_cpu = ora.token_sparse_attention(qn, kn, vn, idx, n_threads=T)
+        cpu_ms = (time.perf_counter() - t0) * 1e3
+        same_idx = bool(np.array_equal(idx, st.selection.indices.cpu().numpy()))
+        res.update({"cpu_oracle_ms": round(cpu_ms, 1), "cpu_threads": T,
+                    "gpu_vs_cpu": round(cpu_ms / gpu_ms, 1), "k_keep_oracle": kk,
+                    "index_sets_identical": same_idx,
+                    "max_abs_err_vs_oracle": float(np.abs(o_gpu.cpu().numpy() - o_cpu).max())
+                    if same_idx else None})
+    return res
+
+
 def run_extra(name, args, tsa, workloads, Sharded, rank, world, device):
     """Latency of another BASELINE config: dense and every tau of its sweep,
     with the per-stage split of the sparse step at the last tau."""
     if name == "cfg4":
         return run_cfg4(args, tsa, rank, world, device)
+    if name == "cfg1":
+        return run_cfg1(args, tsa, rank, world, device)
     c = EXTRA[name]
     H_, Hkv_, L = c["H"], c["Hkv"], c["L"]
     if c["gen"] == "uniform":
@@ -449,6 +500,23 @@ def run_extra(name, args, tsa, workloads, Sharded, rank, world, device):
            "heads_per_gpu": sh.h_per, "dense_ms": round(dense_ms, 3) if dense_ms else None,
            "dense_TFLOP_per_s": round(f_attn(L, D, sh.h_per) / (dense_ms * 1e-3) / 1e12, 1)
            if dense_ms else None, "tau_sweep": rows}
+    if name == "cfg5" and world == 1:
+        # what one rank of the 8-GPU head-parallel run computes: 8 Q + 1 KV heads at the
+        # full layer's budget (fixed to the same k), without the two all-gathers
+        k_full = rows[-1]["k_keep"]
+        plan = tsa.SparsePlan(mode=tsa.SparseMode.kFixed, sparse_layers=[0],
+                              s_fixed=1.0 - k_full / L)
+        g = H_ // Hkv_
+        lay = Sharded(g, 1, L, D, torch.bfloat16, plan, rank=0, world=1, device=device)
+        ql, kl, vl = q[:g].contiguous(), k[:1].contiguous(), v[:1].contiguous()
+        ms_sh = time_layer(lay, ql, kl, vl, steps, warm, 1, device)
+        dense_sh = time_layer(lay, ql, kl, vl, steps, warm, 1, device, dense=True)
+        out["per_rank_of_8"] = {"heads": f"{g} Q / 1 KV", "k_keep": lay.k_keep,
+                                "ms": round(ms_sh, 3), "dense_ms": round(dense_sh, 3),
+                                "speedup_vs_dense": round(dense_sh / ms_sh, 3),
+                                "note": "one GPU's share of the G=8 head-parallel layer "
+                                        "(C1/C2 all-gathers not included)"}
+        del lay, ql, kl, vl
     del q, k, v
     return out
 
