@@ -474,3 +474,66 @@ def test_host_api_equals_device_layer_bitwise(cuda, dtype, L):
         assert int(kk.item()) == st.k_keep
         assert torch.equal(hout.view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
                            ref.cpu().view(torch.int16 if dtype == torch.bfloat16 else torch.int32))
+
+
+def test_cfg3_full_size_layer(cuda, port):
+    """BASELINE configs[2] at full size (L = 131072, 32 / 8 heads, bf16,
+    heavy-tailed inputs, tau = 0.01): budget within the FAST-scoring rule of the
+    oracle's, index sets identical to the oracle's selection at that budget up
+    to FAST near ties, sampled compressed rows (the costliest, at the end of
+    the causal range) within the bf16 gate, dropped rows +0.0 everywhere, and
+    tau = 0 sparse == dense bitwise at this size."""
+    from oracle.oracle import n_threads_default
+    from paper_2602_03216_b200 import workloads
+    L, H, Hkv = 131072, 32, 8
+    q, k, v = workloads.heavy_tailed_heads(H, Hkv, L, 128, seed=2602)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.01)
+    out, st = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), plan)
+    T = n_threads_default()
+    up_q, up_k = host(q), host(k)
+    s_ora = port.score_tokens(up_q, up_k, 64, 7, n_threads=T)
+    k_ora = port.coverage_budget(port.aggregate_scores(s_ora), 0.01, 1)
+    assert abs(st.k_keep - k_ora) <= parity.FAST_BUDGET_REL * L, (st.k_keep, k_ora)
+    idx = host(st.selection.indices).astype(np.int32)
+    ora_idx = port.select_tokens(s_ora, st.k_keep, [L - 1], n_threads=T)
+    parity.check_index_sets(idx, ora_idx, s_ora, [L - 1], rel_tol=parity.FAST_SCORE_REL)
+    keep = torch.zeros((H, L), dtype=torch.bool, device=q.device)
+    keep.scatter_(1, st.selection.indices.long(), True)
+    assert bool((out[~keep] == 0).all())
+    kk = st.k_keep
+    ref = port.token_sparse_attention_sampled(up_q, up_k, host(v), idx, head_stride=16,
+                                              r0=kk - 256, r1=kk, n_threads=T)
+    o = host(out)
+    for hh in (0, 16):
+        rows = idx[hh, kk - 256:kk]
+        assert parity.rel_l2(o[hh][rows], ref[hh][rows]) <= parity.BF16_REL_L2
+    del out, o, ref
+    plan0 = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.0)
+    a, st0 = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), plan0)
+    assert st0.k_keep == L
+    b, _ = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), tsa.SparsePlan())
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+@pytest.mark.parametrize("L", [1500, 4096])
+def test_llama70b_gqa8_layer_vs_oracle(cuda, port, L):
+    """cfg5 head geometry (8 query heads per KV head): FAST scoring tiles hold
+    2 heads and a KV group spans 4 tiles; budget, selection and output against
+    the oracle on the same bf16 inputs."""
+    from paper_2602_03216_b200 import workloads
+    H, Hkv = 16, 2
+    q, k, v = workloads.heavy_tailed_heads(H, Hkv, L, 128, seed=70)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.01)
+    out, st = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), plan)
+    up = [host(t) for t in (q, k, v)]
+    s_ora = port.score_tokens(up[0], up[1], 64, 7, n_threads=8)
+    k_ora = port.coverage_budget(port.aggregate_scores(s_ora), 0.01, 1)
+    assert abs(st.k_keep - k_ora) <= max(1, parity.FAST_BUDGET_REL * L)
+    idx = host(st.selection.indices).astype(np.int32)
+    ora_idx = port.select_tokens(s_ora, st.k_keep, [L - 1])
+    parity.check_index_sets(idx, ora_idx, s_ora, [L - 1], rel_tol=parity.FAST_SCORE_REL)
+    ref = port.token_sparse_attention(up[0], up[1], up[2], idx, n_threads=8)
+    o = host(out)
+    for hh in range(H):
+        assert parity.rel_l2(o[hh], ref[hh]) <= parity.BF16_REL_L2
+    assert parity.unselected_rows_zero(o, idx, L)
