@@ -59,14 +59,6 @@ struct __align__(1024) AttnSmem {
     uint32_t tmem_base;
 };
 
-// The issuing warp runs with 40 registers (setmaxnreg): launder the smem base
-// so the compiler recomputes the cheap descriptors instead of hoisting 16
-// loop-invariant 64-bit values (which spilled).
-__device__ __forceinline__ uint32_t opaque(uint32_t x) {
-    asm volatile("mov.b32 %0, %0;" : "+r"(x));
-    return x;
-}
-
 // Shared-memory descriptors differ between the K-steps of one operand only in
 // the start-address field (bits 0-13, address >> 4), which never carries into
 // the LBO field for shared-memory addresses: build the low word once per
