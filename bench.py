@@ -360,7 +360,8 @@ def run_cfg4(args, tsa, rank, world, device):
     if world > 1:
         return {"skipped": "the stack runs single-process in this build"}
     L, D, n_layers = 65536, 4096, 32
-    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=args.tau)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=list(range(n_layers)),
+                          tau=args.tau)
     st = PrefillAttentionStack(n_layers, H, HKV, D_HEAD, D, L, plan, seed=4, device=device)
     x0 = structured_hidden(L, D, seed=5, device=device)
     x = torch.empty_like(x0)
@@ -399,9 +400,25 @@ def run_cfg4(args, tsa, rank, world, device):
     split.pop("start", None)
     kk = st.k_keep.cpu().tolist()
     F = sum(f_attn(k, D_HEAD, H) for k in kk)
+    # the paper's setting: drift calibration (drift.cpp:67-80, delta = 0.5) picks the
+    # lower-drift half of the layers for sparse attention, the rest stay dense
+    prof = st.calibrate(x0, delta=0.5)
+    run(False)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    run(False)
+    e.record(stream)
+    torch.cuda.synchronize()
+    out["drift_delta_0.5"] = {"ms": round(s.elapsed_time(e), 1),
+                              "speedup_vs_dense": round(out["dense_ms"] / s.elapsed_time(e), 3),
+                              "sparse_layers": prof["sparse_layers"],
+                              "R": [round(r, 5) for r in prof["R"]],
+                              "k_keep_per_layer": st.k_keep.cpu().tolist()}
     out.update({
         "workload": "cfg4: 32-layer prefill attention stack (rms_norm -> QKV GEMM -> RoPE -> "
-                    "sparse attention -> W_o GEMM + residual), Llama-3-8B heads (32 Q / 8 KV, "
+                    "sparse attention on every layer -> W_o GEMM + residual; drift_delta_0.5: "
+                    "the paper's drift-selected half), Llama-3-8B heads (32 Q / 8 KV, "
                     "d=128, d_model 4096), L=65536, bf16, random-init layers (xavier; W_q, W_k "
                     "x per-layer gain 2.5-4.0) on a structured synthetic hidden state",
         "seq_len": L, "n_layers": n_layers, "tau": args.tau,

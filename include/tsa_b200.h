@@ -238,6 +238,19 @@ TSA_API int tsa_split_heads_rope(const tsa_desc* d, const void* qkv, const float
 /* Head concat before W_o (model.cpp:196-200): heads [H][L][d] -> cat [L][H d]. */
 TSA_API int tsa_heads_concat(const tsa_desc* d, const void* heads, void* cat, void* stream);
 
+/* ---- Drift calibration (drift.hpp, drift.cpp:14-65) ----
+ * compute_drift for one layer boundary: *r_out (device double) = mean over
+ * the rows t of |next[t] - prev[t]|_2 / (|prev[t]|_2 + epsilon), with the
+ * sums in double in the reference's order (j, then t ascending; f32 inputs
+ * match it bit for bit).  ws: rows doubles of device scratch. */
+TSA_API int tsa_layer_drift(const void* prev, const void* next, int64_t rows, int32_t cols,
+                            int32_t dtype, double epsilon, double* r_out, void* ws, void* stream);
+
+/* select_sparse_layers (host): R_hat[l] = #{k : R[k] <= R[l]} / n and the
+ * layers with R_hat <= delta, ascending (layers needs room for n). */
+TSA_API int tsa_select_sparse_layers(const double* R, int32_t n, double delta, double* R_hat,
+                                     int32_t* layers, int32_t* n_layers);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,6 +31,7 @@ REF_SO = HERE / "_ref" / "libtsa_ref.so"
 
 _f32p = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
 _i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _I = C.c_int
 _D = C.c_double
 
@@ -82,6 +83,8 @@ class Oracle:
             L.tsa_oracle_apply_rope.argtypes = [_f32p, _I, _I, C.c_float, _f32p]
             L.tsa_oracle_project_qkv.argtypes = [_f32p, _f32p, _f32p, _f32p, _I, _I, _I, _I, _I,
                                                  C.c_float, _f32p, _f32p, _f32p]
+            L.tsa_oracle_compute_drift.argtypes = [_f32p, _I, _I, _I, _D, _f64p]
+            L.tsa_oracle_select_sparse_layers.argtypes = [_f64p, _I, _D, _f64p, _i32p, C.POINTER(_I)]
             L.tsa_oracle_rng_new.restype = C.c_void_p
             L.tsa_oracle_rng_new.argtypes = [C.c_uint64]
             L.tsa_oracle_rng_free.argtypes = [C.c_void_p]
@@ -109,6 +112,8 @@ class Oracle:
             L.tsa_ref_apply_rope.argtypes = [_f32p, _I, _I, C.c_float, _f32p]
             L.tsa_ref_project_qkv.argtypes = [_f32p, _f32p, _f32p, _f32p, _I, _I, _I, _I, _I,
                                               C.c_float, _f32p, _f32p, _f32p]
+            L.tsa_ref_compute_drift.argtypes = [_f32p, _I, _I, _I, _D, _f64p]
+            L.tsa_ref_select_sparse_layers.argtypes = [_f64p, _I, _D, _f64p, _i32p, C.POINTER(_I)]
 
     def _check(self, rc: int):
         if rc != 0:
@@ -258,6 +263,22 @@ class Oracle:
         v = np.empty((Hkv, L, d), np.float32)
         self._check(self._fn("project_qkv")(x_norm, wq, wk, wv, L, D, H, Hkv, d, theta, q, k, v))
         return q, k, v
+
+    def compute_drift(self, hidden, epsilon=1e-6):
+        """drift.cpp:14-45: hidden [n_mats, rows, cols] -> R [n_mats - 1] (double)."""
+        h = _f32(hidden)
+        R = np.empty(h.shape[0] - 1, np.float64)
+        self._check(self._fn("compute_drift")(h, h.shape[0], h.shape[1], h.shape[2], epsilon, R))
+        return R
+
+    def select_sparse_layers(self, R, delta):
+        """drift.cpp:47-65 -> (R_hat, sparse layer list)."""
+        R = np.ascontiguousarray(R, np.float64)
+        R_hat = np.empty_like(R)
+        layers = np.empty(R.size, np.int32)
+        m = _I()
+        self._check(self._fn("select_sparse_layers")(R, R.size, delta, R_hat, layers, C.byref(m)))
+        return R_hat, layers[:m.value].tolist()
 
     def avg_pool_1d(self, v, kernel):
         assert self.kind == "port"

@@ -242,3 +242,28 @@ int tsa_ref_project_qkv(const float* x_norm, const float* wq, const float* wk, c
 }
 
 }  // extern "C"
+
+// ---- drift calibration (drift.cpp:14-65) ----
+#include "tsa/drift.hpp"
+extern "C" {
+// hidden: n_mats row-major [rows x cols] f32 matrices back to back; R_out [n_mats - 1].
+int tsa_ref_compute_drift(const float* hidden, int n_mats, int rows, int cols, double epsilon,
+                          double* R_out) {
+    return guarded([&] {
+        std::vector<Matrix> h;
+        for (int i = 0; i < n_mats; ++i) h.push_back(to_mat(hidden + size_t(i) * rows * cols, rows, cols));
+        const std::vector<double> R = compute_drift(h, epsilon);
+        std::copy(R.begin(), R.end(), R_out);
+    });
+}
+
+int tsa_ref_select_sparse_layers(const double* R, int n, double delta, double* R_hat_out,
+                                 int* layers_out, int* n_layers) {
+    return guarded([&] {
+        const DriftProfile p = select_sparse_layers(std::vector<double>(R, R + n), delta);
+        std::copy(p.R_hat.begin(), p.R_hat.end(), R_hat_out);
+        std::copy(p.sparse_layers.begin(), p.sparse_layers.end(), layers_out);
+        *n_layers = static_cast<int>(p.sparse_layers.size());
+    });
+}
+}  // extern "C"

@@ -714,3 +714,46 @@ EXPORT int tsa_oracle_project_qkv(const float* x_norm, const float* wq, const fl
     free(head);
     return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * Drift calibration (drift.cpp:14-65): R[l] = mean_t |h[l+1][t] - h[l][t]|_2 /
+ * (|h[l][t]|_2 + eps), sums in double with j and t ascending; normalized ranks
+ * R_hat[l] = #{k : R[k] <= R[l]} / n and the sparse set {l : R_hat[l] <= delta}.
+ */
+EXPORT int tsa_oracle_compute_drift(const float* hidden, int n_mats, int rows, int cols,
+                                    double epsilon, double* R_out) {
+    if (n_mats < 2) return fail("compute_drift: need at least 2 hidden-state matrices, got %ld",
+                                n_mats, 0, 0);
+    if (!(epsilon > 0)) return fail("compute_drift: epsilon must be positive", 0, 0, 0);
+    for (int l = 0; l + 1 < n_mats; ++l) {
+        const float* a = hidden + (size_t)l * rows * cols;
+        const float* b = a + (size_t)rows * cols;
+        double acc = 0.0;
+        for (int t = 0; t < rows; ++t) {
+            double num = 0.0, den = 0.0;
+            for (int j = 0; j < cols; ++j) {
+                const double d = (double)b[(size_t)t * cols + j] - a[(size_t)t * cols + j];
+                num += d * d;
+                den += (double)a[(size_t)t * cols + j] * a[(size_t)t * cols + j];
+            }
+            acc += sqrt(num) / (sqrt(den) + epsilon);
+        }
+        R_out[l] = acc / (double)rows;
+    }
+    return 0;
+}
+
+EXPORT int tsa_oracle_select_sparse_layers(const double* R, int n, double delta, double* R_hat,
+                                           int* layers, int* n_layers) {
+    if (n < 1) return fail("select_sparse_layers: empty drift vector", 0, 0, 0);
+    int m = 0;
+    for (int l = 0; l < n; ++l) {
+        int count = 0;
+        for (int k = 0; k < n; ++k)
+            if (R[k] <= R[l]) ++count;
+        R_hat[l] = (double)count / (double)n;
+        if (R_hat[l] <= delta) layers[m++] = l;
+    }
+    *n_layers = m;
+    return 0;
+}

@@ -25,6 +25,7 @@ EXPORTS = (
     "tsa_scatter_rows", "tsa_check", "tsa_token_sparse_attention",
     "tsa_dense_attention", "tsa_sparse_attention_layer", "tsa_rms_norm", "tsa_rope_table",
     "tsa_split_heads_rope", "tsa_heads_concat", "tsa_sparse_attention_layer_host",
+    "tsa_layer_drift", "tsa_select_sparse_layers",
 )
 
 
@@ -79,6 +80,8 @@ def load() -> C.CDLL:
         "tsa_rope_table": (C.c_int, [I, I, C.c_float, P, P]),
         "tsa_split_heads_rope": (C.c_int, [D, P, P, P, P, P, P]),
         "tsa_heads_concat": (C.c_int, [D, P, P, P]),
+        "tsa_layer_drift": (C.c_int, [P, P, C.c_int64, I, I, C.c_double, P, P, P]),
+        "tsa_select_sparse_layers": (C.c_int, [P, I, C.c_double, P, P, P]),
         "tsa_sparse_attention_layer_host": (C.c_int, [D, P, P, P, P, P, P, P, P, P, P, P, P, I, P]),
         "tsa_workspace_size": (C.c_int, [D, C.POINTER(C.c_size_t)]),
         "tsa_score": (C.c_int, [D, P, P, P, P, P]),

@@ -542,4 +542,32 @@ int tsa_heads_concat(const tsa_desc* d, const void* heads, void* cat, void* stre
     return launch_heads_concat(*d, heads, cat, S(stream));
 }
 
+// ---- drift calibration (drift.cpp:14-65) ----
+int tsa_layer_drift(const void* prev, const void* next, int64_t rows, int32_t cols, int32_t dtype,
+                    double epsilon, double* r_out, void* ws, void* stream) {
+    if (!(epsilon > 0)) return invalid("compute_drift: epsilon must be positive");
+    if (rows < 1 || cols < 1 || !prev || !next || !r_out || !ws)
+        return invalid("compute_drift: bad arguments");
+    if (dtype != TSA_F32 && dtype != TSA_BF16) return invalid("compute_drift: unknown dtype");
+    return launch_layer_drift(prev, next, rows, cols, dtype, epsilon, r_out,
+                              static_cast<double*>(ws), S(stream));
+}
+
+int tsa_select_sparse_layers(const double* R, int32_t n, double delta, double* R_hat,
+                             int32_t* layers, int32_t* n_layers) {
+    if (n < 1 || !R) return invalid("select_sparse_layers: empty drift vector");
+    int m = 0;
+    for (int l = 0; l < n; ++l) {
+        int count = 0;
+        for (int k = 0; k < n; ++k)
+            if (R[k] <= R[l]) ++count;
+        const double rh = static_cast<double>(count) / static_cast<double>(n);
+        if (R_hat) R_hat[l] = rh;
+        if (rh <= delta && layers) layers[m] = l;
+        if (rh <= delta) ++m;
+    }
+    if (n_layers) *n_layers = m;
+    return 0;
+}
+
 }  // extern "C"

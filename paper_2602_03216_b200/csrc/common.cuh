@@ -125,6 +125,8 @@ int launch_rope_table(int seq_len, int d_head, float theta, float* table, cudaSt
 int launch_split_heads_rope(const tsa_desc& d, const void* qkv, const float* table, void* q,
                             void* k, void* v, cudaStream_t st);
 int launch_heads_concat(const tsa_desc& d, const void* heads, void* cat, cudaStream_t st);
+int launch_layer_drift(const void* prev, const void* next, int64_t rows, int cols, int dtype,
+                       double eps, double* out, double* ratio_ws, cudaStream_t st);
 // attend_simt.cu / attend_sm100.cu
 int launch_attend_simt(const tsa_desc& d, const void* q, const void* k, const void* v,
                        const int32_t* n_dev, int32_t n_const, int32_t kv_group, int32_t rows_per_head,

@@ -12,6 +12,10 @@
 //                                       [H, L, d], k / v [Hkv, L, d], RoPE on q and
 //                                       k in f32 (x0 c - x1 s, x0 s + x1 c, no FMA)
 //   heads_concat      model.cpp:196-200 [H, L, d] -> [L, H d] for the W_O GEMM
+//   layer_drift       drift.cpp:14-45   per token |h'[t] - h[t]| / (|h[t]| + eps)
+//                                       with the sums in double, j ascending, then
+//                                       the token mean summed t ascending (the
+//                                       reference's order: bit-exact for f32)
 //
 // The projections themselves (x W_q, x W_k, x W_v, cat W_o) are plain GEMMs and
 // go to cuBLAS through the host; everything here is HBM-bound byte movement.
@@ -177,6 +181,57 @@ __global__ void __launch_bounds__(256) heads_concat_kernel(const uint4* __restri
     cat[e] = heads[((int64_t)h * L + t) * units_per_row + c];
 }
 
+// Drift of one layer boundary, pass 1: a CTA owns 32 tokens; both matrices
+// stream through shared memory in 128-column chunks and lane t of warp 0
+// accumulates num = sum (b - a)^2 and den = sum a^2 in double, j ascending.
+constexpr int DR_ROWS = 32, DR_CHUNK = 128, DR_THREADS = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(DR_THREADS) drift_ratio_kernel(const T* __restrict__ a,
+                                                                const T* __restrict__ b,
+                                                                int64_t rows, int cols,
+                                                                double eps,
+                                                                double* __restrict__ ratio) {
+    __shared__ float ca[DR_ROWS][DR_CHUNK + 1], cb[DR_ROWS][DR_CHUNK + 1];
+    const int64_t r0 = (int64_t)blockIdx.x * DR_ROWS;
+    const int nrows = rows - r0 < DR_ROWS ? (int)(rows - r0) : DR_ROWS;
+    const int tid = threadIdx.x;
+    double num = 0.0, den = 0.0;
+    for (int c0 = 0; c0 < cols; c0 += DR_CHUNK) {
+        const int n = min(DR_CHUNK, cols - c0);
+        for (int e = tid; e < DR_ROWS * DR_CHUNK; e += DR_THREADS) {
+            const int rr = e / DR_CHUNK, j = e % DR_CHUNK;
+            float va = 0.0f, vb = 0.0f;
+            if (rr < nrows && j < n) {
+                va = ld_f32(a + (r0 + rr) * cols + c0 + j);
+                vb = ld_f32(b + (r0 + rr) * cols + c0 + j);
+            }
+            ca[rr][j] = va;
+            cb[rr][j] = vb;
+        }
+        __syncthreads();
+        if (tid < DR_ROWS) {
+            for (int j = 0; j < n; ++j) {
+                const double x = (double)ca[tid][j];
+                const double d = __dsub_rn((double)cb[tid][j], x);
+                num = __dadd_rn(num, __dmul_rn(d, d));
+                den = __dadd_rn(den, __dmul_rn(x, x));
+            }
+        }
+        __syncthreads();
+    }
+    if (tid < nrows)
+        ratio[r0 + tid] = __ddiv_rn(__dsqrt_rn(num), __dadd_rn(__dsqrt_rn(den), eps));
+}
+
+// Pass 2: the token mean, summed sequentially (t ascending) as the reference does.
+__global__ void drift_mean_kernel(const double* __restrict__ ratio, int64_t rows,
+                                  double* __restrict__ out) {
+    double acc = 0.0;
+    for (int64_t t = 0; t < rows; ++t) acc = __dadd_rn(acc, ratio[t]);
+    *out = __ddiv_rn(acc, (double)rows);
+}
+
 }  // namespace
 
 int launch_rms_norm(const void* x, const float* gain, int64_t rows, int cols, float eps, int dtype,
@@ -235,6 +290,26 @@ int launch_heads_concat(const tsa_desc& d, const void* heads, void* cat, cudaStr
     heads_concat_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
         (const uint4*)heads, d.seq_len, d.n_heads, upr, (uint4*)cat);
     TSA_LAUNCH_CHECK("heads_concat");
+    return 0;
+}
+
+}  // namespace tsa
+
+namespace tsa {
+
+int launch_layer_drift(const void* prev, const void* next, int64_t rows, int cols, int dtype,
+                       double eps, double* out, double* ratio_ws, cudaStream_t st) {
+    const unsigned grid = (unsigned)((rows + DR_ROWS - 1) / DR_ROWS);
+    if (dtype == TSA_BF16)
+        drift_ratio_kernel<__nv_bfloat16><<<grid, DR_THREADS, 0, st>>>(
+            (const __nv_bfloat16*)prev, (const __nv_bfloat16*)next, rows, cols, eps, ratio_ws);
+    else
+        drift_ratio_kernel<float><<<grid, DR_THREADS, 0, st>>>((const float*)prev,
+                                                               (const float*)next, rows, cols,
+                                                               eps, ratio_ws);
+    TSA_LAUNCH_CHECK("drift_ratio");
+    drift_mean_kernel<<<1, 1, 0, st>>>(ratio_ws, rows, out);
+    TSA_LAUNCH_CHECK("drift_mean");
     return 0;
 }
 

@@ -45,6 +45,7 @@ __all__ = [
     "fixed_budget", "select_tokens", "validate", "dense_causal_attention",
     "token_sparse_attention", "sparse_attention_layer", "InvalidArgument", "NativeLibraryError",
     "rms_norm", "rope_table", "split_heads_rope", "heads_concat", "sparse_attention_layer_host",
+    "layer_drift", "select_sparse_layers",
 ]
 
 
@@ -576,3 +577,32 @@ def sparse_attention_layer_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tenso
         C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(qd), _ptr(kd), _ptr(vd),
         _ptr(od), None, _ptr(kk), None, _ptr(ws), n_groups, _stream(device)))
     return kk
+
+
+# ------------------------------------------------------------ drift calibration
+def layer_drift(prev: torch.Tensor, nxt: torch.Tensor, epsilon: float = 1e-6,
+                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """compute_drift (drift.cpp:14-45) for one layer boundary: the mean over rows
+    of |next - prev| / (|prev| + eps), in double; returns a device float64 [1]
+    (written asynchronously, no host sync)."""
+    _require_cuda(prev, nxt)
+    if prev.shape != nxt.shape or prev.dim() != 2 or prev.dtype != nxt.dtype:
+        raise InvalidArgument(f"compute_drift: shape {tuple(nxt.shape)} != {tuple(prev.shape)}")
+    prev, nxt = prev.contiguous(), nxt.contiguous()
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=prev.device)
+    ws = torch.empty(prev.shape[0], dtype=torch.float64, device=prev.device)
+    _lib.check(_lib.load().tsa_layer_drift(_ptr(prev), _ptr(nxt), prev.shape[0], prev.shape[1],
+                                           _dtype_code(prev), epsilon, _ptr(out), _ptr(ws),
+                                           _stream(prev.device)))
+    return out
+
+
+def select_sparse_layers(R: Sequence[float], delta: float):
+    """drift.cpp:47-65: (R_hat, sparse layers) with R_hat[l] = #{k: R[k] <= R[l]} / n."""
+    r = (C.c_double * len(R))(*[float(x) for x in R])
+    rh = (C.c_double * len(R))()
+    layers = (C.c_int32 * len(R))()
+    m = C.c_int32()
+    _lib.check(_lib.load().tsa_select_sparse_layers(r, len(R), delta, rh, layers, C.byref(m)))
+    return list(rh), list(layers[:m.value])

@@ -130,7 +130,25 @@ class PrefillAttentionStack:
         return x
 
     def forward(self, x: torch.Tensor, dense: bool = False, marks=None) -> torch.Tensor:
-        """All layers in place on x [L, D] (the residual stream)."""
+        """All layers in place on x [L, D] (the residual stream).  Layers outside
+        ``plan.sparse_layers`` run dense (layer_forward, model.cpp:184-194)."""
         for i in range(self.n_layers):
-            self.layer(i, x, dense=dense, marks=marks)
+            self.layer(i, x, dense=dense or not self.plan.is_sparse_layer(i), marks=marks)
         return x
+
+    def calibrate(self, x: torch.Tensor, delta: float = 0.5, epsilon: float = 1e-6) -> dict:
+        """drift.cpp:67-80 for one prompt: a dense pass over a copy of x, the drift
+        R[l] of every layer boundary (tsa_layer_drift, on the device), then the
+        rank selection; sets plan.sparse_layers and returns the profile."""
+        h = x.clone()
+        prev = torch.empty_like(h)
+        R = torch.empty(self.n_layers, dtype=torch.float64, device=self.device)
+        for i in range(self.n_layers):
+            prev.copy_(h)
+            self.layer(i, h, dense=True)
+            ops.layer_drift(prev, h, epsilon, out=R[i:i + 1])
+        r = R.cpu().tolist()
+        r_hat, layers = ops.select_sparse_layers(r, delta)
+        self.plan.sparse_layers = layers
+        return {"R": r, "R_hat": r_hat, "delta": delta, "sparse_layers": layers,
+                "epsilon": epsilon}

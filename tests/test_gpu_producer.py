@@ -99,7 +99,8 @@ def test_heads_concat_exact(cuda):
 
 def _stack(L, n_layers=2, tau=0.01, seed=0):
     from paper_2602_03216_b200.stack import PrefillAttentionStack
-    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=list(range(n_layers)),
+                          tau=tau)
     return PrefillAttentionStack(n_layers, 8, 2, 128, 512, L, plan, seed=seed, device="cuda")
 
 
@@ -141,3 +142,41 @@ def test_stack_varies_selection_and_tau0_equals_dense(cuda):
     b = s0.forward(x.clone(), dense=True)
     assert torch.equal(a.view(torch.int16), b.view(torch.int16))
     assert torch.isfinite(a.float()).all()
+
+
+@pytest.mark.parametrize("rows,cols", [(40, 64), (129, 4096), (1, 3)])
+def test_layer_drift_f32_bit_exact(cuda, port, rows, cols):
+    """compute_drift (drift.cpp:14-45) per boundary: double sums in the
+    reference's order -> bit-exact against the oracle (pinned to drift.cpp)."""
+    rng = RefRng(rows * 7 + cols)
+    h = np.stack([rng.random_matrix(rows, cols, 1.0 + 0.3 * i) for i in range(3)])
+    ref = port.compute_drift(h, 1e-6)
+    for l in range(2):
+        g = float(tsa.layer_drift(dev(h[l]), dev(h[l + 1]), 1e-6).item())
+        assert np.float64(g).view(np.uint64) == ref[l].view(np.uint64)
+
+
+def test_select_sparse_layers_matches_oracle(cuda, port):
+    for R in ([0.3, 0.1, 0.2, 0.4], [1.0, 1.0, 1.0], [0.5], [0.2, 0.2, 0.1, 0.3, 0.1]):
+        for delta in (0.0, 0.25, 0.5, 1.0):
+            rh, layers = tsa.select_sparse_layers(R, delta)
+            orh, ol = port.select_sparse_layers(np.array(R), delta)
+            assert np.array_equal(np.array(rh), orh) and layers == ol
+
+
+def test_stack_drift_calibration_selects_half(cuda):
+    """drift.cpp:67-80 on the stack: delta = 0.5 picks the lower-drift half of
+    the layers; those run sparse, the rest dense (budget = L)."""
+    from paper_2602_03216_b200.stack import structured_hidden
+    L = 1024
+    st = _stack(L, n_layers=4)
+    x = structured_hidden(L, 512, seed=3)
+    prof = st.calibrate(x, delta=0.5)
+    assert len(prof["sparse_layers"]) == 2 and len(prof["R"]) == 4
+    st.forward(x.clone())
+    kk = st.k_keep.cpu().tolist()
+    for i in range(4):
+        if i in prof["sparse_layers"]:
+            assert kk[i] <= L
+        else:
+            assert kk[i] == L
