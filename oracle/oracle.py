@@ -113,6 +113,7 @@ class Oracle:
             L.tsa_ref_project_qkv.argtypes = [_f32p, _f32p, _f32p, _f32p, _I, _I, _I, _I, _I,
                                               C.c_float, _f32p, _f32p, _f32p]
             L.tsa_ref_compute_drift.argtypes = [_f32p, _I, _I, _I, _D, _f64p]
+            L.tsa_ref_estimate_flops.argtypes = [_I, _I, _I, _i32p, _I, _I, _I, _f64p]
             L.tsa_ref_select_sparse_layers.argtypes = [_f64p, _I, _D, _f64p, _i32p, C.POINTER(_I)]
 
     def _check(self, rc: int):
@@ -279,6 +280,17 @@ class Oracle:
         m = _I()
         self._check(self._fn("select_sparse_layers")(R, R.size, delta, R_hat, layers, C.byref(m)))
         return R_hat, layers[:m.value].tolist()
+
+    def estimate_flops(self, seq_len, d_head, n_heads, k_keep, last_q=64, kernel=7):
+        """flops.cpp:12-51 (reference only); k_keep entries None = dense layer."""
+        assert self.kind == "reference"
+        kk = np.array([-1 if k is None else k for k in k_keep], np.int32)
+        out = np.empty(6, np.float64)
+        self._check(self.lib.tsa_ref_estimate_flops(seq_len, d_head, n_heads, kk, kk.size, last_q,
+                                                    kernel, out))
+        keys = ["dense_flops", "sparse_flops", "overhead_flops", "attn_ratio", "est_speedup",
+                "avg_map_sparsity"]
+        return dict(zip(keys, out.tolist()))
 
     def avg_pool_1d(self, v, kernel):
         assert self.kind == "port"

@@ -267,3 +267,25 @@ int tsa_ref_select_sparse_layers(const double* R, int n, double delta, double* R
     });
 }
 }  // extern "C"
+
+// ---- FLOP model (flops.cpp:12-51) ----
+#include "tsa/flops.hpp"
+extern "C" {
+// k_keep[i] < 0 marks a dense layer (nullopt); out: dense, sparse, overhead, attn_ratio,
+// est_speedup, avg_map_sparsity.
+int tsa_ref_estimate_flops(int seq_len, int d_head, int n_heads, const int* k_keep, int n_layers,
+                           int last_q, int kernel, double* out) {
+    return guarded([&] {
+        std::vector<std::optional<int>> b;
+        for (int i = 0; i < n_layers; ++i)
+            b.push_back(k_keep[i] < 0 ? std::nullopt : std::optional<int>(k_keep[i]));
+        const FlopReport r = estimate_flops(seq_len, d_head, n_heads, b, last_q, kernel);
+        out[0] = r.dense_flops;
+        out[1] = r.sparse_flops;
+        out[2] = r.overhead_flops;
+        out[3] = r.attn_ratio;
+        out[4] = r.est_speedup;
+        out[5] = r.avg_map_sparsity;
+    });
+}
+}  // extern "C"

@@ -97,6 +97,7 @@ class PrefillAttentionStack:
                 wqkv=torch.cat([wq, wk, wv], dim=1).to(dtype).contiguous(),
                 wo=wo.to(dtype).contiguous(), qk_gain=qk_gain[i]))
             del wq, wk, wv, wo
+        self.scoring = scoring
         self.attn = ShardedSparseAttention(n_heads, n_kv_heads, seq_len, d_head, dtype, plan,
                                            device=device, scoring=scoring)
         # persistent buffers: the whole forward is a fixed launch sequence
@@ -109,6 +110,12 @@ class PrefillAttentionStack:
             torch.empty((n_kv_heads, seq_len, d_head), dtype=dtype, device=device))
         self.cat = torch.empty((seq_len, Wq), dtype=dtype, device=device)
         self.k_keep = torch.zeros(n_layers, dtype=torch.int32, device=device)
+
+    def set_plan(self, plan: SparsePlan) -> None:
+        """Switch the sparsification plan (mode, tau / s, sparse layers); weights stay."""
+        self.plan = plan
+        self.attn = ShardedSparseAttention(self.H, self.Hkv, self.L, self.d, self.dtype, plan,
+                                           device=self.device, scoring=self.scoring)
 
     def layer(self, i: int, x: torch.Tensor, dense: bool = False, marks=None) -> torch.Tensor:
         """One attention branch in place on the residual stream x [L, D]."""

@@ -180,3 +180,26 @@ def test_stack_drift_calibration_selects_half(cuda):
             assert kk[i] <= L
         else:
             assert kk[i] == L
+
+
+def test_report_harness_rows(cuda):
+    """report.py: the reference's sweep / fixed-vs-dynamic rows (bench.cpp:275-314)
+    with the measured columns, in its CSV layout."""
+    import io
+    from paper_2602_03216_b200 import report
+    base = ["--n-layers", "4", "--n-heads", "8", "--n-kv-heads", "2", "--d-model", "512",
+            "--reps", "1"]
+    for cmd in (["sweep", "--seq-lens", "2048"], ["fixed-vs-dynamic", "--seq-len", "2048"]):
+        buf = io.StringIO()
+        import contextlib
+        with contextlib.redirect_stdout(buf):
+            assert report.main(cmd + base + ["--format", "csv"]) == 0
+        lines = buf.getvalue().splitlines()
+        assert lines[0].startswith("# config ") and lines[1].startswith("# reference ")
+        hdr = lines[2].split(",")
+        assert hdr[-3:] == ["ms", "dense_ms", "measured_speedup"] and "est_speedup" in hdr
+        rows = [dict(zip(hdr, l.split(","))) for l in lines[3:]]
+        assert len(rows) == (2 if cmd[0] == "sweep" else 4)
+        for r in rows:
+            assert float(r["ms"]) > 0 and float(r["est_speedup"]) >= 1.0
+            assert 1 <= float(r["avg_k_keep"]) <= 2048

@@ -242,3 +242,27 @@ def test_producer_kats(port):
     assert abs(d1 - d2) < 1e-4 * max(1.0, abs(d1))
     with pytest.raises(OracleError):
         port.apply_rope(np.zeros((1, 3), np.float32), 1e4)
+
+
+def test_report_flop_model_matches_reference(ref):
+    """paper_2602_03216_b200.report.estimate_flops restates flops.cpp:12-51: the
+    same doubles as the reference compiled here."""
+    from paper_2602_03216_b200.report import estimate_flops
+    cases = [(131072, 128, 32, [75533] * 16 + [None] * 16),
+             (4096, 16, 8, [2027, None, 1, 4096]), (256, 8, 1, [None]), (100, 4, 2, [50])]
+    for L, d, H, kk in cases:
+        for lq, ker in ((64, 7), (500, 1)):
+            a = estimate_flops(L, d, H, kk, lq, ker)
+            b = ref.estimate_flops(L, d, H, kk, lq, ker)
+            for key, v in b.items():
+                assert a[key] == v, (key, a[key], v)
+
+
+def test_drift_port_bit_exact_vs_reference(port, ref):
+    rng = RefRng(41)
+    h = np.stack([rng.random_matrix(33, 48, 1.0 + 0.2 * i) for i in range(4)])
+    a, b = port.compute_drift(h, 1e-6), ref.compute_drift(h, 1e-6)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    for delta in (0.0, 0.5, 1.0):
+        pa, pb = port.select_sparse_layers(a, delta), ref.select_sparse_layers(b, delta)
+        assert np.array_equal(pa[0], pb[0]) and pa[1] == pb[1]
