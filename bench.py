@@ -610,7 +610,10 @@ def cpu_baseline(q, k, v, layer, L, Hq, Hk, k_keep, kind="port"):
     idx = ora.select_tokens(s, k_keep, [L - 1], n_threads=T) if kind == "port" else \
         ora.select_tokens(s, k_keep, [L - 1])
     t_select = time.perf_counter() - t0
-    m = min(k_keep, 8192)
+    # compressed rows of the attention sample: the reference materialises m x m
+    # scores per head (cost ~ m^2), so its arm samples fewer rows to keep each
+    # --impl reference step near 10 s
+    m = min(k_keep, 8192 if kind == "port" else 2048)
     t0 = time.perf_counter()
     if kind == "port":
         ora.token_sparse_attention_sampled(qn, kn, vn, idx, head_stride=1, r0=0, r1=m,
