@@ -20,9 +20,16 @@ METRICS = [
 ]
 
 
+def num(v):
+    return v if isinstance(v, float) else 0.0
+
+
 def main(rep, out_json):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".csv"):  # a saved `ncu -i ... --page raw --csv` dump
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     res = {}
@@ -45,12 +52,12 @@ def main(rep, out_json):
     for k, d in res.items():
         scale = {"ms": 1, "us": 1e-3, "ns": 1e-6, "usecond": 1e-3, "msecond": 1}.get(d.get("duration_unit"), 1)
         gb = {"Gbyte": 1, "Mbyte": 1e-3, "Kbyte": 1e-6, "byte": 1e-9}
-        rd = d.get("dram_read", 0) * gb.get(d.get("dram_read_unit"), 1)
-        wr = d.get("dram_write", 0) * gb.get(d.get("dram_write_unit"), 1)
+        rd = num(d.get("dram_read", 0)) * gb.get(d.get("dram_read_unit"), 1)
+        wr = num(d.get("dram_write", 0)) * gb.get(d.get("dram_write_unit"), 1)
         d["dram_GB_per_launch"] = round(rd + wr, 4)
-        print(f"{k[:40]:40s} {d.get('duration', 0) * scale:8.3f} {rd + wr:8.3f} "
-              f"{d.get('dram_pct', 0):6.1f} {d.get('tensor_pipe_pct', 0):7.1f} "
-              f"{d.get('xu_pct', 0):5.1f} {d.get('issue_pct', 0):6.1f}")
+        print(f"{k[:40]:40s} {num(d.get('duration', 0)) * scale:8.3f} {rd + wr:8.3f} "
+              f"{num(d.get('dram_pct', 0)):6.1f} {num(d.get('tensor_pipe_pct', 0)):7.1f} "
+              f"{num(d.get('xu_pct', 0)):5.1f} {num(d.get('issue_pct', 0)):6.1f}")
     json.dump(res, open(out_json, "w"), indent=1)
 
 

@@ -10,9 +10,11 @@ from paper_2602_03216_b200 import workloads  # noqa: E402
 from paper_2602_03216_b200.dist import ShardedSparseAttention  # noqa: E402
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
-q, k, v = workloads.heavy_tailed_heads(32, 8, L, 128, seed=2602)
+H = int(sys.argv[2]) if len(sys.argv) > 2 else 32
+HKV = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+q, k, v = workloads.heavy_tailed_heads(H, HKV, L, 128, seed=2602)
 plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.01)
-lay = ShardedSparseAttention(32, 8, L, 128, torch.bfloat16, plan, device=torch.device("cuda"))
+lay = ShardedSparseAttention(H, HKV, L, 128, torch.bfloat16, plan, device=torch.device("cuda"))
 for _ in range(2):
     lay.step(q, k, v)
 torch.cuda.synchronize()
