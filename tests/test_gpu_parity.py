@@ -69,7 +69,8 @@ def test_budget_and_select_on_oracle_scores_bit_exact(cuda, port, name):
 
 @pytest.mark.parametrize("L,H,tau,seed", [(4096, 8, 0.005, 1), (4096, 8, 0.1, 2),
                                           (4096, 8, 0.5, 3), (2000, 4, 0.99, 4),
-                                          (131072, 2, 0.01, 5), (65537, 4, 0.3, 6)])
+                                          (131072, 2, 0.01, 5), (65537, 4, 0.3, 6),
+                                          (150001, 2, 0.01, 7)])  # slice > 16384: global path
 def test_budget_random_scores(cuda, port, L, H, tau, seed):
     rng = np.random.default_rng(seed)
     # heavy-tailed positive scores with ties
@@ -83,7 +84,8 @@ def test_budget_random_scores(cuda, port, L, H, tau, seed):
 
 
 @pytest.mark.parametrize("L,k,nf", [(1, 1, 1), (10, 3, 1), (4096, 1000, 1), (4096, 4096, 1),
-                                    (5000, 64, 64), (131072, 70000, 1), (3000, 1, 1)])
+                                    (5000, 64, 64), (131072, 70000, 1), (3000, 1, 1),
+                                    (150001, 80000, 1), (140000, 140000, 64)])
 def test_select_random_with_ties(cuda, port, L, k, nf):
     rng = np.random.default_rng(L + k)
     s = rng.integers(0, 50, (4, L)).astype(np.float32) / 7.0  # many exact ties
