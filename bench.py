@@ -56,6 +56,9 @@ def parse():
                    help="extra tau levels reported in tau_sweep (comma list, '' = none)")
     p.add_argument("--sigma", type=float, default=None)
     p.add_argument("--scoring", type=int, default=0, help="0 default, 1 reference-order, 2 fast")
+    p.add_argument("--c2", choices=["auto", "nccl", "peer"], default="auto",
+                   help="multi-GPU output exchange: peer-memory stores fused into the kernels "
+                        "(auto: when symmetric memory is available) or an NCCL all-gather")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-dense", action="store_true")
@@ -176,7 +179,8 @@ def run_ours(args):
     def make(tau, mode=tsa.SparseMode.kDynamic):
         plan = tsa.SparsePlan(mode=mode, sparse_layers=[0], tau=tau)
         return ShardedSparseAttention(Hq, Hk, L, D, torch.bfloat16, plan, rank=rank, world=world,
-                                      device=device, scoring=args.scoring)
+                                      device=device, scoring=args.scoring,
+                                      c2=args.c2 if world > 1 else "auto")
 
     layer = make(args.tau)
     sh = layer.shard
@@ -304,6 +308,9 @@ def run_ours(args):
                        "n_heads": Hq, "n_kv_heads": Hk, "d_head": D, "tau": args.tau,
                        "sigma": sigma, "last_q": 64, "kernel": 7, "forced": "final_token",
                        "parallelism": f"head-parallel x{world}",
+                       "c2": (layer.c2 if world > 1 else None),
+                       **({"c2_fallback": layer.c2_error} if getattr(layer, "c2_error", None)
+                          else {}),
                        "l2": "inputs (1.5 GiB) larger than L2; no flush"},
             "k_keep": k_keep, "map_sparsity": round(1 - (k_keep / L) ** 2, 4),
             "tokens_per_s": round(L / (sparse_ms * 1e-3), 1),

@@ -155,6 +155,26 @@ TSA_API int tsa_gather_zero(const tsa_desc* d, const void* k, const void* v, con
                             const int32_t* k_keep, void* kc, void* vc, const int32_t* inv,
                             void* out, void* stream);
 
+/* --- the multi-GPU boundary fused into the producers (C2 over peer memory) ---
+ * The head concat before W_O (model.cpp:197-200) needs every head's output on
+ * every rank.  Instead of an all-gather after the layer, the two kernels that
+ * write output rows (the zero rows and the attention epilogue) store each
+ * row of the shard's heads to all n_outs bases: outs[i] is an [H x L x d]
+ * buffer -- this rank's and each peer's symmetric buffer mapped into this
+ * device's address space over NVLink (CUDA IPC / torch symmetric memory) --
+ * and the rows land at the same offsets in each.  The kernels end with a
+ * system-scope fence; the caller orders the peers' reads after them with a
+ * cross-rank barrier on the stream.  1 <= n_outs <= TSA_MAX_REPLICAS. */
+#define TSA_MAX_REPLICAS 8
+TSA_API int tsa_gather_zero_replicas(const tsa_desc* d, const void* k, const void* v,
+                                     const int32_t* idx, const int32_t* k_keep, void* kc,
+                                     void* vc, const int32_t* inv, void* const* outs,
+                                     int32_t n_outs, void* stream);
+TSA_API int tsa_attend_indexed_replicas(const tsa_desc* d, const void* q, const void* kc,
+                                        const void* vc, const int32_t* idx,
+                                        const int32_t* k_keep, void* const* outs,
+                                        int32_t n_outs, void* stream);
+
 /* out[h, t] = +0.0 for every t with inv[h, t] < 0 (scatter_rows' zero rows). */
 TSA_API int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream);
 

@@ -141,7 +141,7 @@ template <uint32_t kPolyMask>
 __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32_t warp,
                                              uint32_t lane, int tA, int tB, bool hasB, int n,
                                              int q_row0, float scale_log2,
-                                             __nv_bfloat16* __restrict__ o,
+                                             const OutReplicas& o,
                                              const int32_t* __restrict__ idx_h, size_t out_head_row) {
         const int tile = warp < 4 ? 0 : 1;  // warps 0..3 -> A, 4..7 -> B
     if (tile == 0 || hasB) {
@@ -228,7 +228,7 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
         const float inv_l = 1.0f / l_run;
         size_t out_row = (size_t)q_row0 + tile * BM + row;
         if (idx_h && qi < n) out_row = out_head_row + (size_t)__ldg(idx_h + qi);
-        __nv_bfloat16* dst = o + out_row * HD;
+        const size_t out_off = out_row * HD;
 #pragma unroll
         for (int c0 = 0; c0 < HD; c0 += 32) {
             uint32_t r[32];
@@ -241,11 +241,19 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
                 for (int e = 0; e < 16; ++e)
                     ow[e] = pack_bf16x2(__uint_as_float(r[2 * e]) * inv_l,
                                         __uint_as_float(r[2 * e + 1]) * inv_l);
-                uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+                // every output replica (multi-GPU: this rank's buffer and the
+                // peers' over NVLink -- the head all-gather fused into the epilogue)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) d4[e] = outv[e];
+                for (int i = 0; i < TSA_MAX_REPLICAS; ++i) {
+                    if (i >= o.n) break;
+                    uint4* d4 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(o.p[i]) +
+                                                         out_off + c0);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) d4[e] = outv[e];
+                }
             }
         }
+        if (o.n > 1) __threadfence_system();  // peers read after a cross-rank barrier
     }
 }
 
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ n_dev,
                     int n_const, int kv_group, int rows_per_head, int kv_rows_per_head,
-                    int head_begin, float scale_log2, __nv_bfloat16* __restrict__ o,
+                    int head_begin, float scale_log2, const __grid_constant__ OutReplicas o,
                     const int32_t* __restrict__ idx) {
     extern __shared__ uint8_t smem_raw[];
     AttnSmem& sm = *reinterpret_cast<AttnSmem*>(
@@ -501,7 +509,7 @@ template <bool kIndexed, uint32_t kPolyMask>
 void run_kernel(dim3 grid, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
                 const CUtensorMap& mv, const int32_t* n_dev, int32_t n_const, int32_t kv_group,
                 int32_t rows_per_head, int32_t kv_rows_per_head, int head_begin, float scale_log2,
-                void* o, const int32_t* idx) {
+                const OutReplicas& o, const int32_t* idx) {
     const int smem = (int)sizeof(AttnSmem) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
@@ -511,13 +519,14 @@ void run_kernel(dim3 grid, cudaStream_t st, const CUtensorMap& mq, const CUtenso
     }
     attend_sm100_kernel<kIndexed, kPolyMask><<<grid, kThreads, smem, st>>>(
         mq, mk, mv, n_dev, n_const, kv_group, rows_per_head, kv_rows_per_head, head_begin,
-        scale_log2, (__nv_bfloat16*)o, idx);
+        scale_log2, o, idx);
 }
 
 template <bool kIndexed>
 int launch_impl(const tsa_desc& d, const void* q, const void* k, const void* v,
                 const int32_t* idx, const int32_t* n_dev, int32_t n_const, int32_t kv_group,
-                int32_t rows_per_head, int32_t kv_rows_per_head, void* o, cudaStream_t st) {
+                int32_t rows_per_head, int32_t kv_rows_per_head, const OutReplicas& o,
+                cudaStream_t st) {
     if (!attend_sm100_supported(d)) return invalid("attend_sm100: needs bf16, d_head 128");
     const int nh = d.head_end - d.head_begin;
     const int n_q_heads = d.n_heads;
@@ -564,13 +573,21 @@ int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const v
                         int32_t rows_per_head, int32_t kv_rows_per_head, void* o,
                         cudaStream_t st) {
     return launch_impl<false>(d, q, k, v, nullptr, n_dev, n_const, kv_group, rows_per_head,
-                              kv_rows_per_head, o, st);
+                              kv_rows_per_head, single_replica(o), st);
 }
 
 // Fused gather -> causal attention -> scatter of the selected rows (the
 // unselected rows are zeroed separately by launch_zero_unselected).
 int launch_attend_indexed(const tsa_desc& d, const void* q, const void* kc, const void* vc,
                           const int32_t* idx, const int32_t* k_keep, void* out, cudaStream_t st) {
+    const int L = d.seq_len;
+    return launch_impl<true>(d, q, kc, vc, idx, k_keep, L, 1, L, L, single_replica(out), st);
+}
+
+// The same with the output rows stored to every replica (tsa_attend_indexed_replicas).
+int launch_attend_indexed_rep(const tsa_desc& d, const void* q, const void* kc, const void* vc,
+                              const int32_t* idx, const int32_t* k_keep, const OutReplicas& out,
+                              cudaStream_t st) {
     const int L = d.seq_len;
     return launch_impl<true>(d, q, kc, vc, idx, k_keep, L, 1, L, L, out, st);
 }

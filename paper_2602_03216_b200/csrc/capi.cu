@@ -263,6 +263,40 @@ int tsa_gather_zero(const tsa_desc* d, const void* k, const void* v, const int32
     return launch_gather_zero(*d, nullptr, k, v, idx, k_keep, nullptr, kc, vc, inv, out, S(stream));
 }
 
+static int make_replicas(const char* who, void* const* outs, int32_t n_outs, OutReplicas* r) {
+    if (!outs || n_outs < 1 || n_outs > TSA_MAX_REPLICAS)
+        return invalid(std::string(who) + ": n_outs must be in [1, " +
+                       std::to_string(TSA_MAX_REPLICAS) + "], got " + std::to_string(n_outs));
+    *r = OutReplicas{};
+    for (int i = 0; i < n_outs; ++i) {
+        if (!outs[i]) return invalid(std::string(who) + ": null output replica " + std::to_string(i));
+        r->p[i] = outs[i];
+    }
+    r->n = n_outs;
+    return 0;
+}
+
+int tsa_gather_zero_replicas(const tsa_desc* d, const void* k, const void* v, const int32_t* idx,
+                             const int32_t* k_keep, void* kc, void* vc, const int32_t* inv,
+                             void* const* outs, int32_t n_outs, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!kc || !vc || !inv) return invalid("tsa_gather_zero_replicas: null buffer");
+    OutReplicas r;
+    if (int rc = make_replicas("tsa_gather_zero_replicas", outs, n_outs, &r)) return rc;
+    return launch_gather_zero_rep(*d, k, v, idx, k_keep, kc, vc, inv, r, S(stream));
+}
+
+int tsa_attend_indexed_replicas(const tsa_desc* d, const void* q, const void* kc, const void* vc,
+                                const int32_t* idx, const int32_t* k_keep, void* const* outs,
+                                int32_t n_outs, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!attend_sm100_supported(*d))
+        return invalid("tsa_attend_indexed_replicas: the fused path needs bf16 and d_head 128");
+    OutReplicas r;
+    if (int rc = make_replicas("tsa_attend_indexed_replicas", outs, n_outs, &r)) return rc;
+    return launch_attend_indexed_rep(*d, q, kc, vc, idx, k_keep, r, S(stream));
+}
+
 int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream) {
     if (int rc = check_desc(d)) return rc;
     return launch_zero_unselected(*d, inv, out, S(stream));

@@ -15,6 +15,22 @@ namespace tsa {
 
 constexpr int kNumSMs = 148;
 
+// Output replicas of the fused multi-GPU boundary: the same [H, L, d] layout
+// at up to TSA_MAX_REPLICAS bases (this rank's buffer and the peers'
+// symmetric buffers mapped over NVLink).  Kernels write every output row of
+// their shard to each base, so the head all-gather (model.cpp:197-200) costs
+// no separate pass.  n = 1 is the single-GPU case.
+struct OutReplicas {
+    void* p[TSA_MAX_REPLICAS];
+    int n;
+};
+inline OutReplicas single_replica(void* p) {
+    OutReplicas r{};
+    r.p[0] = p;
+    r.n = 1;
+    return r;
+}
+
 // Error state (thread-local, read through tsa_last_error()).
 void set_error(const std::string& msg);
 int invalid(const std::string& msg);
@@ -114,9 +130,15 @@ int launch_scatter(const tsa_desc& d, const void* oc, const int32_t* inv, void* 
                    cudaStream_t st);
 int launch_inverse(const tsa_desc& d, const int32_t* idx, const int32_t* k_keep, int32_t* inv,
                    cudaStream_t st);
+int launch_gather_zero_rep(const tsa_desc& d, const void* k, const void* v, const int32_t* idx,
+                           const int32_t* k_keep, void* kc, void* vc, const int32_t* inv,
+                           const OutReplicas& out, cudaStream_t st);
 int launch_zero_unselected(const tsa_desc& d, const int32_t* inv, void* out, cudaStream_t st);
 int launch_attend_indexed(const tsa_desc& d, const void* q, const void* k, const void* v,
                           const int32_t* idx, const int32_t* k_keep, void* out, cudaStream_t st);
+int launch_attend_indexed_rep(const tsa_desc& d, const void* q, const void* k, const void* v,
+                              const int32_t* idx, const int32_t* k_keep, const OutReplicas& out,
+                              cudaStream_t st);
 int launch_colsum_pool(const tsa_desc& d, const float* probs, float* s, cudaStream_t st);
 // producer.cu (attention-branch producer / consumer, model.cpp:81-158, 196-200)
 int launch_rms_norm(const void* x, const float* gain, int64_t rows, int cols, float eps, int dtype,

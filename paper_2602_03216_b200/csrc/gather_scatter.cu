@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
                                                      int chunks /* access units per row */,
                                                      int head_begin,
                                                      const int32_t* __restrict__ inv,
-                                                     V* __restrict__ out) {
+                                                     const OutReplicas out) {
     __shared__ int32_t rows[G_ROWS];
     __shared__ bool drop[G_ROWS];
     // block order: the `group` query heads sharing a KV head are adjacent and
@@ -49,18 +49,26 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
     (void)nrb;
     const int pad_end = min(L, (n + 127) / 128 * 128);
     const bool gather = r0 < pad_end;
-    if (!gather && !out) return;
+    if (!gather && out.n == 0) return;
     if (threadIdx.x < G_ROWS) {
         const int r = r0 + threadIdx.x;
         rows[threadIdx.x] = gather && r < n ? idx[(size_t)h * L + r] : -1;
         // fused zero-fill: output rows the selection dropped (scatter_rows'
         // zero rows, tensor_ops.cpp:107): fire-and-forget stores beside the gather
-        if (out) drop[threadIdx.x] = r < L && __ldg(inv + (size_t)h * L + r) < 0;
+        if (out.n) drop[threadIdx.x] = r < L && __ldg(inv + (size_t)h * L + r) < 0;
     }
     __syncthreads();
-    if (out) {
-        for (int e = threadIdx.x; e < G_ROWS * chunks; e += 256)
-            if (drop[e / chunks]) out[((size_t)h * L + r0) * chunks + e] = V{};
+    if (out.n) {
+        // every replica of the output (multi-GPU: this rank's and the peers'
+        // buffers over NVLink) receives the same rows
+#pragma unroll
+        for (int i = 0; i < TSA_MAX_REPLICAS; ++i) {
+            if (i >= out.n) break;
+            V* o = static_cast<V*>(out.p[i]) + ((size_t)h * L + r0) * chunks;
+            for (int e = threadIdx.x; e < G_ROWS * chunks; e += 256)
+                if (drop[e / chunks]) o[e] = V{};
+        }
+        if (out.n > 1) __threadfence_system();
     }
     if (!gather) return;
     const int total = G_ROWS * chunks;
@@ -188,7 +196,7 @@ int launch_zero_unselected(const tsa_desc& d, const int32_t* inv, void* out, cud
 template <typename V>
 static int gather_t(const tsa_desc& d, const void* q, const void* k, const void* v,
                     const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
-                    const int32_t* inv, void* out, cudaStream_t st) {
+                    const int32_t* inv, const OutReplicas& out, cudaStream_t st) {
     const int L = d.seq_len;
     const int chunks = (int)(d.d_head * elem_bytes(d.dtype) / sizeof(V));
     const int nh = d.head_end - d.head_begin;
@@ -196,19 +204,34 @@ static int gather_t(const tsa_desc& d, const void* q, const void* k, const void*
     dim3 grid((L + 63) / 64 * group, nh / group);
     gather_kernel<V><<<grid, 256, 0, st>>>((const V*)q, (const V*)k, (const V*)v, idx, k_keep,
                                            (V*)qc, (V*)kc, (V*)vc, L, d.n_heads / d.n_kv_heads,
-                                           chunks, d.head_begin, inv, (V*)out);
+                                           chunks, d.head_begin, inv, out);
     TSA_LAUNCH_CHECK("gather");
     return 0;
 }
 
-int launch_gather_zero(const tsa_desc& d, const void* q, const void* k, const void* v,
-                       const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
-                       const int32_t* inv, void* out, cudaStream_t st) {
+static int gather_dispatch(const tsa_desc& d, const void* q, const void* k, const void* v,
+                           const int32_t* idx, const int32_t* k_keep, void* qc, void* kc,
+                           void* vc, const int32_t* inv, const OutReplicas& out,
+                           cudaStream_t st) {
     switch (unit_bytes(d)) {
         case 16: return gather_t<uint4>(d, q, k, v, idx, k_keep, qc, kc, vc, inv, out, st);
         case 4: return gather_t<uint32_t>(d, q, k, v, idx, k_keep, qc, kc, vc, inv, out, st);
         default: return gather_t<uint16_t>(d, q, k, v, idx, k_keep, qc, kc, vc, inv, out, st);
     }
+}
+
+int launch_gather_zero(const tsa_desc& d, const void* q, const void* k, const void* v,
+                       const int32_t* idx, const int32_t* k_keep, void* qc, void* kc, void* vc,
+                       const int32_t* inv, void* out, cudaStream_t st) {
+    OutReplicas r{};
+    if (out) r = single_replica(out);
+    return gather_dispatch(d, q, k, v, idx, k_keep, qc, kc, vc, inv, r, st);
+}
+
+int launch_gather_zero_rep(const tsa_desc& d, const void* k, const void* v, const int32_t* idx,
+                           const int32_t* k_keep, void* kc, void* vc, const int32_t* inv,
+                           const OutReplicas& out, cudaStream_t st) {
+    return gather_dispatch(d, nullptr, k, v, idx, k_keep, nullptr, kc, vc, inv, out, st);
 }
 
 int launch_gather(const tsa_desc& d, const void* q, const void* k, const void* v,

@@ -11,9 +11,23 @@ score / select / gather / attend / scatter are local.  Two exchanges:
   C2  all-gather of the head outputs    ([H/G x L x d] per rank) -- the head
       concat before W_O (model.cpp:197-200).
 
-Collectives go through torch.distributed (NCCL on GPUs, gloo in the CPU
-tests).  The per-stage compute is a pluggable backend: ``CudaBackend`` (the
-C ABI, the product) or a test backend; the orchestration is shared.
+C1 goes through torch.distributed (NCCL on GPUs, gloo in the CPU tests).  C2
+has two forms:
+
+  ``c2="peer"``  fused into the kernels that produce output rows: the output
+                 is a symmetric [H, L, d] buffer on every rank (torch symmetric
+                 memory: CUDA IPC mappings over NVLink), and the zero-row pass
+                 and the attention epilogue store each row of this rank's heads
+                 to every rank's buffer (tsa_*_replicas), so the exchange
+                 overlaps the attention tile by tile; a device-side barrier
+                 over the signal pads ends the step (and one starts it, so no
+                 rank overwrites a buffer a peer is still reading);
+  ``c2="nccl"``  ``all_gather_into_tensor`` after the attention (the gloo
+                 tests, the unfused f32 / d != 128 path, and the fallback when
+                 symmetric memory cannot be set up).
+
+The per-stage compute is a pluggable backend: ``CudaBackend`` (the C ABI, the
+product) or a test backend; the orchestration is shared.
 """
 from __future__ import annotations
 
@@ -116,6 +130,16 @@ class CudaBackend:
                                             _ptr(k_keep), _ptr(self.kc), _ptr(self.vc),
                                             _ptr(self.inv), _ptr(out_local), _stream(self.device)))
 
+    def gather_kv_zero_replicas(self, k, v, k_keep, outs, n_outs):
+        _lib.check(self.lib.tsa_gather_zero_replicas(
+            C.byref(self.local), _ptr(k), _ptr(v), _ptr(self.idx), _ptr(k_keep), _ptr(self.kc),
+            _ptr(self.vc), _ptr(self.inv), outs, n_outs, _stream(self.device)))
+
+    def attend_indexed_replicas(self, q, k_keep, outs, n_outs):
+        _lib.check(self.lib.tsa_attend_indexed_replicas(
+            C.byref(self.local), _ptr(q), _ptr(self.kc), _ptr(self.vc), _ptr(self.idx),
+            _ptr(k_keep), outs, n_outs, _stream(self.device)))
+
     def attend_indexed(self, q, k_keep, out_local):
         _lib.check(self.lib.tsa_attend_indexed(C.byref(self.local), _ptr(q), _ptr(self.kc),
                                                _ptr(self.vc), _ptr(self.idx), _ptr(k_keep),
@@ -150,7 +174,7 @@ class ShardedSparseAttention:
     """
 
     def __init__(self, H, Hkv, L, d, dtype, plan: SparsePlan, rank=0, world=1, device=None,
-                 backend=None, gather_output=True, scoring: int = 0):
+                 backend=None, gather_output=True, scoring: int = 0, c2: str = "auto"):
         self.shard = Shard(rank, world, H, Hkv)
         self.H, self.Hkv, self.L, self.d = H, Hkv, L, d
         self.plan = plan
@@ -164,8 +188,39 @@ class ShardedSparseAttention:
         self.s_full = self.s_local if world == 1 else torch.zeros((H, L), dtype=torch.float32,
                                                                   device=device)
         self.out_local = torch.empty((sh.h_per, L, d), dtype=dtype, device=device)
-        self.out_full = self.out_local if world == 1 or not gather_output else torch.empty(
-            (H, L, d), dtype=dtype, device=device)
+        self.c2 = "nccl"
+        self._symm = None
+        if c2 not in ("auto", "nccl", "peer"):
+            raise _lib.InvalidArgument(f"dist: c2 must be auto, nccl or peer, got {c2!r}")
+        want_peer = ((world > 1 or c2 == "peer") and gather_output and c2 != "nccl"
+                     and getattr(self.backend, "fused", False)
+                     and dist.is_initialized() and dist.get_backend() == "nccl")
+        if c2 == "peer" and not want_peer:
+            raise _lib.InvalidArgument("dist: c2='peer' needs an NCCL process group, the "
+                                       "gathered output and the fused bf16 / d = 128 path")
+        if want_peer:
+            try:
+                self._setup_peer(H, L, d, dtype, device)
+            except Exception as e:  # symmetric memory unavailable: all-gather instead
+                if c2 == "peer":
+                    raise
+                self.c2_error = f"{type(e).__name__}: {e}"
+        if self.c2 != "peer":
+            self.out_full = self.out_local if world == 1 or not gather_output else torch.empty(
+                (H, L, d), dtype=dtype, device=device)
+
+    def _setup_peer(self, H, L, d, dtype, device):
+        import torch.distributed._symmetric_memory as symm_mem
+        out = symm_mem.empty((H, L, d), dtype=dtype, device=device)
+        hdl = symm_mem.rendezvous(out, dist.group.WORLD)
+        ptrs = list(hdl.buffer_ptrs)
+        if len(ptrs) != self.shard.world or len(ptrs) > _lib.TSA_MAX_REPLICAS:
+            raise RuntimeError(f"symmetric memory: {len(ptrs)} buffers for world "
+                               f"{self.shard.world}")
+        self.out_full, self._symm = out, hdl
+        self._replicas = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(*ptrs)
+        self._n_replicas = len(ptrs)
+        self.c2 = "peer"
 
     def _all_gather(self, dst, src):
         if self.shard.world == 1:
@@ -181,8 +236,9 @@ class ShardedSparseAttention:
         these input buffers: the chain never waits on the host (k_keep stays
         on the device), so the launch sequence is fixed and one graph launch
         replaces ~8 host launches and their gaps.  Single-process only (the
-        NCCL all-gathers of a sharded step run eagerly)."""
-        if self.shard.world > 1:
+        NCCL all-gathers and symmetric-memory barriers of a sharded step run
+        eagerly)."""
+        if self.shard.world > 1 or self.c2 == "peer":
             return self.step(q, k, v, dense=dense)
         key = (q.data_ptr(), k.data_ptr(), v.data_ptr(), dense)
         graphs = self.__dict__.setdefault("_graphs", {})
@@ -215,6 +271,8 @@ class ShardedSparseAttention:
             mark("allgather_out")
             return self.out_full
         mark("start")
+        if self.c2 == "peer":  # no rank writes into a buffer a peer still reads
+            self._symm.barrier(channel=0)
         b.score(q, k, self.s_local)
         mark("score")
         self._all_gather(self.s_full, self.s_local)
@@ -223,6 +281,16 @@ class ShardedSparseAttention:
         mark("budget")
         b.select(self.s_local, k_keep)
         mark("select")
+        if self.c2 == "peer":
+            # C2 fused into the producers: zero rows and attention output rows
+            # go to every rank's symmetric buffer over NVLink
+            b.gather_kv_zero_replicas(k, v, k_keep, self._replicas, self._n_replicas)
+            mark("gather_zero")
+            b.attend_indexed_replicas(q, k_keep, self._replicas, self._n_replicas)
+            mark("attend")
+            self._symm.barrier(channel=1)
+            mark("c2_barrier")
+            return self.out_full
         if getattr(b, "fused", False):
             # K/V compress + zero the dropped rows (one launch), then attend with
             # Q gathered by TMA gather4 and the output rows stored at their

@@ -82,6 +82,10 @@ def run_rank(rank, world, port, plan_kw, out_path):
                                  rank=rank, world=world, device=torch.device("cpu"), backend=be)
     out = lay.step(torch.from_numpy(q[shard.h0:shard.h1]), torch.from_numpy(k[shard.kv0:shard.kv1]),
                    torch.from_numpy(v[shard.kv0:shard.kv1]))
+    assert lay.c2 == "nccl"  # gloo: the all-gather form of C2
+    with pytest.raises(ValueError, match="c2='peer' needs an NCCL process group"):
+        ShardedSparseAttention(c["H"], c["Hkv"], c["L"], c["d"], torch.float32, plan, rank=rank,
+                               world=world, device=torch.device("cpu"), backend=be, c2="peer")
     if rank == 0:
         np.savez(out_path, out=out.numpy(), k_keep=lay.k_keep, s=lay.s_full.numpy())
     dist.barrier()
@@ -112,6 +116,14 @@ def test_two_rank_head_sharding_matches_unsharded(tmp_path, plan_kw):
     assert int(got["k_keep"]) == kk
     assert np.array_equal(got["s"].view(np.uint32), s.view(np.uint32))   # head-ordered gather
     assert np.array_equal(got["out"].view(np.uint32), ref.view(np.uint32))
+
+
+def test_c2_mode_is_validated():
+    plan = SparsePlan(sparse_layers=[0])
+    be = OracleBackend(plan, Shard(0, 1, 8, 4), 16)
+    with pytest.raises(ValueError, match="c2 must be"):
+        ShardedSparseAttention(8, 4, 16, 16, torch.float32, plan, device=torch.device("cpu"),
+                               backend=be, c2="shmem")
 
 
 def test_shard_geometry():
