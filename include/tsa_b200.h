@@ -141,16 +141,19 @@ TSA_API int tsa_scatter(const tsa_desc* d, const void* oc, const int32_t* inv, v
 
 /* Fused attend + decompress for bf16 / d = 128 (the production path of
  * tsa_sparse_attention_layer): Q rows are fetched from the original q by idx
- * with TMA gather4, K/V tiles from the compressed per-head kc/vc (tsa_gather
- * with qc = NULL), causal attention runs over the first k_keep rows, and each
- * output row is stored at its original position out[h, idx[h, r]].  Rows not
- * selected are left untouched -- pair with tsa_zero_unselected. */
-TSA_API int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* kc, const void* vc,
-                               const int32_t* idx, const int32_t* k_keep, void* out,
-                               void* stream);
+ * with TMA gather4, K/V tiles from the compressed per-head kc/vc
+ * (tsa_gather_zero), causal attention runs over the first k_keep rows, and each
+ * output row is stored at its original position out[h, idx[h, r]].  When
+ * k_keep == L the selection is the identity and the K/V tiles are read in
+ * place from k / v (the KV heads; kc / vc are not read).  Rows not selected are
+ * left untouched -- pair with tsa_gather_zero or tsa_zero_unselected. */
+TSA_API int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* k, const void* v,
+                               const void* kc, const void* vc, const int32_t* idx,
+                               const int32_t* k_keep, void* out, void* stream);
 
 /* K/V half of tsa_gather (kc, vc) and tsa_zero_unselected in one pass: the
- * two independent HBM streams of the fused path share a launch. */
+ * two independent HBM streams of the fused path share a launch.  When
+ * k_keep == L the copy is skipped (tsa_attend_indexed reads K/V in place). */
 TSA_API int tsa_gather_zero(const tsa_desc* d, const void* k, const void* v, const int32_t* idx,
                             const int32_t* k_keep, void* kc, void* vc, const int32_t* inv,
                             void* out, void* stream);
@@ -170,10 +173,10 @@ TSA_API int tsa_gather_zero_replicas(const tsa_desc* d, const void* k, const voi
                                      const int32_t* idx, const int32_t* k_keep, void* kc,
                                      void* vc, const int32_t* inv, void* const* outs,
                                      int32_t n_outs, void* stream);
-TSA_API int tsa_attend_indexed_replicas(const tsa_desc* d, const void* q, const void* kc,
-                                        const void* vc, const int32_t* idx,
-                                        const int32_t* k_keep, void* const* outs,
-                                        int32_t n_outs, void* stream);
+TSA_API int tsa_attend_indexed_replicas(const tsa_desc* d, const void* q, const void* k,
+                                        const void* v, const void* kc, const void* vc,
+                                        const int32_t* idx, const int32_t* k_keep,
+                                        void* const* outs, int32_t n_outs, void* stream);
 
 /* out[h, t] = +0.0 for every t with inv[h, t] < 0 (scatter_rows' zero rows). */
 TSA_API int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream);

@@ -94,11 +94,11 @@ def load() -> C.CDLL:
         "tsa_gather": (C.c_int, [D, P, P, P, P, P, P, P, P, P]),
         "tsa_attend": (C.c_int, [D, P, P, P, P, I, P, P]),
         "tsa_scatter": (C.c_int, [D, P, P, P, P]),
-        "tsa_attend_indexed": (C.c_int, [D, P, P, P, P, P, P, P]),
+        "tsa_attend_indexed": (C.c_int, [D, P, P, P, P, P, P, P, P, P]),
         "tsa_zero_unselected": (C.c_int, [D, P, P, P]),
         "tsa_gather_zero": (C.c_int, [D, P, P, P, P, P, P, P, P, P]),
         "tsa_gather_zero_replicas": (C.c_int, [D, P, P, P, P, P, P, P, P, I, P]),
-        "tsa_attend_indexed_replicas": (C.c_int, [D, P, P, P, P, P, P, I, P]),
+        "tsa_attend_indexed_replicas": (C.c_int, [D, P, P, P, P, P, P, P, P, I, P]),
         "tsa_scatter_rows": (C.c_int, [D, P, P, P, P, P, P]),
         "tsa_check": (C.c_int, [D, P, P]),
         "tsa_token_sparse_attention": (C.c_int, [D, P, P, P, P, P, P, P, P]),

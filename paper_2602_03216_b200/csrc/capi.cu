@@ -247,12 +247,15 @@ int tsa_scatter_rows(const tsa_desc* d, const void* oc, const int32_t* idx, cons
     return launch_scatter(*d, oc, at<int32_t>(ws, w.inv), out, S(stream));
 }
 
-int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* kc, const void* vc,
-                       const int32_t* idx, const int32_t* k_keep, void* out, void* stream) {
+int tsa_attend_indexed(const tsa_desc* d, const void* q, const void* k, const void* v,
+                       const void* kc, const void* vc, const int32_t* idx, const int32_t* k_keep,
+                       void* out, void* stream) {
     if (int rc = check_desc(d)) return rc;
     if (!attend_sm100_supported(*d))
         return invalid("tsa_attend_indexed: the fused path needs bf16 and d_head 128");
-    return launch_attend_indexed(*d, q, kc, vc, idx, k_keep, out, S(stream));
+    if (!q || !k || !v || !kc || !vc || !idx || !k_keep || !out)
+        return invalid("tsa_attend_indexed: null buffer");
+    return launch_attend_indexed(*d, q, k, v, kc, vc, idx, k_keep, out, S(stream));
 }
 
 int tsa_gather_zero(const tsa_desc* d, const void* k, const void* v, const int32_t* idx,
@@ -286,15 +289,18 @@ int tsa_gather_zero_replicas(const tsa_desc* d, const void* k, const void* v, co
     return launch_gather_zero_rep(*d, k, v, idx, k_keep, kc, vc, inv, r, S(stream));
 }
 
-int tsa_attend_indexed_replicas(const tsa_desc* d, const void* q, const void* kc, const void* vc,
-                                const int32_t* idx, const int32_t* k_keep, void* const* outs,
-                                int32_t n_outs, void* stream) {
+int tsa_attend_indexed_replicas(const tsa_desc* d, const void* q, const void* k, const void* v,
+                                const void* kc, const void* vc, const int32_t* idx,
+                                const int32_t* k_keep, void* const* outs, int32_t n_outs,
+                                void* stream) {
     if (int rc = check_desc(d)) return rc;
     if (!attend_sm100_supported(*d))
         return invalid("tsa_attend_indexed_replicas: the fused path needs bf16 and d_head 128");
+    if (!q || !k || !v || !kc || !vc || !idx || !k_keep)
+        return invalid("tsa_attend_indexed_replicas: null buffer");
     OutReplicas r;
     if (int rc = make_replicas("tsa_attend_indexed_replicas", outs, n_outs, &r)) return rc;
-    return launch_attend_indexed_rep(*d, q, kc, vc, idx, k_keep, r, S(stream));
+    return launch_attend_indexed_rep(*d, q, k, v, kc, vc, idx, k_keep, r, S(stream));
 }
 
 int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream) {
@@ -329,8 +335,8 @@ int tsa_token_sparse_attention(const tsa_desc* d, const void* q, const void* k, 
         if ((rc = launch_gather_zero(*d, q, k, v, idx, k_keep, nullptr, at<void>(ws, w.kc),
                                      at<void>(ws, w.vc), at<int32_t>(ws, w.inv), out, st)))
             return rc;
-        return launch_attend_indexed(*d, q, at<void>(ws, w.kc), at<void>(ws, w.vc), idx, k_keep,
-                                     out, st);
+        return launch_attend_indexed(*d, q, k, v, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
+                                     k_keep, out, st);
     }
     if ((rc = launch_gather(*d, q, k, v, idx, k_keep, at<void>(ws, w.qc), at<void>(ws, w.kc),
                             at<void>(ws, w.vc), st)))
@@ -371,7 +377,7 @@ static int layer_eager(const tsa_desc* d, const void* q, const void* k, const vo
             if ((rc = launch_gather_zero(*d, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
                                          at<void>(ws, w.vc), inv, out, st)))
                 return rc;
-            if ((rc = launch_attend_indexed(*d, q, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
+            if ((rc = launch_attend_indexed(*d, q, k, v, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
                                             k_keep_out, out, st)))
                 return rc;
         } else {
@@ -526,7 +532,7 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
         if ((rc = launch_gather_zero(dg, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
                                      at<void>(ws, w.vc), inv, out, st)))
             return rc;
-        if ((rc = launch_attend_indexed(dg, q, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
+        if ((rc = launch_attend_indexed(dg, q, k, v, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
                                         k_keep_out, out, st)))
             return rc;
         TSA_HCK(cudaEventRecord(p->done[gi], st));

@@ -134,11 +134,14 @@ int launch_gather_zero_rep(const tsa_desc& d, const void* k, const void* v, cons
                            const int32_t* k_keep, void* kc, void* vc, const int32_t* inv,
                            const OutReplicas& out, cudaStream_t st);
 int launch_zero_unselected(const tsa_desc& d, const int32_t* inv, void* out, cudaStream_t st);
+// k / v: the KV heads, read in place when k_keep == L (the identity selection,
+// for which launch_gather_zero skips the compressed copy); kc / vc otherwise.
 int launch_attend_indexed(const tsa_desc& d, const void* q, const void* k, const void* v,
-                          const int32_t* idx, const int32_t* k_keep, void* out, cudaStream_t st);
+                          const void* kc, const void* vc, const int32_t* idx,
+                          const int32_t* k_keep, void* out, cudaStream_t st);
 int launch_attend_indexed_rep(const tsa_desc& d, const void* q, const void* k, const void* v,
-                              const int32_t* idx, const int32_t* k_keep, const OutReplicas& out,
-                              cudaStream_t st);
+                              const void* kc, const void* vc, const int32_t* idx,
+                              const int32_t* k_keep, const OutReplicas& out, cudaStream_t st);
 int launch_colsum_pool(const tsa_desc& d, const float* probs, float* s, cudaStream_t st);
 // producer.cu (attention-branch producer / consumer, model.cpp:81-158, 196-200)
 int launch_rms_norm(const void* x, const float* gain, int64_t rows, int cols, float eps, int dtype,

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
                                                      int chunks /* access units per row */,
                                                      int head_begin,
                                                      const int32_t* __restrict__ inv,
-                                                     const OutReplicas out) {
+                                                     const OutReplicas out, int skip_identity) {
     __shared__ int32_t rows[G_ROWS];
     __shared__ bool drop[G_ROWS];
     // block order: the `group` query heads sharing a KV head are adjacent and
@@ -48,7 +48,9 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
     const int r0 = rb * G_ROWS;
     (void)nrb;
     const int pad_end = min(L, (n + 127) / 128 * 128);
-    const bool gather = r0 < pad_end;
+    // k_keep == L: the selection is the identity and the fused attention reads
+    // K/V in place (attend_sm100 in_place), so the compressed copy is skipped
+    const bool gather = r0 < pad_end && !(skip_identity && n == L);
     if (!gather && out.n == 0) return;
     if (threadIdx.x < G_ROWS) {
         const int r = r0 + threadIdx.x;
@@ -204,7 +206,8 @@ static int gather_t(const tsa_desc& d, const void* q, const void* k, const void*
     dim3 grid((L + 63) / 64 * group, nh / group);
     gather_kernel<V><<<grid, 256, 0, st>>>((const V*)q, (const V*)k, (const V*)v, idx, k_keep,
                                            (V*)qc, (V*)kc, (V*)vc, L, d.n_heads / d.n_kv_heads,
-                                           chunks, d.head_begin, inv, out);
+                                           chunks, d.head_begin, inv, out,
+                                           /*skip_identity=*/(qc == nullptr && out.n > 0) ? 1 : 0);
     TSA_LAUNCH_CHECK("gather");
     return 0;
 }

@@ -135,13 +135,14 @@ class CudaBackend:
             C.byref(self.local), _ptr(k), _ptr(v), _ptr(self.idx), _ptr(k_keep), _ptr(self.kc),
             _ptr(self.vc), _ptr(self.inv), outs, n_outs, _stream(self.device)))
 
-    def attend_indexed_replicas(self, q, k_keep, outs, n_outs):
+    def attend_indexed_replicas(self, q, k, v, k_keep, outs, n_outs):
         _lib.check(self.lib.tsa_attend_indexed_replicas(
-            C.byref(self.local), _ptr(q), _ptr(self.kc), _ptr(self.vc), _ptr(self.idx),
-            _ptr(k_keep), outs, n_outs, _stream(self.device)))
+            C.byref(self.local), _ptr(q), _ptr(k), _ptr(v), _ptr(self.kc), _ptr(self.vc),
+            _ptr(self.idx), _ptr(k_keep), outs, n_outs, _stream(self.device)))
 
-    def attend_indexed(self, q, k_keep, out_local):
-        _lib.check(self.lib.tsa_attend_indexed(C.byref(self.local), _ptr(q), _ptr(self.kc),
+    def attend_indexed(self, q, k, v, k_keep, out_local):
+        _lib.check(self.lib.tsa_attend_indexed(C.byref(self.local), _ptr(q), _ptr(k), _ptr(v),
+                                               _ptr(self.kc),
                                                _ptr(self.vc), _ptr(self.idx), _ptr(k_keep),
                                                _ptr(out_local), _stream(self.device)))
 
@@ -286,7 +287,7 @@ class ShardedSparseAttention:
             # go to every rank's symmetric buffer over NVLink
             b.gather_kv_zero_replicas(k, v, k_keep, self._replicas, self._n_replicas)
             mark("gather_zero")
-            b.attend_indexed_replicas(q, k_keep, self._replicas, self._n_replicas)
+            b.attend_indexed_replicas(q, k, v, k_keep, self._replicas, self._n_replicas)
             mark("attend")
             self._symm.barrier(channel=1)
             mark("c2_barrier")
@@ -297,7 +298,7 @@ class ShardedSparseAttention:
             # original positions
             b.gather_kv_zero(k, v, k_keep, self.out_local)
             mark("gather_zero")
-            b.attend_indexed(q, k_keep, self.out_local)
+            b.attend_indexed(q, k, v, k_keep, self.out_local)
             mark("attend")
         else:
             b.gather(q, k, v, k_keep)

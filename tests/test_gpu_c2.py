@@ -39,7 +39,7 @@ def test_replica_kernels_write_identical_rows(cuda, L, n_rep):
     outs = [torch.full_like(ref, float("nan")) for _ in range(n_rep)]
     arr = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(*[o.data_ptr() for o in outs])
     b.gather_kv_zero_replicas(k, v, b.k_keep, arr, n_rep)
-    b.attend_indexed_replicas(q, b.k_keep, arr, n_rep)
+    b.attend_indexed_replicas(q, k, v, b.k_keep, arr, n_rep)
     torch.cuda.synchronize()
     assert lay.k_keep < L
     for o in outs:  # every row written (no NaN left), identical to the single-output path
@@ -54,7 +54,7 @@ def test_replica_count_is_validated(cuda):
     arr = (C.c_void_p * _lib.TSA_MAX_REPLICAS)()
     for n in (0, _lib.TSA_MAX_REPLICAS + 1):
         with pytest.raises(_lib.InvalidArgument, match="n_outs"):
-            b.attend_indexed_replicas(q, b.k_keep, arr, n)
+            b.attend_indexed_replicas(q, k, v, b.k_keep, arr, n)
     with pytest.raises(_lib.InvalidArgument, match="null output replica"):
         b.gather_kv_zero_replicas(k, v, b.k_keep, arr, 1)
 

@@ -212,6 +212,36 @@ def test_tau0_equals_dense_bitwise(cuda):
         assert torch.equal(out, dense)
 
 
+@pytest.mark.parametrize("L", [640, 3000])
+def test_tau0_reads_kv_in_place(cuda, L):
+    """k_keep == L: the selection is the identity, the fused pair skips the
+    compressed K/V copy and the attention reads the KV heads in place -- the
+    output equals dense attention bitwise through every entry point, and the
+    compressed buffers are not read (poisoned with NaN here)."""
+    from paper_2602_03216_b200 import workloads
+    from paper_2602_03216_b200.dist import ShardedSparseAttention
+    q, k, v = workloads.heavy_tailed_heads(8, 2, L, 128, seed=31)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.0)
+    dense, _ = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), tsa.SparsePlan())
+    lay = ShardedSparseAttention(8, 2, L, 128, torch.bfloat16, plan, device=q.device)
+    lay.backend.kc.fill_(float("nan"))
+    lay.backend.vc.fill_(float("nan"))
+    o = lay.step(q, k, v)
+    torch.cuda.synchronize()
+    assert lay.k_keep == L
+    assert torch.equal(o.view(torch.int16), dense.view(torch.int16))
+    assert bool(torch.isnan(lay.backend.kc).all())  # the copy was skipped
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    hout = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+    tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan, n_groups=2)
+    torch.cuda.synchronize()
+    assert torch.equal(hout.view(torch.int16), dense.cpu().view(torch.int16))
+    # one token short of L: the compressed path again, still causal-exact
+    plan_f = tsa.SparsePlan(mode=tsa.SparseMode.kFixed, sparse_layers=[0], s_fixed=1.0 / L)
+    out_f, st_f = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), plan_f)
+    assert st_f.k_keep == L - 1
+
+
 def test_causality_bitwise(cuda):
     """test_attention.cpp:293-316: perturbing K/V after row t leaves rows <= t unchanged."""
     q, k, v = gqa_heads(RefRng(22), 4, 2, 512, 128)
