@@ -158,17 +158,24 @@ TSA_API int tsa_gather_zero(const tsa_desc* d, const void* k, const void* v, con
                             const int32_t* k_keep, void* kc, void* vc, const int32_t* inv,
                             void* out, void* stream);
 
-/* --- the multi-GPU boundary fused into the producers (C2 over peer memory) ---
- * The head concat before W_O (model.cpp:197-200) needs every head's output on
- * every rank.  Instead of an all-gather after the layer, the two kernels that
- * write output rows (the zero rows and the attention epilogue) store each
- * row of the shard's heads to all n_outs bases: outs[i] is an [H x L x d]
+/* --- the multi-GPU exchanges fused into the producers (peer memory) ---
+ * The budget sums the score rows of every head (token_coverage.cpp:55-57) and
+ * the head concat before W_O (model.cpp:197-200) needs every head's output on
+ * every rank.  Instead of all-gathers between the kernels, the kernels that
+ * write score rows (the pool pass of tsa_score) and output rows (the zero rows
+ * and the attention epilogue) store each row of the shard's heads to all
+ * n_outs bases: outs[i] is an [H x L x d]
  * buffer -- this rank's and each peer's symmetric buffer mapped into this
  * device's address space over NVLink (CUDA IPC / torch symmetric memory) --
  * and the rows land at the same offsets in each.  The kernels end with a
  * system-scope fence; the caller orders the peers' reads after them with a
  * cross-rank barrier on the stream.  1 <= n_outs <= TSA_MAX_REPLICAS. */
 #define TSA_MAX_REPLICAS 8
+/* tsa_score with each score row written to every replica: row h of the
+ * descriptor's heads lands at s_outs[i] + h * L (f32) -- the score all-gather
+ * before the budget. */
+TSA_API int tsa_score_replicas(const tsa_desc* d, const void* q, const void* k,
+                               float* const* s_outs, int32_t n_outs, void* ws, void* stream);
 TSA_API int tsa_gather_zero_replicas(const tsa_desc* d, const void* k, const void* v,
                                      const int32_t* idx, const int32_t* k_keep, void* kc,
                                      void* vc, const int32_t* inv, void* const* outs,

@@ -26,7 +26,7 @@ EXPORTS = (
     "tsa_dense_attention", "tsa_sparse_attention_layer", "tsa_rms_norm", "tsa_rope_table",
     "tsa_split_heads_rope", "tsa_heads_concat", "tsa_sparse_attention_layer_host",
     "tsa_layer_drift", "tsa_select_sparse_layers", "tsa_gather_zero_replicas",
-    "tsa_attend_indexed_replicas",
+    "tsa_attend_indexed_replicas", "tsa_score_replicas",
 )
 TSA_MAX_REPLICAS = 8
 
@@ -98,6 +98,7 @@ def load() -> C.CDLL:
         "tsa_zero_unselected": (C.c_int, [D, P, P, P]),
         "tsa_gather_zero": (C.c_int, [D, P, P, P, P, P, P, P, P, P]),
         "tsa_gather_zero_replicas": (C.c_int, [D, P, P, P, P, P, P, P, P, I, P]),
+        "tsa_score_replicas": (C.c_int, [D, P, P, P, I, P, P]),
         "tsa_attend_indexed_replicas": (C.c_int, [D, P, P, P, P, P, P, P, P, I, P]),
         "tsa_scatter_rows": (C.c_int, [D, P, P, P, P, P, P]),
         "tsa_check": (C.c_int, [D, P, P]),

@@ -363,7 +363,7 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (q_by_threads)
             load_q_rows(sm, q_raw, idx + (size_t)h * rows_per_head, tA, hasB, n,
                         (size_t)h * rows_per_head, warp, lane);
-        softmax_role<kPolyMask>(sm, tmem, warp, lane, tA, tB, hasB, n, q_row0, scale_log2, o,
+        softmax_role<kPolyMask>(sm, 0u /* TMEM base: 0, see the MMA warp */, warp, lane, tA, tB, hasB, n, q_row0, scale_log2, o,
                      kIndexed ? idx + (size_t)h * rows_per_head : nullptr,
                      (size_t)h * rows_per_head);
         tc_fence_before();

@@ -178,13 +178,30 @@ int tsa_workspace_size(const tsa_desc* d, size_t* bytes) {
     return 0;
 }
 
-int tsa_score(const tsa_desc* d, const void* q, const void* k, float* s, void* ws, void* stream) {
-    if (int rc = check_desc(d)) return rc;
+static int score_impl(const tsa_desc* d, const void* q, const void* k, const OutReplicas& s,
+                      void* ws, void* stream) {
     const Workspace w = workspace_layout(*d);
     if (scoring_mode(*d) == TSA_SCORING_FAST)
         return launch_score_fast(*d, q, k, s, at<float>(ws, w.logits), at<float>(ws, w.rowstat),
                                  S(stream));
     return launch_score_reference(*d, q, k, s, at<float>(ws, w.logits), S(stream));
+}
+
+int tsa_score(const tsa_desc* d, const void* q, const void* k, float* s, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    return score_impl(d, q, k, single_replica(s), ws, stream);
+}
+
+static int make_replicas(const char* who, void* const* outs, int32_t n_outs, OutReplicas* r);
+
+int tsa_score_replicas(const tsa_desc* d, const void* q, const void* k, float* const* s_outs,
+                       int32_t n_outs, void* ws, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    OutReplicas r;
+    if (int rc = make_replicas("tsa_score_replicas", reinterpret_cast<void* const*>(s_outs),
+                               n_outs, &r))
+        return rc;
+    return score_impl(d, q, k, r, ws, stream);
 }
 
 int tsa_budget(const tsa_desc* d, const float* s, int32_t* k_keep, void* ws, void* stream) {

@@ -104,10 +104,12 @@ inline int scoring_mode(const tsa_desc& d) {
 
 // --------------------------------------------------------------- launchers
 // score.cu
-int launch_score_reference(const tsa_desc& d, const void* q, const void* k, float* s,
+// s: the [H x L] score rows, or several replicas of them (multi-GPU, each
+// rank's buffer); rows of the descriptor's heads are written to every one.
+int launch_score_reference(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s,
                            float* logits, cudaStream_t st);
-int launch_score_fast(const tsa_desc& d, const void* q, const void* k, float* s, float* logits,
-                      float* rowstat, cudaStream_t st);
+int launch_score_fast(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s,
+                      float* logits, float* rowstat, cudaStream_t st);
 // select.cu
 int launch_budget(const tsa_desc& d, const float* s, int32_t* k_keep, float* headsum,
                   int32_t* status, int min_keep, cudaStream_t st);
@@ -142,7 +144,8 @@ int launch_attend_indexed(const tsa_desc& d, const void* q, const void* k, const
 int launch_attend_indexed_rep(const tsa_desc& d, const void* q, const void* k, const void* v,
                               const void* kc, const void* vc, const int32_t* idx,
                               const int32_t* k_keep, const OutReplicas& out, cudaStream_t st);
-int launch_colsum_pool(const tsa_desc& d, const float* probs, float* s, cudaStream_t st);
+int launch_colsum_pool(const tsa_desc& d, const float* probs, const OutReplicas& s,
+                       cudaStream_t st);
 // producer.cu (attention-branch producer / consumer, model.cpp:81-158, 196-200)
 int launch_rms_norm(const void* x, const float* gain, int64_t rows, int cols, float eps, int dtype,
                     void* out, cudaStream_t st);

@@ -154,7 +154,7 @@ constexpr int CS_T = 256;
 // P rows are read from `probs` [H x lq x L] (entries past the causal limit are
 // treated as exact zeros, as the reference's masked softmax writes them).
 __global__ void __launch_bounds__(CS_T) score_colsum_pool(const float* __restrict__ probs,
-                                                          float* __restrict__ s, int L, int lq,
+                                                          const OutReplicas s, int L, int lq,
                                                           int kernel, int head_begin) {
     extern __shared__ float col[];  // CS_T + kernel - 1
     const int h = head_begin + blockIdx.y;
@@ -182,12 +182,20 @@ __global__ void __launch_bounds__(CS_T) score_colsum_pool(const float* __restric
         const int cnt = hi - lo + 1;
         out = __fdiv_rn(eigen_segment_sum(col + (lo - t0 + half), cnt, lo), (float)cnt);
     }
-    s[(size_t)h * L + t] = out;
+    // every replica of the score rows (multi-GPU: each rank's [H x L] buffer,
+    // the score all-gather fused into the producing kernel)
+#pragma unroll
+    for (int i = 0; i < TSA_MAX_REPLICAS; ++i) {
+        if (i >= s.n) break;
+        static_cast<float*>(s.p[i])[(size_t)h * L + t] = out;
+    }
+    if (s.n > 1) __threadfence_system();
 }
 
 }  // namespace
 
-int launch_colsum_pool(const tsa_desc& d, const float* probs, float* s, cudaStream_t st) {
+int launch_colsum_pool(const tsa_desc& d, const float* probs, const OutReplicas& s,
+                       cudaStream_t st) {
     const int L = d.seq_len, lq = lq_of(d);
     const int nh = d.head_end - d.head_begin;
     dim3 grid((L + CS_T - 1) / CS_T, nh);
@@ -197,7 +205,7 @@ int launch_colsum_pool(const tsa_desc& d, const float* probs, float* s, cudaStre
     return 0;
 }
 
-int launch_score_reference(const tsa_desc& d, const void* q, const void* k, float* s,
+int launch_score_reference(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s,
                            float* logits, cudaStream_t st) {
     const int L = d.seq_len, lq = lq_of(d), D = d.d_head;
     const int nh = d.head_end - d.head_begin;

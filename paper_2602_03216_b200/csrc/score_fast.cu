@@ -333,7 +333,8 @@ bool score_fast_supported(const tsa_desc& d) {
     return d.dtype == TSA_BF16 && d.d_head == SF_HD && lq % 32 == 0 && lq <= 128;
 }
 
-int launch_score_fast(const tsa_desc& d, const void* q, const void* k, float* s, float* colraw,
+int launch_score_fast(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s,
+                      float* colraw,
                       float* partial_ws, cudaStream_t st) {
     if (!score_fast_supported(d))
         return invalid("score_tokens: FAST scoring needs bf16, d_head 128 and last_q (clamped to "

@@ -11,18 +11,20 @@ score / select / gather / attend / scatter are local.  Two exchanges:
   C2  all-gather of the head outputs    ([H/G x L x d] per rank) -- the head
       concat before W_O (model.cpp:197-200).
 
-C1 goes through torch.distributed (NCCL on GPUs, gloo in the CPU tests).  C2
-has two forms:
+The exchanges have two forms (``c2`` selects; "auto" = peer when possible):
 
-  ``c2="peer"``  fused into the kernels that produce output rows: the output
-                 is a symmetric [H, L, d] buffer on every rank (torch symmetric
-                 memory: CUDA IPC mappings over NVLink), and the zero-row pass
-                 and the attention epilogue store each row of this rank's heads
-                 to every rank's buffer (tsa_*_replicas), so the exchange
-                 overlaps the attention tile by tile; a device-side barrier
-                 over the signal pads ends the step (and one starts it, so no
+  ``c2="peer"``  both exchanges fused into the kernels that produce the rows:
+                 the scores [H, L] and the output [H, L, d] are symmetric
+                 buffers on every rank (torch symmetric memory: CUDA IPC
+                 mappings over NVLink); the pool pass of the scoring, the
+                 zero-row pass and the attention epilogue store each row of
+                 this rank's heads to every rank's buffer (tsa_*_replicas), so
+                 the output exchange overlaps the attention tile by tile;
+                 device-side barriers over the signal pads order the budget
+                 after the scores and end the step (and one starts it, so no
                  rank overwrites a buffer a peer is still reading);
-  ``c2="nccl"``  ``all_gather_into_tensor`` after the attention (the gloo
+  ``c2="nccl"``  ``all_gather_into_tensor`` after the scoring and after the
+                 attention through torch.distributed (the gloo
                  tests, the unfused f32 / d != 128 path, and the fallback when
                  symmetric memory cannot be set up).
 
@@ -97,6 +99,10 @@ class CudaBackend:
         fb = forced_begin(plan, L)
         self.forced = torch.arange(fb, L, dtype=torch.int32, device=device)
         self.lib = lib
+
+    def score_replicas(self, q, k, s_outs, n_outs):
+        _lib.check(self.lib.tsa_score_replicas(C.byref(self.local), _ptr(q), _ptr(k), s_outs,
+                                               n_outs, _ptr(self.ws), _stream(self.device)))
 
     def score(self, q, k, s_local):
         _lib.check(self.lib.tsa_score(C.byref(self.local), _ptr(q), _ptr(k), _ptr(s_local),
@@ -187,7 +193,7 @@ class ShardedSparseAttention:
         sh = self.shard
         self.s_local = torch.zeros((sh.h_per, L), dtype=torch.float32, device=device)
         self.s_full = self.s_local if world == 1 else torch.zeros((H, L), dtype=torch.float32,
-                                                                  device=device)
+                                                                  device=device)  # peer: symmetric
         self.out_local = torch.empty((sh.h_per, L, d), dtype=dtype, device=device)
         self.c2 = "nccl"
         self._symm = None
@@ -212,15 +218,23 @@ class ShardedSparseAttention:
 
     def _setup_peer(self, H, L, d, dtype, device):
         import torch.distributed._symmetric_memory as symm_mem
+        world = self.shard.world
+        if world > _lib.TSA_MAX_REPLICAS:
+            raise RuntimeError(f"peer exchange: world {world} > {_lib.TSA_MAX_REPLICAS}")
         out = symm_mem.empty((H, L, d), dtype=dtype, device=device)
         hdl = symm_mem.rendezvous(out, dist.group.WORLD)
-        ptrs = list(hdl.buffer_ptrs)
-        if len(ptrs) != self.shard.world or len(ptrs) > _lib.TSA_MAX_REPLICAS:
-            raise RuntimeError(f"symmetric memory: {len(ptrs)} buffers for world "
-                               f"{self.shard.world}")
+        s_full = symm_mem.empty((H, L), dtype=torch.float32, device=device)
+        hdl_s = symm_mem.rendezvous(s_full, dist.group.WORLD)
+        ptrs, sptrs = list(hdl.buffer_ptrs), list(hdl_s.buffer_ptrs)
+        if len(ptrs) != world or len(sptrs) != world:
+            raise RuntimeError(f"symmetric memory: {len(ptrs)} buffers for world {world}")
         self.out_full, self._symm = out, hdl
+        self.s_full, self._symm_s = s_full, hdl_s
         self._replicas = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(*ptrs)
-        self._n_replicas = len(ptrs)
+        # this rank's score rows start at row h0 of every rank's [H, L] buffer
+        off = self.shard.h0 * L * 4
+        self._s_replicas = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(*[p + off for p in sptrs])
+        self._n_replicas = world
         self.c2 = "peer"
 
     def _all_gather(self, dst, src):
@@ -272,15 +286,24 @@ class ShardedSparseAttention:
             mark("allgather_out")
             return self.out_full
         mark("start")
-        if self.c2 == "peer":  # no rank writes into a buffer a peer still reads
+        if self.c2 == "peer":
+            # no rank writes into a buffer a peer still reads; then the score
+            # rows go to every rank's [H, L] buffer from the pool kernel
             self._symm.barrier(channel=0)
-        b.score(q, k, self.s_local)
-        mark("score")
-        self._all_gather(self.s_full, self.s_local)
-        mark("allgather_scores")
+            b.score_replicas(q, k, self._s_replicas, self._n_replicas)
+            mark("score")
+            self._symm_s.barrier(channel=2)
+            mark("c1_barrier")
+            s_local = self.s_full[self.shard.h0:self.shard.h1]
+        else:
+            b.score(q, k, self.s_local)
+            mark("score")
+            self._all_gather(self.s_full, self.s_local)
+            mark("allgather_scores")
+            s_local = self.s_local
         k_keep = b.budget(self.s_full)
         mark("budget")
-        b.select(self.s_local, k_keep)
+        b.select(s_local, k_keep)
         mark("select")
         if self.c2 == "peer":
             # C2 fused into the producers: zero rows and attention output rows

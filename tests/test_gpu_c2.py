@@ -46,6 +46,28 @@ def test_replica_kernels_write_identical_rows(cuda, L, n_rep):
         assert torch.equal(o.view(torch.int16), ref.view(torch.int16))
 
 
+@pytest.mark.parametrize("scoring", [1, 2])  # REFERENCE-order and FAST (tensor-core) scoring
+def test_score_replicas_write_identical_rows(cuda, scoring):
+    from paper_2602_03216_b200 import _lib, workloads
+    from paper_2602_03216_b200.dist import ShardedSparseAttention
+    L = 2048
+    q, k, v = workloads.heavy_tailed_heads(8, 2, L, 128, seed=8)
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.02)
+    lay = ShardedSparseAttention(8, 2, L, 128, torch.bfloat16, plan, device=q.device,
+                                 scoring=scoring)
+    b = lay.backend
+    ref = torch.empty((8, L), dtype=torch.float32, device=q.device)
+    b.score(q, k, ref)
+    # replicas of a [16, L] buffer, this "rank" owning rows 8..15 (offset bases)
+    outs = [torch.full((16, L), float("nan"), device=q.device) for _ in range(3)]
+    arr = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(*[o.data_ptr() + 8 * L * 4 for o in outs])
+    b.score_replicas(q, k, arr, 3)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o[8:].view(torch.int32), ref.view(torch.int32))
+        assert bool(torch.isnan(o[:8]).all())  # other ranks' rows untouched
+
+
 def test_replica_count_is_validated(cuda):
     from paper_2602_03216_b200 import _lib
     lay, q, k, v = _layer(512, seed=3)
@@ -78,9 +100,11 @@ SCRIPT = textwrap.dedent("""
     a = ref.step(q, k, v).clone()
     for _ in range(2):
         peer.out_full.fill_(float("nan"))
+        peer.s_full.fill_(float("nan"))
         b = peer.step(q, k, v)
         torch.cuda.synchronize()
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+        assert torch.equal(peer.s_full, ref.s_full) and peer.k_keep == ref.k_keep
     dist.destroy_process_group()
     print("peer c2 ok", ref.k_keep)
 """)
