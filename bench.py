@@ -589,9 +589,9 @@ def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau):
     return {"value": round(ms, 3), "unit": "ms",
             "h2d_bytes_per_step": (nb(ql) + nb(kl) + nb(vl)) * world,
             "d2h_bytes_per_step": nb(ql) * world,
-            "api": "sparse_attention_layer_host (tsa_sparse_attention_layer_host): H2D of K/V/Q "
-                   "tails, then Q by head group, and D2H of each finished head group overlap the "
-                   "compute",
+            "api": "sparse_attention_layer_host (tsa_sparse_attention_layer_host): H2D of K and "
+                   "the Q tails, then V and Q by head group (first and last group head by head), "
+                   "and D2H of each finished chunk overlap the compute",
             "note": "per-rank head shard; world>1 runs the single-GPU layer call per rank"}
 
 

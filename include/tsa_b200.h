@@ -232,7 +232,9 @@ TSA_API int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const v
  * copied first (scoring needs them), the remaining Q rows follow in n_groups
  * head groups (0 = one per KV head) while the compute stream scores, selects
  * and compresses; the attention runs per head group as its Q rows arrive and
- * each group's output rows are copied back while the next group computes.
+ * each group's output rows are copied back while the next group computes.  The
+ * first and the last group run head by head, so the attention starts after one
+ * head's rows arrive and the final copy back is one head's rows.
  * Completion on `stream` covers every copy.  f32 / d != 128 / dense mode: one
  * copy in, the layer, one copy out. */
 TSA_API int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host,

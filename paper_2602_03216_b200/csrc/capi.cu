@@ -438,7 +438,8 @@ int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const void* k, 
 namespace {
 struct HostPipe {
     cudaStream_t in = nullptr, out = nullptr;
-    cudaEvent_t start = nullptr, kvq = nullptr, q[64] = {}, done[64] = {}, fin = nullptr;
+    cudaEvent_t start = nullptr, kvq = nullptr, q[64] = {}, done[64] = {}, vr[64] = {},
+                fin = nullptr;
 };
 HostPipe* host_pipe(int device) {
     static HostPipe pipes[16];
@@ -455,7 +456,8 @@ HostPipe* host_pipe(int device) {
             return nullptr;
         for (int g = 0; g < 64; ++g)
             if (cudaEventCreateWithFlags(&p.q[g], f) != cudaSuccess ||
-                cudaEventCreateWithFlags(&p.done[g], f) != cudaSuccess)
+                cudaEventCreateWithFlags(&p.done[g], f) != cudaSuccess ||
+                cudaEventCreateWithFlags(&p.vr[g], f) != cudaSuccess)
                 return nullptr;
         init[device] = true;
     }
@@ -514,18 +516,38 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
     TSA_HCK(cudaMemcpy2DAsync(qd + tail_off, head_bytes, qh + tail_off, head_bytes, lq * D * eb, H,
                               cudaMemcpyHostToDevice, p->in));
     TSA_HCK(cudaEventRecord(p->kvq, p->in));
-    // then, group by group, the group's V heads and the rest of its Q rows
-    const int kvpg = Hkv / G;
+    // Compute chunks: whole head groups, except the first and the last group,
+    // which run head by head -- the first attention then waits for one head's
+    // Q rows (not a group's) and the last copy back is one head's rows (not a
+    // group's): the two ends of the pipeline that the PCIe copies expose.
+    struct Chunk { int h0, h1, gi; };
+    Chunk chunks[64];
+    int nc = 0;
+    const bool split_ends = G >= 2 && hpg > 1 && (G - 2) + 2 * hpg <= 64;
     for (int gi = 0; gi < G; ++gi) {
-        const size_t h0 = (size_t)gi * hpg, kv0 = (size_t)gi * kvpg;
-        TSA_HCK(cudaMemcpyAsync(static_cast<uint8_t*>(v) + kv0 * head_bytes,
-                                static_cast<const uint8_t*>(v_host) + kv0 * head_bytes,
-                                (size_t)kvpg * head_bytes, cudaMemcpyHostToDevice, p->in));
+        if (split_ends && (gi == 0 || gi == G - 1))
+            for (int h = gi * hpg; h < (gi + 1) * hpg; ++h) chunks[nc++] = {h, h + 1, gi};
+        else
+            chunks[nc++] = {gi * hpg, (gi + 1) * hpg, gi};
+    }
+    // then, group by group, the group's V heads and the rest of its Q rows (per chunk)
+    const int kvpg = Hkv / G;
+    for (int c = 0, gi_done = -1; c < nc; ++c) {
+        const int gi = chunks[c].gi;
+        if (gi != gi_done) {
+            const size_t kv0 = (size_t)gi * kvpg;
+            TSA_HCK(cudaMemcpyAsync(static_cast<uint8_t*>(v) + kv0 * head_bytes,
+                                    static_cast<const uint8_t*>(v_host) + kv0 * head_bytes,
+                                    (size_t)kvpg * head_bytes, cudaMemcpyHostToDevice, p->in));
+            TSA_HCK(cudaEventRecord(p->vr[gi], p->in));
+            gi_done = gi;
+        }
+        const size_t h0 = chunks[c].h0, nh = chunks[c].h1 - chunks[c].h0;
         if (L > lq)
             TSA_HCK(cudaMemcpy2DAsync(qd + h0 * head_bytes, head_bytes, qh + h0 * head_bytes,
-                                      head_bytes, (L - lq) * D * eb, hpg, cudaMemcpyHostToDevice,
+                                      head_bytes, (L - lq) * D * eb, nh, cudaMemcpyHostToDevice,
                                       p->in));
-        TSA_HCK(cudaEventRecord(p->q[gi], p->in));
+        TSA_HCK(cudaEventRecord(p->q[c], p->in));
     }
     // score -> budget -> select on the compute stream
     TSA_HCK(cudaStreamWaitEvent(st, p->kvq, 0));
@@ -539,24 +561,33 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
     if ((rc = tsa_score(d, q, k, s, ws, stream))) return rc;
     if ((rc = budget_impl(*d, s, k_keep_out, ws, std::max(1, nf), st))) return rc;
     if ((rc = launch_select(*d, s, k_keep_out, nullptr, nf, fb, idx, inv, st))) return rc;
-    // per head group: compress K/V (+ zero the dropped rows), attend, and stream
-    // the group's output rows back while the next group computes
-    for (int gi = 0; gi < G; ++gi) {
-        tsa_desc dg = *d;
-        dg.head_begin = gi * hpg;
-        dg.head_end = (gi + 1) * hpg;
-        TSA_HCK(cudaStreamWaitEvent(st, p->q[gi], 0));
-        if ((rc = launch_gather_zero(dg, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
-                                     at<void>(ws, w.vc), inv, out, st)))
-            return rc;
-        if ((rc = launch_attend_indexed(dg, q, k, v, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
+    // per chunk: compress K/V of its group (+ zero the group's dropped rows) once,
+    // attend, and stream the chunk's output rows back while the next one computes
+    for (int c = 0, gi_done = -1; c < nc; ++c) {
+        const int gi = chunks[c].gi;
+        if (gi != gi_done) {
+            tsa_desc dg = *d;
+            dg.head_begin = gi * hpg;
+            dg.head_end = (gi + 1) * hpg;
+            TSA_HCK(cudaStreamWaitEvent(st, p->vr[gi], 0));
+            if ((rc = launch_gather_zero(dg, q, k, v, idx, k_keep_out, nullptr, at<void>(ws, w.kc),
+                                         at<void>(ws, w.vc), inv, out, st)))
+                return rc;
+            gi_done = gi;
+        }
+        tsa_desc dc = *d;
+        dc.head_begin = chunks[c].h0;
+        dc.head_end = chunks[c].h1;
+        TSA_HCK(cudaStreamWaitEvent(st, p->q[c], 0));
+        if ((rc = launch_attend_indexed(dc, q, k, v, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
                                         k_keep_out, out, st)))
             return rc;
-        TSA_HCK(cudaEventRecord(p->done[gi], st));
-        TSA_HCK(cudaStreamWaitEvent(p->out, p->done[gi], 0));
-        TSA_HCK(cudaMemcpyAsync(static_cast<uint8_t*>(out_host) + (size_t)dg.head_begin * head_bytes,
-                                static_cast<uint8_t*>(out) + (size_t)dg.head_begin * head_bytes,
-                                (size_t)hpg * head_bytes, cudaMemcpyDeviceToHost, p->out));
+        TSA_HCK(cudaEventRecord(p->done[c], st));
+        TSA_HCK(cudaStreamWaitEvent(p->out, p->done[c], 0));
+        TSA_HCK(cudaMemcpyAsync(static_cast<uint8_t*>(out_host) + (size_t)dc.head_begin * head_bytes,
+                                static_cast<uint8_t*>(out) + (size_t)dc.head_begin * head_bytes,
+                                (size_t)(dc.head_end - dc.head_begin) * head_bytes,
+                                cudaMemcpyDeviceToHost, p->out));
     }
     if (k_keep_host)
         TSA_HCK(cudaMemcpyAsync(k_keep_host, k_keep_out, 4, cudaMemcpyDeviceToHost, st));
