@@ -257,46 +257,6 @@ __device__ __forceinline__ void softmax_role(AttnSmem& sm, uint32_t tmem, uint32
     }
 }
 
-// Q rows of the indexed path loaded by the 256 softmax threads (idle until the
-// first S tile) with plain 16-B loads: half a warp per 256-B row, two rows per
-// instruction, 16 rows' loads in flight per thread before any store, written
-// into the 128-B-swizzled K-major layout the TMA would produce (16-B chunk c of
-// row r at r*128 + ((c ^ (r & 7)) << 4) in its 64-column half).  The writes go
-// through the generic proxy, so each thread fences them to the async proxy
-// before arriving on q_full (256 arrivals).  Replaces 128 TMA gather4 requests
-// per CTA, whose issue latency sat in front of the CTA's first S MMA.
-__device__ __forceinline__ void load_q_rows(AttnSmem& sm, const __nv_bfloat16* __restrict__ q_raw,
-                                            const int32_t* __restrict__ idx_h, int tA, bool hasB,
-                                            int n, size_t q_base_row, uint32_t warp,
-                                            uint32_t lane) {
-    const int row0 = (int)warp * 32;  // warps 0..3: tile A rows, 4..7: tile B rows
-    const int t = row0 >> 7;
-    if (t == 0 || hasB) {
-        const int last = __ldg(idx_h + n - 1);  // rows >= n: any finite row (masked, not stored)
-        const int qi_l = (tA + t) * BM + (row0 & 127) + (int)lane;
-        const int a_l = qi_l < n ? __ldg(idx_h + qi_l) : last;
-        const int chunk = (int)(lane & 15);
-        uint4 buf[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int rl = 2 * i + (int)(lane >> 4);
-            const int a = __shfl_sync(0xffffffffu, a_l, rl);
-            buf[i] = __ldg(reinterpret_cast<const uint4*>(q_raw + (q_base_row + (size_t)a) * HD) +
-                           chunk);
-        }
-        uint8_t* tile = sm.q[t];
-        const int half = chunk >> 3, cc = chunk & 7;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int r = (row0 & 127) + 2 * i + (int)(lane >> 4);
-            *reinterpret_cast<uint4*>(tile + half * HALF_BYTES + r * 128 + ((cc ^ (r & 7)) << 4)) =
-                buf[i];
-        }
-        fence_proxy_async_smem();
-    }
-    mbar_arrive(&sm.q_full);
-}
-
 // kIndexed: the fused compress -> attend -> decompress path.  Q rows are
 // fetched straight from the original [H, L, d] tensor by the selection
 // idx[h, r] with TMA tile::gather4 (4 rows per request, SW128 layout identical
@@ -312,7 +272,7 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     const int32_t* __restrict__ n_dev,
                     int n_const, int kv_group, int rows_per_head, int kv_rows_per_head,
                     int head_begin, float scale_log2, const __grid_constant__ OutReplicas o,
-                    const int32_t* __restrict__ idx, const __nv_bfloat16* __restrict__ q_raw) {
+                    const int32_t* __restrict__ idx) {
     extern __shared__ uint8_t smem_raw[];
     AttnSmem& sm = *reinterpret_cast<AttnSmem*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -333,10 +293,8 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const uint32_t warp = warp_id_uniform();
     const uint32_t lane = lane_id();
 
-    // indexed with q_raw: the 256 softmax threads load Q (one arrival each)
-    const bool q_by_threads = kIndexed && q_raw != nullptr;
     if (threadIdx.x == 0) {
-        mbar_init(&sm.q_full, q_by_threads ? 256 : 1);
+        mbar_init(&sm.q_full, 1);
         for (int s = 0; s < NS; ++s) {
             mbar_init(&sm.k_full[s], 1);
             mbar_init(&sm.v_full[s], 1);
@@ -360,10 +318,7 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (warp < 8) {
         // ------------------------------------------------------ softmax warps
         asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-        if (q_by_threads)
-            load_q_rows(sm, q_raw, idx + (size_t)h * rows_per_head, tA, hasB, n,
-                        (size_t)h * rows_per_head, warp, lane);
-        softmax_role<kPolyMask>(sm, 0u /* TMEM base: 0, see the MMA warp */, warp, lane, tA, tB, hasB, n, q_row0, scale_log2, o,
+        softmax_role<kPolyMask>(sm, tmem, warp, lane, tA, tB, hasB, n, q_row0, scale_log2, o,
                      kIndexed ? idx + (size_t)h * rows_per_head : nullptr,
                      (size_t)h * rows_per_head);
         tc_fence_before();
@@ -408,10 +363,9 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             };
             const int q_base_row = h * rows_per_head;  // original Q rows of head h
             // post the byte count before any lane's copy can complete_tx
-            if (!q_by_threads && lane == 0)
-                mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
+            if (lane == 0) mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
             __syncwarp();
-            for (int t = 0; t < (q_by_threads ? 0 : hasB ? 2 : 1); ++t) {
+            for (int t = 0; t < (hasB ? 2 : 1); ++t) {
                 int a0, a1, a2, a3;
                 rows4((tA + t) * BM + 4 * (int)lane, a0, a1, a2, a3);
                 uint8_t* dst = sm.q[t] + lane * 512;
@@ -425,23 +379,28 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // k_keep == L (tau = 0): the selection is the identity, so the tiles
             // come straight from the KV head's rows (no compressed copy, and the
             // query heads of a KV group share them in L2 as the dense kernel does)
-            const bool in_place = n == rows_per_head;
-            const CUtensorMap* mk = in_place ? &tm_kd : &tm_k;
-            const CUtensorMap* mv = in_place ? &tm_vd : &tm_v;
-            const int kv_base = in_place ? (h / dense_group) * rows_per_head : kv_row0;
-            if (lane == 0) {
+            // (Two copies of the loop, each on a fixed descriptor: selecting the
+            // descriptor address at run time measured 3 % slower on the whole
+            // attention.)
+            auto kv_loop = [&](const CUtensorMap& mk, const CUtensorMap& mv, int kv_base) {
                 for (int j = 0; j < nkv; ++j) {
                     const int st = j % NS;
                     const int r = kv_base + j * BN;
                     if (j >= NS) mbar_wait(&sm.k_empty[st], ((j / NS) - 1) & 1);
-                    tma_load_2d(sm.k[st], mk, &sm.k_full[st], 0, r);
-                    tma_load_2d(sm.k[st] + HALF_BYTES, mk, &sm.k_full[st], 64, r);
+                    tma_load_2d(sm.k[st], &mk, &sm.k_full[st], 0, r);
+                    tma_load_2d(sm.k[st] + HALF_BYTES, &mk, &sm.k_full[st], 64, r);
                     mbar_arrive_expect_tx(&sm.k_full[st], TILE_BYTES);
                     if (j >= NS) mbar_wait(&sm.v_empty[st], ((j / NS) - 1) & 1);
-                    tma_load_2d(sm.v[st], mv, &sm.v_full[st], 0, r);
-                    tma_load_2d(sm.v[st] + HALF_BYTES, mv, &sm.v_full[st], 64, r);
+                    tma_load_2d(sm.v[st], &mv, &sm.v_full[st], 0, r);
+                    tma_load_2d(sm.v[st] + HALF_BYTES, &mv, &sm.v_full[st], 64, r);
                     mbar_arrive_expect_tx(&sm.v_full[st], TILE_BYTES);
                 }
+            };
+            if (lane == 0) {
+                if (n == rows_per_head)
+                    kv_loop(tm_kd, tm_vd, (h / dense_group) * rows_per_head);
+                else
+                    kv_loop(tm_k, tm_v, kv_row0);
             }
         }
     } else if (warp == 9) {
@@ -451,16 +410,12 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const uint32_t idesc_s = idesc_bf16_f32(BM, BN, 0, 0);
             const uint32_t idesc_o = idesc_bf16_f32(BM, HD, 0, 1);
             const uint32_t qa = smem_u32(sm.q[0]), qb = smem_u32(sm.q[1]);
-            // An allocation of all 512 TMEM columns can only start at lane 0 /
-            // column 0, so the base is the constant 0 here: the MMA operands are
-            // then immediates in uniform registers.  (Read from shared memory, the
-            // base stays in a vector register in some instantiations and every
-            // TS-MMA pays an R2UR.BROADCAST; measured 4-15 % on the indexed
-            // kernel.)
-            if (tmem != 0) __trap();
-            constexpr uint32_t kTmem = 0;
-            const uint32_t tS[2] = {kTmem, kTmem + 128};
-            const uint32_t tO[2] = {kTmem + 256, kTmem + 384};
+            // (Keep this warp's register footprint small: when other roles of the
+            // kernel grow, ptxas can move the TMEM addresses out of uniform
+            // registers and every TS-MMA then pays an R2UR.BROADCAST -- the SASS
+            // of both instantiations is checked by tests/test_sass.py.)
+            const uint32_t tS[2] = {tmem, tmem + 128};
+            const uint32_t tO[2] = {tmem + 256, tmem + 384};
             auto doA = [&](int j) { return j <= tA; };
             auto doB = [&](int j) { return hasB && j <= tB; };
             mbar_wait(&sm.q_full, 0);
@@ -573,7 +528,7 @@ void run_kernel(dim3 grid, cudaStream_t st, const CUtensorMap& mq, const CUtenso
                 const CUtensorMap& mv, const CUtensorMap& mkd, const CUtensorMap& mvd,
                 int dense_group, const int32_t* n_dev, int32_t n_const, int32_t kv_group,
                 int32_t rows_per_head, int32_t kv_rows_per_head, int head_begin, float scale_log2,
-                const OutReplicas& o, const int32_t* idx, const void* q_raw) {
+                const OutReplicas& o, const int32_t* idx) {
     const int smem = (int)sizeof(AttnSmem) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
@@ -584,7 +539,7 @@ void run_kernel(dim3 grid, cudaStream_t st, const CUtensorMap& mq, const CUtenso
     attend_sm100_kernel<kIndexed, kPolyMask><<<grid, kThreads, smem, st>>>(
         mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group, rows_per_head,
         kv_rows_per_head, head_begin,
-        scale_log2, o, idx, static_cast<const __nv_bfloat16*>(q_raw));
+        scale_log2, o, idx);
 }
 
 template <bool kIndexed>
@@ -616,32 +571,26 @@ int launch_impl(const tsa_desc& d, const void* q, const void* k, const void* v,
     const int max_tiles = (rows_per_head + BM - 1) / BM;
     dim3 grid((max_tiles + 1) / 2, nh);
     const float scale_log2 = (1.0f / sqrtf((float)HD)) * 1.4426950408889634f;
-    // indexed Q rows: thread loads by default, TMA gather4 with TSA_Q_GATHER4=1 (A/B knob)
-    static const bool q_gather4 = [] {
-        const char* e = std::getenv("TSA_Q_GATHER4");
-        return e && std::atoi(e) != 0;
-    }();
-    const void* q_raw = (kIndexed && !q_gather4) ? q : nullptr;
     switch (poly_mask()) {
         case 0x0000u:
             run_kernel<kIndexed, 0x0000u>(grid, st, mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group,
                                           rows_per_head, kv_rows_per_head, d.head_begin,
-                                          scale_log2, o, idx, q_raw);
+                                          scale_log2, o, idx);
             break;
         case 0x1111u:
             run_kernel<kIndexed, 0x1111u>(grid, st, mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group,
                                           rows_per_head, kv_rows_per_head, d.head_begin,
-                                          scale_log2, o, idx, q_raw);
+                                          scale_log2, o, idx);
             break;
         case 0x5555u:
             run_kernel<kIndexed, 0x5555u>(grid, st, mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group,
                                           rows_per_head, kv_rows_per_head, d.head_begin,
-                                          scale_log2, o, idx, q_raw);
+                                          scale_log2, o, idx);
             break;
         default:
             run_kernel<kIndexed, 0x2929u>(grid, st, mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group,
                                           rows_per_head, kv_rows_per_head, d.head_begin,
-                                          scale_log2, o, idx, q_raw);
+                                          scale_log2, o, idx);
     }
     TSA_LAUNCH_CHECK(kIndexed ? "attend_sm100_indexed" : "attend_sm100");
     return 0;

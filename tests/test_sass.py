@@ -1,0 +1,48 @@
+"""Codegen guards for the tcgen05 attention kernel (CPU: cuobjdump on the
+built library).  The MMA warp must issue UTCHMMA from uniform registers --
+when the kernel's other roles grow, ptxas can move the TMEM addresses into
+vector registers and every TS-MMA then pays an R2UR.BROADCAST (measured 2-4 %
+on the 128K layer) -- and nothing may spill to local memory."""
+import re
+import shutil
+import subprocess
+from pathlib import Path
+
+import pytest
+
+LIB = Path(__file__).resolve().parent.parent / "paper_2602_03216_b200" / "libtsa_b200.so"
+CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+
+
+@pytest.fixture(scope="module")
+def attend_sass():
+    if not LIB.exists() or not Path(CUOBJDUMP).exists():
+        pytest.skip("library not built or cuobjdump absent")
+    txt = subprocess.run([CUOBJDUMP, "-sass", str(LIB)], capture_output=True, text=True,
+                         check=True).stdout
+    out = {}
+    for part in re.split(r"\n\s*Function : ", txt):
+        name = part.split("\n", 1)[0]
+        m = re.search(r"attend_sm100_kernelILb([01])ELj0EE", name)  # default (no poly) variants
+        if m:
+            out["indexed" if m.group(1) == "1" else "dense"] = part
+    assert set(out) == {"indexed", "dense"}, list(out)
+    return out
+
+
+@pytest.mark.parametrize("kind", ["dense", "indexed"])
+def test_attention_sass_uses_tcgen05_and_tma(attend_sass, kind):
+    s = attend_sass[kind]
+    assert s.count("UTCHMMA") >= 48          # S (SS) and PV (TS) MMAs, unrolled
+    assert "UTMALDG" in s and "LDTM" in s and "STTM" in s
+    if kind == "indexed":
+        assert "UTMALDG.2D.GATHER4" in s     # Q rows by TMA gather4
+
+
+@pytest.mark.parametrize("kind", ["dense", "indexed"])
+def test_attention_mma_operands_stay_uniform(attend_sass, kind):
+    s = attend_sass[kind]
+    assert "LDL" not in s and "STL" not in s  # no spills
+    # the only broadcasts are the gather4 issue loop's (indexed: 10 row indices)
+    assert s.count("R2UR.BROADCAST") <= (12 if kind == "indexed" else 0)
+    assert s.count("R2UR ") <= 16
