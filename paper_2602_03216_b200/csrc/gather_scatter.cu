@@ -23,7 +23,7 @@ namespace {
 // poison O.
 constexpr int G_ROWS = 64;
 
-template <typename V>
+template <typename V, int kChunks>  // kChunks: access units per row if fixed (d = 128 bf16: 16), else 0
 __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
                                                      const V* __restrict__ k,
                                                      const V* __restrict__ v,
@@ -31,12 +31,14 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
                                                      const int32_t* __restrict__ k_keep_p,
                                                      V* __restrict__ qc, V* __restrict__ kc,
                                                      V* __restrict__ vc, int L, int group,
-                                                     int chunks /* access units per row */,
+                                                     int chunks_rt /* access units per row */,
                                                      int head_begin,
                                                      const int32_t* __restrict__ inv,
                                                      const OutReplicas out, int skip_identity) {
     __shared__ int32_t rows[G_ROWS];
     __shared__ bool drop[G_ROWS];
+    // a compile-time row width turns the per-unit row / column split into shifts
+    const int chunks = kChunks ? kChunks : chunks_rt;
     // block order: the `group` query heads sharing a KV head are adjacent and
     // take the same 64-row block of their selections, whose token positions
     // nearly coincide -- the K/V rows they read hit L2 after the first head
@@ -204,10 +206,15 @@ static int gather_t(const tsa_desc& d, const void* q, const void* k, const void*
     const int nh = d.head_end - d.head_begin;
     const int group = d.n_heads / d.n_kv_heads;  // shards hold whole KV groups
     dim3 grid((L + 63) / 64 * group, nh / group);
-    gather_kernel<V><<<grid, 256, 0, st>>>((const V*)q, (const V*)k, (const V*)v, idx, k_keep,
-                                           (V*)qc, (V*)kc, (V*)vc, L, d.n_heads / d.n_kv_heads,
-                                           chunks, d.head_begin, inv, out,
-                                           /*skip_identity=*/(qc == nullptr && out.n > 0) ? 1 : 0);
+    const int skip = (qc == nullptr && out.n > 0) ? 1 : 0;
+    if (sizeof(V) == 16 && chunks == 16)  // d = 128 bf16 rows
+        gather_kernel<V, 16><<<grid, 256, 0, st>>>((const V*)q, (const V*)k, (const V*)v, idx,
+                                                   k_keep, (V*)qc, (V*)kc, (V*)vc, L, group,
+                                                   chunks, d.head_begin, inv, out, skip);
+    else
+        gather_kernel<V, 0><<<grid, 256, 0, st>>>((const V*)q, (const V*)k, (const V*)v, idx,
+                                                  k_keep, (V*)qc, (V*)kc, (V*)vc, L, group,
+                                                  chunks, d.head_begin, inv, out, skip);
     TSA_LAUNCH_CHECK("gather");
     return 0;
 }
