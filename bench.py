@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--heads", type=int, default=H)
     p.add_argument("--kv-heads", type=int, default=HKV)
     p.add_argument("--tau", type=float, default=0.01)
-    p.add_argument("--sweep", type=str, default="0.005,0.01",
+    p.add_argument("--sweep", type=str, default="0,0.005,0.008,0.01,0.02",
                    help="extra tau levels reported in tau_sweep (comma list, '' = none)")
     p.add_argument("--sigma", type=float, default=None)
     p.add_argument("--scoring", type=int, default=0, help="0 default, 1 reference-order, 2 fast")
