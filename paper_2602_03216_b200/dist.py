@@ -206,12 +206,24 @@ class ShardedSparseAttention:
             raise _lib.InvalidArgument("dist: c2='peer' needs an NCCL process group, the "
                                        "gathered output and the fused bf16 / d = 128 path")
         if want_peer:
+            err = None
             try:
                 self._setup_peer(H, L, d, dtype, device)
+                self._symm.barrier(channel=0)  # the device barriers work on this node
+                self._symm_s.barrier(channel=0)
+                torch.cuda.synchronize(device)
             except Exception as e:  # symmetric memory unavailable: all-gather instead
                 if c2 == "peer":
                     raise
-                self.c2_error = f"{type(e).__name__}: {e}"
+                err = f"{type(e).__name__}: {e}"
+            if world > 1:  # every rank must take the same form of the exchange
+                ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=device)
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                if not int(ok.item()) and not err:
+                    err = "symmetric memory failed on another rank"
+            if err:
+                self.c2, self._symm = "nccl", None
+                self.c2_error = err
         if self.c2 != "peer":
             self.out_full = self.out_local if world == 1 or not gather_output else torch.empty(
                 (H, L, d), dtype=dtype, device=device)
