@@ -651,6 +651,35 @@ def cpu_baseline(q, k, v, layer, L, Hq, Hk, k_keep, kind="port"):
                          "select": round(t_select, 2), "attn": round(t_attn, 2)}}
 
 
+def single_thread_sample(ora, q, k, v, L, Hq, Hk, k_keep, kind):
+    """The reference as it runs (single-threaded, README.md:51): one head's
+    full-L scoring, its selection and the first m compressed rows of its
+    attention on one thread, extrapolated to the layer (x H heads, attention
+    x (k/m)^2)."""
+    g = Hq // Hk
+    qn = q[:1].float().cpu().numpy()
+    kn, vn = k[:1].float().cpu().numpy(), v[:1].float().cpu().numpy()
+    t0 = time.perf_counter()
+    s = ora.score_tokens(qn, kn, 64, 7, n_threads=1)
+    t_score = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    idx = ora.select_tokens(s, k_keep, [L - 1])
+    t_select = time.perf_counter() - t0
+    m = min(k_keep, 2048)
+    t0 = time.perf_counter()
+    if kind == "port":
+        ora.token_sparse_attention_sampled(qn, kn, vn, idx, head_stride=1, r0=0, r1=m, n_threads=1)
+    else:
+        ora.tsa_head_prefix(qn, kn, vn, idx, 0, m)
+    t_attn = time.perf_counter() - t0
+    full_s = Hq * (t_score + t_select + t_attn * (k_keep / m) ** 2)
+    return {"value": round(full_s * 1e3, 1), "unit": "ms", "cores": 1, "kind": kind,
+            "sample": (f"1 of {Hq} heads on one thread (GQA group {g}): full-L scoring + "
+                       f"selection, first {m} compressed rows of attention; extrapolated "
+                       f"x{Hq} heads, attention x(k/{m})^2 with k={k_keep}; sample wall "
+                       f"{t_score + t_select + t_attn:.1f}s")}
+
+
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation (oracle/_ref,
     the reference sources compiled here) on the box's host cores, same metric
@@ -681,6 +710,7 @@ def run_reference(args):
             vals.append(res["value"])
     ms = float(np.median(vals))
     res["value"] = round(ms, 1)
+    single = single_thread_sample(ora, q, k, v, L, args.heads, args.kv_heads, k_keep, kind)
     line = {"metric": METRIC, "impl": "reference", "value": round(ms, 1), "unit": "ms",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 1), "higher_is_better": False, "scaling": "strong",
@@ -689,7 +719,7 @@ def run_reference(args):
             "config": {"workload": "cfg3: one attention layer, Llama-3-8B heads (32 Q / 8 KV, "
                                    "d=128), L=131072, bf16 inputs upcast to f32, dynamic tau",
                        "seq_len": L, "tau": args.tau, "sigma": sigma, "k_keep": k_keep},
-            "cpu_baseline": res,
+            "cpu_baseline": res, "cpu_baseline_single_thread": single,
             "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
