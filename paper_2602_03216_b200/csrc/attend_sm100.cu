@@ -125,11 +125,18 @@ __device__ __forceinline__ void exp_pack_row(const uint32_t (&r)[BN], uint64_t s
             ps[e & 3] = add2(ps[e & 3], x);
             pk[e] = pack_bf16x2(p0, p1);
         }
-        tmem_st16(t_s + c0 / 2, pk);
-        if (c0 == 32 || c0 == 96) {
+        // keys 0..63 are released once the next chunk's exponentials are in
+        // registers, so the wait for their TMEM stores overlaps that work
+        if (c0 == 64) {
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&p_full[c0 == 96]);
+            mbar_arrive(&p_full[0]);
+        }
+        tmem_st16(t_s + c0 / 2, pk);
+        if (c0 == 96) {
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&p_full[1]);
         }
     }
 }
@@ -268,7 +275,8 @@ template <bool kIndexed, uint32_t kPolyMask>
 __global__ void __launch_bounds__(kThreads, 1)
 attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kd,
-                    const __grid_constant__ CUtensorMap tm_vd, int dense_group,
+                    const __grid_constant__ CUtensorMap tm_vd, const __grid_constant__ CUtensorMap tm_v3,
+                    const __grid_constant__ CUtensorMap tm_vd3, int dense_group,
                     const int32_t* __restrict__ n_dev,
                     int n_const, int kv_group, int rows_per_head, int kv_rows_per_head,
                     int head_begin, float scale_log2, const __grid_constant__ OutReplicas o,
@@ -287,8 +295,8 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const bool hasB = tB < n_tiles;
     const int nkv = hasB ? tB + 1 : tA + 1;  // KV tiles 0..nkv-1
     const int kvh = h / kv_group;
-    const int q_row0 = h * rows_per_head + tA * BM;
     const int kv_row0 = kvh * kv_rows_per_head;
+    const int q_row0 = h * rows_per_head + tA * BM;
 
     const uint32_t warp = warp_id_uniform();
     const uint32_t lane = lane_id();
@@ -340,14 +348,14 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 mbar_arrive_expect_tx(&sm.q_full, hasB ? 2 * TILE_BYTES : TILE_BYTES);
                 for (int j = 0; j < nkv; ++j) {
                     const int st = j % NS;
-                    const int r = kv_row0 + j * BN;
+                    const int r = j * BN;
                     if (j >= NS) mbar_wait(&sm.k_empty[st], ((j / NS) - 1) & 1);
-                    tma_load_2d(sm.k[st], &tm_k, &sm.k_full[st], 0, r);
-                    tma_load_2d(sm.k[st] + HALF_BYTES, &tm_k, &sm.k_full[st], 64, r);
+                    tma_load_2d(sm.k[st], &tm_k, &sm.k_full[st], 0, kv_row0 + r);
+                    tma_load_2d(sm.k[st] + HALF_BYTES, &tm_k, &sm.k_full[st], 64, kv_row0 + r);
                     mbar_arrive_expect_tx(&sm.k_full[st], TILE_BYTES);
                     if (j >= NS) mbar_wait(&sm.v_empty[st], ((j / NS) - 1) & 1);
-                    tma_load_2d(sm.v[st], &tm_v, &sm.v_full[st], 0, r);
-                    tma_load_2d(sm.v[st] + HALF_BYTES, &tm_v, &sm.v_full[st], 64, r);
+                    tma_load_2d(sm.v[st], &tm_v, &sm.v_full[st], 0, kv_row0 + r);
+                    tma_load_2d(sm.v[st] + HALF_BYTES, &tm_v, &sm.v_full[st], 64, kv_row0 + r);
                     mbar_arrive_expect_tx(&sm.v_full[st], TILE_BYTES);
                 }
             }
@@ -382,25 +390,32 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // (Two copies of the loop, each on a fixed descriptor: selecting the
             // descriptor address at run time measured 3 % slower on the whole
             // attention.)
-            auto kv_loop = [&](const CUtensorMap& mk, const CUtensorMap& mv, int kv_base) {
+            auto kv_loop = [&](const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mv3,
+                               int head) {
+                const int row0 = head * rows_per_head;
                 for (int j = 0; j < nkv; ++j) {
                     const int st = j % NS;
-                    const int r = kv_base + j * BN;
+                    const int r = j * BN;
                     if (j >= NS) mbar_wait(&sm.k_empty[st], ((j / NS) - 1) & 1);
-                    tma_load_2d(sm.k[st], &mk, &sm.k_full[st], 0, r);
-                    tma_load_2d(sm.k[st] + HALF_BYTES, &mk, &sm.k_full[st], 64, r);
+                    tma_load_2d(sm.k[st], &mk, &sm.k_full[st], 0, row0 + r);
+                    tma_load_2d(sm.k[st] + HALF_BYTES, &mk, &sm.k_full[st], 64, row0 + r);
                     mbar_arrive_expect_tx(&sm.k_full[st], TILE_BYTES);
                     if (j >= NS) mbar_wait(&sm.v_empty[st], ((j / NS) - 1) & 1);
-                    tma_load_2d(sm.v[st], &mv, &sm.v_full[st], 0, r);
-                    tma_load_2d(sm.v[st] + HALF_BYTES, &mv, &sm.v_full[st], 64, r);
+                    if (r + BN <= rows_per_head) {
+                        tma_load_2d(sm.v[st], &mv, &sm.v_full[st], 0, row0 + r);
+                        tma_load_2d(sm.v[st] + HALF_BYTES, &mv, &sm.v_full[st], 64, row0 + r);
+                    } else {  // past the head's rows: zeros (3-D map)
+                        tma_load_3d(sm.v[st], &mv3, &sm.v_full[st], 0, r, head);
+                        tma_load_3d(sm.v[st] + HALF_BYTES, &mv3, &sm.v_full[st], 64, r, head);
+                    }
                     mbar_arrive_expect_tx(&sm.v_full[st], TILE_BYTES);
                 }
             };
             if (lane == 0) {
                 if (n == rows_per_head)
-                    kv_loop(tm_kd, tm_vd, (h / dense_group) * rows_per_head);
+                    kv_loop(tm_kd, tm_vd, tm_vd3, h / dense_group);
                 else
-                    kv_loop(tm_k, tm_v, kv_row0);
+                    kv_loop(tm_k, tm_v, tm_v3, kvh);
             }
         }
     } else if (warp == 9) {
@@ -508,6 +523,28 @@ int make_bf16_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t b
     return 0;
 }
 
+// 3-D map over [heads x rows x 128] bf16 with the same 64 x 128 SW128 boxes,
+// used by the indexed kernel for a head's last, partial V tile: past the
+// head's last row it reads zeros (out of bounds), never the next head's rows
+// -- which may not have arrived yet (the host-tensor pipeline copies V per
+// head group) or hold anything at all; those keys are masked, but P = 0 times
+// a NaN still poisons O.  (Only the partial tile: 3-D loads for every tile
+// measured ~1 % slower.)
+int make_bf16_map_3d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t heads) {
+    auto fn = encode_fn();
+    if (!fn) return invalid("tsa: cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {HD, rows, heads};
+    cuuint64_t strides[2] = {HD * 2, rows * HD * 2};
+    cuuint32_t box[3] = {64, 128, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return invalid("tsa: tensor map encode failed (" + std::to_string((int)r) + ")");
+    return 0;
+}
+
 bool attend_sm100_supported(const tsa_desc& d) { return d.dtype == TSA_BF16 && d.d_head == HD; }
 
 namespace {
@@ -526,7 +563,7 @@ uint32_t poly_mask() {
 template <bool kIndexed, uint32_t kPolyMask>
 void run_kernel(dim3 grid, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
                 const CUtensorMap& mv, const CUtensorMap& mkd, const CUtensorMap& mvd,
-                int dense_group, const int32_t* n_dev, int32_t n_const, int32_t kv_group,
+                const CUtensorMap& mv3, const CUtensorMap& mvd3, int dense_group, const int32_t* n_dev, int32_t n_const, int32_t kv_group,
                 int32_t rows_per_head, int32_t kv_rows_per_head, int head_begin, float scale_log2,
                 const OutReplicas& o, const int32_t* idx) {
     const int smem = (int)sizeof(AttnSmem) + 1024;
@@ -537,7 +574,7 @@ void run_kernel(dim3 grid, cudaStream_t st, const CUtensorMap& mq, const CUtenso
         attr_set = true;
     }
     attend_sm100_kernel<kIndexed, kPolyMask><<<grid, kThreads, smem, st>>>(
-        mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group, rows_per_head,
+        mq, mk, mv, mkd, mvd, mv3, mvd3, dense_group, n_dev, n_const, kv_group, rows_per_head,
         kv_rows_per_head, head_begin,
         scale_log2, o, idx);
 }
@@ -559,13 +596,18 @@ int launch_impl(const tsa_desc& d, const void* q, const void* k, const void* v,
         return rc;
     if ((rc = make_bf16_map_2d(&mk, k, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
     if ((rc = make_bf16_map_2d(&mv, v, (uint64_t)n_kv_heads_buf * kv_rows_per_head, 128))) return rc;
+    CUtensorMap mv3;  // V's last partial tile per head (zeros past the head's rows)
+    if ((rc = make_bf16_map_3d(&mv3, v, (uint64_t)kv_rows_per_head, (uint64_t)n_kv_heads_buf)))
+        return rc;
     // the KV heads in place (indexed path, k_keep == L); the compressed maps otherwise
-    CUtensorMap mkd = mk, mvd = mv;
+    CUtensorMap mkd = mk, mvd = mv, mvd3 = mv3;
     const int dense_group = d.n_heads / d.n_kv_heads;
     if (kIndexed && k_dense && v_dense) {
         if ((rc = make_bf16_map_2d(&mkd, k_dense, (uint64_t)d.n_kv_heads * rows_per_head, 128)))
             return rc;
         if ((rc = make_bf16_map_2d(&mvd, v_dense, (uint64_t)d.n_kv_heads * rows_per_head, 128)))
+            return rc;
+        if ((rc = make_bf16_map_3d(&mvd3, v_dense, (uint64_t)rows_per_head, (uint64_t)d.n_kv_heads)))
             return rc;
     }
     const int max_tiles = (rows_per_head + BM - 1) / BM;
@@ -573,22 +615,22 @@ int launch_impl(const tsa_desc& d, const void* q, const void* k, const void* v,
     const float scale_log2 = (1.0f / sqrtf((float)HD)) * 1.4426950408889634f;
     switch (poly_mask()) {
         case 0x0000u:
-            run_kernel<kIndexed, 0x0000u>(grid, st, mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group,
+            run_kernel<kIndexed, 0x0000u>(grid, st, mq, mk, mv, mkd, mvd, mv3, mvd3, dense_group, n_dev, n_const, kv_group,
                                           rows_per_head, kv_rows_per_head, d.head_begin,
                                           scale_log2, o, idx);
             break;
         case 0x1111u:
-            run_kernel<kIndexed, 0x1111u>(grid, st, mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group,
+            run_kernel<kIndexed, 0x1111u>(grid, st, mq, mk, mv, mkd, mvd, mv3, mvd3, dense_group, n_dev, n_const, kv_group,
                                           rows_per_head, kv_rows_per_head, d.head_begin,
                                           scale_log2, o, idx);
             break;
         case 0x5555u:
-            run_kernel<kIndexed, 0x5555u>(grid, st, mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group,
+            run_kernel<kIndexed, 0x5555u>(grid, st, mq, mk, mv, mkd, mvd, mv3, mvd3, dense_group, n_dev, n_const, kv_group,
                                           rows_per_head, kv_rows_per_head, d.head_begin,
                                           scale_log2, o, idx);
             break;
         default:
-            run_kernel<kIndexed, 0x2929u>(grid, st, mq, mk, mv, mkd, mvd, dense_group, n_dev, n_const, kv_group,
+            run_kernel<kIndexed, 0x2929u>(grid, st, mq, mk, mv, mkd, mvd, mv3, mvd3, dense_group, n_dev, n_const, kv_group,
                                           rows_per_head, kv_rows_per_head, d.head_begin,
                                           scale_log2, o, idx);
     }

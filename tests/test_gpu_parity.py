@@ -242,6 +242,35 @@ def test_tau0_reads_kv_in_place(cuda, L):
     assert st_f.k_keep == L - 1
 
 
+def test_kv_tiles_never_read_the_next_head(cuda):
+    """L % 128 != 0: the last K/V tile of a head runs past its rows.  Those keys
+    are masked, but P = 0 times a NaN would still poison O, so in the indexed
+    (production) kernel the V tile reads zeros there, not the next KV head's
+    rows -- the host-tensor pipeline copies V per head group, so the next
+    head's rows may not have arrived yet.  NaN in KV head 1 must leave the
+    outputs of KV head 0's query heads bitwise unchanged on the in-place
+    (k_keep = L) path.  (The dense baseline kernel reads the next head's rows
+    there -- the caller's finite data, masked.)"""
+    from paper_2602_03216_b200 import workloads
+    from paper_2602_03216_b200.dist import ShardedSparseAttention
+    L = 3000
+    q, k, v = workloads.heavy_tailed_heads(8, 2, L, 128, seed=33)
+    v_nan = v.clone()
+    v_nan[1, :72] = float("nan")
+    k_nan = k.clone()
+    k_nan[1, :72] = float("nan")
+    clean, _ = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), tsa.SparsePlan())
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.0)
+    lay = ShardedSparseAttention(8, 2, L, 128, torch.bfloat16, plan, device=q.device)
+    b = lay.backend
+    lay.step(q, k, v)  # identity selection
+    assert lay.k_keep == L
+    out = torch.empty_like(q)
+    b.attend_indexed(q, k_nan, v_nan, b.k_keep, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:4].view(torch.int16), clean[:4].view(torch.int16))
+
+
 def test_causality_bitwise(cuda):
     """test_attention.cpp:293-316: perturbing K/V after row t leaves rows <= t unchanged."""
     q, k, v = gqa_heads(RefRng(22), 4, 2, 512, 128)

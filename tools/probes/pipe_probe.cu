@@ -59,6 +59,23 @@ __device__ __forceinline__ void op_add2(float& x0, float& x1) {
     x1 = __uint_as_float((uint32_t)(r >> 32));
 }
 
+// packed exponentials: two results per lane per instruction
+__device__ __forceinline__ float op_ex2_h2(float x) {
+    uint32_t y;
+    asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(__float_as_uint(x)));
+    return __uint_as_float(y);
+}
+__device__ __forceinline__ float op_ex2_bf2(float x) {
+    uint32_t y;
+    asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(__float_as_uint(x)));
+    return __uint_as_float(y);
+}
+__device__ __forceinline__ float op_cvt_h2(float x, float y) {
+    uint32_t r;
+    asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x), "f"(y));
+    return __uint_as_float(r);
+}
+
 template <int OP>
 __global__ void probe(float* out, long long* cyc, float seed) {
     float x[CH];
@@ -84,6 +101,10 @@ __global__ void probe(float* out, long long* cyc, float seed) {
             if (OP == 12) { x[i] = op_ex2(x[i]); x[i] = op_max3(x[i], x[(i + 3) % CH], x[(i + 5) % CH]); }
             if (OP == 13) { x[i] = op_cvt(x[i], x[(i + 1) % CH]); if ((i & 1) == 0) op_fma2(x[i], x[i + 1]); }
             if (OP == 14) { x[i] = op_ex2(x[i]); x[i] = op_imad(x[i]); }
+            if (OP == 20) x[i] = op_ex2_h2(x[i]);
+            if (OP == 21) x[i] = op_ex2_bf2(x[i]);
+            if (OP == 22) x[i] = op_cvt_h2(x[i], x[(i + 1) % CH]);
+            if (OP == 23) { x[i] = op_cvt_h2(x[i], x[(i + 1) % CH]); x[i] = op_ex2_h2(x[i]); }
         }
     }
     long long t1 = clock64();
@@ -129,6 +150,10 @@ int main() {
         run<12>("ex2 + max3 (2)", 2, out, cyc, th);
         run<13>("cvt + fma2 (1.5)", 1.5, out, cyc, th);
         run<14>("ex2 + imad (2)", 2, out, cyc, th);
+        run<20>("ex2.approx.f16x2", 1, out, cyc, th);
+        run<21>("ex2.approx.ftz.bf16x2", 1, out, cyc, th);
+        run<22>("cvt.rn.f16x2.f32", 1, out, cyc, th);
+        run<23>("cvt f16x2 + ex2 f16x2", 2, out, cyc, th);
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
