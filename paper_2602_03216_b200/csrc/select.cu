@@ -175,13 +175,15 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
                     }
                     __syncthreads();
                 }
-                if (tid == 0)
-                    for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(&s_total, r) = acc;
+                if (tid == 0) s_total = acc;
             }
             if (kStaged)
                 for (int t = t_begin + tid; t < t_end; t += BB) staged[t - t_begin] = headsum[t];
+            // (rank 0 publishes locally; the others read it through DSMEM after the
+            // barrier -- no remote write may precede the first cluster barrier,
+            // when a peer CTA may not have started yet)
             cluster.sync();
-            total = s_total;
+            total = *cluster.map_shared_rank(&s_total, 0);
         } else {
             // deterministic parallel f64 reduction (FAST scoring mode): fixed
             // per-CTA partials combined in rank order by every CTA
