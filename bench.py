@@ -280,8 +280,18 @@ def run_ours(args):
             ("scatter", sh.h_per * (k_keep + L) * D * b + 4 * sh.h_per * L)):
         if stages.get(name):
             gbs = nbytes / (stages[name] * 1e-3) / 1e9
-            hbm_rows[name] = {"ms": round(stages[name], 4), "GB/s": round(gbs, 1),
-                              "frac": round(gbs / hbm, 4)}
+            row = {"ms": round(stages[name], 4), "algorithmic_GB/s": round(gbs, 1)}
+            # the algorithmic bytes read every K/V row once per QUERY head (the
+            # reference gathers per query head); the g heads of a KV group hit L2,
+            # so the roofline fraction uses the kernel's DRAM bytes (ncu,
+            # profiles/traffic.json, same 128K layer) over the in-step time
+            dram = profile_traffic(name) if (L == 131072 and sh.h_per == 32) else None
+            if dram:
+                row.update({"dram_bytes": dram, "GB/s": round(dram / (stages[name] * 1e-3) / 1e9, 1),
+                            "frac": round(dram / (stages[name] * 1e-3) / 1e9 / hbm, 4)})
+            else:
+                row.update({"GB/s": round(gbs, 1), "frac": round(gbs / hbm, 4)})
+            hbm_rows[name] = row
 
     extras = {}
     for name in [x.strip() for x in args.extra.split(",") if x.strip()]:
