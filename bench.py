@@ -479,7 +479,7 @@ def run_cfg1(args, tsa, rank, world, device):
     o_gpu, st = tsa.sparse_attention_layer(heads, plan)
     res = {"workload": "cfg1: one attention layer, Llama-3-8B heads (32 Q / 8 KV, d=128), "
                        "L=4096, fp32 uniform inputs, tau=0.5", "gpu_ms": round(gpu_ms, 3),
-           "k_keep": st.k_keep, "dtype": "f32 (REFERENCE-order scoring, SIMT f32 attention)"}
+           "k_keep": st.k_keep, "dtype": "f32 (REFERENCE-order scoring, register-tiled f32 attention on the CUDA cores)"}
     if not args.no_cpu_baseline:
         ora = Oracle("port")
         T = n_threads_default()

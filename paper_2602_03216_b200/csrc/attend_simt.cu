@@ -9,6 +9,8 @@
 //
 // Block = 32 query rows x 4 threads per row; a thread owns the 16-B chunks
 // c = part, part+4, ... of its row (conflict-free shared-memory reads).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace tsa {
@@ -142,6 +144,202 @@ __global__ void __launch_bounds__(128) attend_simt_kernel(const T* __restrict__ 
     }
 }
 
+// f32 inputs, d = 128 (cfg1): register-tiled flash attention on the CUDA
+// cores.  Block = 64 query rows x 32-key tiles, 128 threads; thread t owns
+// rows 4*(t/8) .. +3 and, for S = Q K^T, keys 4*(t%8) .. +3 (a 4 x 4 tile:
+// one float4 of Q and one of K per dim feed 16 FMAs), for O += P V the float4
+// column chunks (t%8) + 8c, c < 4 (64 accumulators; the 8 threads of a row
+// group read 128 contiguous bytes of V -- conflict-free).  Q and K sit in
+// shared memory transposed ([d][row], [d][key]) so those reads are single
+// float4s; P goes through shared memory transposed ([key][row]).  Row max /
+// sum over a key tile: shuffles among the 8 threads of the row group.  Exact
+// f32 online softmax (expf), fma accumulation: within the reference's 1e-5
+// gate (bench.cpp:27) of its non-fused order.
+constexpr int TR = 64, TK = 32, TD = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(128) attend_tiled_d128(const T* __restrict__ q,
+                                                         const T* __restrict__ k,
+                                                         const T* __restrict__ v,
+                                                         const int32_t* __restrict__ n_dev,
+                                                         int n_const, int kv_group,
+                                                         int rows_per_head, int kv_rows_per_head,
+                                                         int head_begin, float scale,
+                                                         T* __restrict__ o) {
+    extern __shared__ float4 smem4[];
+    float* Qs = reinterpret_cast<float*>(smem4);  // [TD][TR]
+    float* Ks = Qs + TD * TR;                     // [TD][TK]
+    float* Vs = Ks + TD * TK;                     // [TK][TD]
+    float* Ps = Vs + TK * TD;                     // [TK][TR]
+    const int tid = threadIdx.x;
+    const int h = head_begin + blockIdx.y;
+    const int n = n_dev ? *n_dev : n_const;
+    const int n_tiles = (n + TR - 1) / TR;
+    if ((int)blockIdx.x >= n_tiles) return;
+    const int r0 = (n_tiles - 1 - (int)blockIdx.x) * TR;  // heaviest first
+    const int kvh = h / kv_group;
+    const T* qh = q + (size_t)h * rows_per_head * TD;
+    const T* kh = k + (size_t)kvh * kv_rows_per_head * TD;
+    const T* vh = v + (size_t)kvh * kv_rows_per_head * TD;
+    const int rg = tid >> 3, cg = tid & 7;  // row group (4 rows), key / column group
+
+    // Q tile, transposed: thread -> (row = e % 64, dim chunk = e / 64)
+    for (int e = tid; e < TR * (TD / 4); e += 128) {
+        const int r = e % TR, c4 = e / TR;
+        float x[4] = {0.f, 0.f, 0.f, 0.f};
+        if (r0 + r < n) {
+            const T* src = qh + (size_t)(r0 + r) * TD + c4 * 4;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = Elem<T>::to_f32(src[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) Qs[(c4 * 4 + u) * TR + r] = x[u];
+    }
+    float acc[4][16];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[r][c] = 0.f;
+    float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, l[4] = {0.f, 0.f, 0.f, 0.f};
+    const int last_key = min(n, r0 + TR) - 1;
+    for (int j0 = 0; j0 <= last_key; j0 += TK) {
+        __syncthreads();  // previous tile's K/V/P reads done (and Q stored)
+        for (int e = tid; e < TK * (TD / 4); e += 128) {
+            const int key = e % TK, c4 = e / TK;  // K transposed: a warp covers 32 keys
+            float x[4] = {0.f, 0.f, 0.f, 0.f};
+            if (j0 + key <= last_key) {
+                const T* src = kh + (size_t)(j0 + key) * TD + c4 * 4;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[u] = Elem<T>::to_f32(src[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) Ks[(c4 * 4 + u) * TK + key] = x[u];
+        }
+        for (int e = tid; e < TK * (TD / 4); e += 128) {
+            const int key = e / (TD / 4), c4 = e % (TD / 4);
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (j0 + key <= last_key) {
+                const T* src = vh + (size_t)(j0 + key) * TD + c4 * 4;
+                x = make_float4(Elem<T>::to_f32(src[0]), Elem<T>::to_f32(src[1]),
+                                Elem<T>::to_f32(src[2]), Elem<T>::to_f32(src[3]));
+            }
+            reinterpret_cast<float4*>(Vs)[key * (TD / 4) + c4] = x;
+        }
+        __syncthreads();
+        // S tile 4 x 4
+        float sc[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sc[r][c] = 0.f;
+#pragma unroll 8
+        for (int d = 0; d < TD; ++d) {
+            const float4 qa = reinterpret_cast<const float4*>(Qs + d * TR)[rg];
+            const float4 kb = reinterpret_cast<const float4*>(Ks + d * TK)[cg];
+            const float qv[4] = {qa.x, qa.y, qa.z, qa.w}, kv[4] = {kb.x, kb.y, kb.z, kb.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) sc[r][c] = fmaf(qv[r], kv[c], sc[r][c]);
+        }
+        float corr[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = r0 + rg * 4 + r;
+            float tmax = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int key = j0 + cg * 4 + c;
+                sc[r][c] = (key <= i && key <= last_key) ? sc[r][c] * scale : -INFINITY;
+                tmax = fmaxf(tmax, sc[r][c]);
+            }
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+            const float m_new = fmaxf(m[r], tmax);
+            float psum = 0.f;
+            if (m_new == -INFINITY) {  // no key visible yet (rows >= n)
+                corr[r] = 1.f;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) sc[r][c] = 0.f;
+            } else {
+                corr[r] = expf(m[r] - m_new);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    sc[r][c] = expf(sc[r][c] - m_new);
+                    psum += sc[r][c];
+                }
+            }
+            psum += __shfl_xor_sync(0xffffffffu, psum, 1);
+            psum += __shfl_xor_sync(0xffffffffu, psum, 2);
+            psum += __shfl_xor_sync(0xffffffffu, psum, 4);
+            l[r] = l[r] * corr[r] + psum;
+            m[r] = m_new;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            reinterpret_cast<float4*>(Ps + (cg * 4 + c) * TR)[rg] =
+                make_float4(sc[0][c], sc[1][c], sc[2][c], sc[3][c]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[r][c] *= corr[r];
+        __syncthreads();
+        // O += P V over the tile's keys
+#pragma unroll 4
+        for (int j = 0; j < TK; ++j) {
+            const float4 pa = reinterpret_cast<const float4*>(Ps + j * TR)[rg];
+            const float pv[4] = {pa.x, pa.y, pa.z, pa.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float4 vb = reinterpret_cast<const float4*>(Vs + j * TD)[cg + 8 * c];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    acc[r][c * 4 + 0] = fmaf(pv[r], vb.x, acc[r][c * 4 + 0]);
+                    acc[r][c * 4 + 1] = fmaf(pv[r], vb.y, acc[r][c * 4 + 1]);
+                    acc[r][c * 4 + 2] = fmaf(pv[r], vb.z, acc[r][c * 4 + 2]);
+                    acc[r][c * 4 + 3] = fmaf(pv[r], vb.w, acc[r][c * 4 + 3]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int i = r0 + rg * 4 + r;
+        if (i >= n) continue;
+        const float inv_l = 1.0f / l[r];
+        T* dst = o + ((size_t)h * rows_per_head + i) * TD;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int col = (cg + 8 * c) * 4;
+            dst[col + 0] = Elem<T>::from_f32(acc[r][c * 4 + 0] * inv_l);
+            dst[col + 1] = Elem<T>::from_f32(acc[r][c * 4 + 1] * inv_l);
+            dst[col + 2] = Elem<T>::from_f32(acc[r][c * 4 + 2] * inv_l);
+            dst[col + 3] = Elem<T>::from_f32(acc[r][c * 4 + 3] * inv_l);
+        }
+    }
+}
+
+int launch_tiled_d128_f32(const tsa_desc& d, const void* q, const void* k, const void* v,
+                          const int32_t* n_dev, int n_const, int kv_group, int rph, int kvrph,
+                          void* o, cudaStream_t st) {
+    const int nh = d.head_end - d.head_begin;
+    dim3 grid((d.seq_len + TR - 1) / TR, nh);
+    const int smem = (TD * TR + TD * TK + TK * TD + TK * TR) * (int)sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(attend_tiled_d128<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem);
+        attr = true;
+    }
+    attend_tiled_d128<float><<<grid, 128, smem, st>>>((const float*)q, (const float*)k,
+                                                      (const float*)v, n_dev, n_const, kv_group,
+                                                      rph, kvrph, d.head_begin,
+                                                      1.0f / sqrtf((float)TD), (float*)o);
+    TSA_LAUNCH_CHECK("attend_tiled_d128");
+    return 0;
+}
+
 // Any other head size (the reference's unit tests use d = 1 and 4): one
 // thread per query row, per-key online softmax, K/V straight from global.
 template <typename T>
@@ -210,7 +408,11 @@ int dispatch_d(const tsa_desc& d, const void* q, const void* k, const void* v,
         case 16: return launch_t<T, 16>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
         case 32: return launch_t<T, 32>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
         case 64: return launch_t<T, 64>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
-        case 128: return launch_t<T, 128>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+        case 128:
+            if (sizeof(T) == 4 && !std::getenv("TSA_SIMT_ROWWISE"))  // f32: register-tiled
+                return launch_tiled_d128_f32(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph,
+                                             o, st);
+            return launch_t<T, 128>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
         case 256: return launch_t<T, 256>(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
         default: {
             if (d.d_head < 1 || d.d_head > 256)
