@@ -166,11 +166,12 @@ __global__ void __launch_bounds__(128) attend_tiled_d128(const T* __restrict__ q
                                                          int rows_per_head, int kv_rows_per_head,
                                                          int head_begin, float scale,
                                                          T* __restrict__ o) {
+    static_assert(sizeof(T) == 4, "cp.async K/V staging copies f32 elements");
     extern __shared__ float4 smem4[];
     float* Qs = reinterpret_cast<float*>(smem4);  // [TD][TR]
-    float* Ks = Qs + TD * TR;                     // [TD][TK]
-    float* Vs = Ks + TD * TK;                     // [TK][TD]
-    float* Ps = Vs + TK * TD;                     // [TK][TR]
+    float* Kb = Qs + TD * TR;                     // 2 x [TD][TK]
+    float* Vb = Kb + 2 * TD * TK;                 // 2 x [TK][TD]
+    float* Ps = Vb + 2 * TK * TD;                 // [TK][TR]
     const int tid = threadIdx.x;
     const int h = head_begin + blockIdx.y;
     const int n = n_dev ? *n_dev : n_const;
@@ -202,30 +203,37 @@ __global__ void __launch_bounds__(128) attend_tiled_d128(const T* __restrict__ q
         for (int c = 0; c < 16; ++c) acc[r][c] = 0.f;
     float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, l[4] = {0.f, 0.f, 0.f, 0.f};
     const int last_key = min(n, r0 + TR) - 1;
-    for (int j0 = 0; j0 <= last_key; j0 += TK) {
-        __syncthreads();  // previous tile's K/V/P reads done (and Q stored)
-        for (int e = tid; e < TK * (TD / 4); e += 128) {
-            const int key = e % TK, c4 = e / TK;  // K transposed: a warp covers 32 keys
-            float x[4] = {0.f, 0.f, 0.f, 0.f};
-            if (j0 + key <= last_key) {
-                const T* src = kh + (size_t)(j0 + key) * TD + c4 * 4;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) x[u] = Elem<T>::to_f32(src[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) Ks[(c4 * 4 + u) * TK + key] = x[u];
+    // K (transposed, 4-byte copies) and V (16-byte copies) of key tile j0 into
+    // buffer b with cp.async, zero-filled past last_key: the next tile's loads
+    // are in flight while the current one computes
+    auto prefetch = [&](int j0, int b) {
+        float* Ks = Kb + b * TD * TK;
+        float* Vs = Vb + b * TK * TD;
+        for (int e = tid; e < TK * TD; e += 128) {
+            const int key = e % TK, dd = e / TK;  // a warp covers 32 keys of one dim
+            const bool ok = j0 + key <= last_key;
+            const T* src = kh + (size_t)(ok ? j0 + key : 0) * TD + dd;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(Ks + dd * TK + key)),
+                         "l"(src), "r"(ok ? 4 : 0));
         }
         for (int e = tid; e < TK * (TD / 4); e += 128) {
             const int key = e / (TD / 4), c4 = e % (TD / 4);
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (j0 + key <= last_key) {
-                const T* src = vh + (size_t)(j0 + key) * TD + c4 * 4;
-                x = make_float4(Elem<T>::to_f32(src[0]), Elem<T>::to_f32(src[1]),
-                                Elem<T>::to_f32(src[2]), Elem<T>::to_f32(src[3]));
-            }
-            reinterpret_cast<float4*>(Vs)[key * (TD / 4) + c4] = x;
+            const bool ok = j0 + key <= last_key;
+            const T* src = vh + (size_t)(ok ? j0 + key : 0) * TD + c4 * 4;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(Vs + key * TD + c4 * 4)),
+                         "l"(src), "r"(ok ? 16 : 0));
         }
-        __syncthreads();
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    prefetch(0, 0);
+    for (int j0 = 0, b = 0; j0 <= last_key; j0 += TK, b ^= 1) {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();  // tile j0 landed for every thread; tile j0 - TK fully consumed
+        if (j0 + TK <= last_key) prefetch(j0 + TK, b ^ 1);
+        const float* Ks = Kb + b * TD * TK;
+        const float* Vs = Vb + b * TK * TD;
         // S tile 4 x 4
         float sc[4][4];
 #pragma unroll
@@ -325,7 +333,7 @@ int launch_tiled_d128_f32(const tsa_desc& d, const void* q, const void* k, const
                           void* o, cudaStream_t st) {
     const int nh = d.head_end - d.head_begin;
     dim3 grid((d.seq_len + TR - 1) / TR, nh);
-    const int smem = (TD * TR + TD * TK + TK * TD + TK * TR) * (int)sizeof(float);
+    const int smem = (TD * TR + 2 * TD * TK + 2 * TK * TD + TK * TR) * (int)sizeof(float);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(attend_tiled_d128<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
