@@ -165,8 +165,8 @@ TSA_API int tsa_gather_zero(const tsa_desc* d, const void* k, const void* v, con
  * write score rows (the pool pass of tsa_score) and output rows (the zero rows
  * and the attention epilogue) store each row of the shard's heads to all
  * n_outs bases: outs[i] is an [H x L x d]
- * buffer -- this rank's and each peer's symmetric buffer mapped into this
- * device's address space over NVLink (CUDA IPC / torch symmetric memory) --
+ * buffer -- this rank's and each peer's buffer mapped into this device's
+ * address space over NVLink (CUDA IPC: tsa_ipc_alloc / tsa_ipc_open below) --
  * and the rows land at the same offsets in each.  The kernels end with a
  * system-scope fence; the caller orders the peers' reads after them with a
  * cross-rank barrier on the stream.  1 <= n_outs <= TSA_MAX_REPLICAS. */
@@ -184,6 +184,23 @@ TSA_API int tsa_attend_indexed_replicas(const tsa_desc* d, const void* q, const 
                                         const void* v, const void* kc, const void* vc,
                                         const int32_t* idx, const int32_t* k_keep,
                                         void* const* outs, int32_t n_outs, void* stream);
+
+/* Peer memory for those exchanges (CUDA IPC): tsa_ipc_alloc returns a zeroed
+ * device buffer and its 64-byte handle, which the other ranks map with
+ * tsa_ipc_open (over NVLink between GPUs; ranks sharing a device work too).
+ * tsa_peer_barrier is a cross-rank barrier on the stream: signals[r] is rank
+ * r's int32 [world] slot array (this rank's own and the mapped peers'); the
+ * call stores `epoch` into slot [rank] of every array (system-scope release,
+ * after a system fence) and waits until this rank's array holds >= epoch in
+ * every slot (acquire).  epoch starts at 1 and grows by one per call on the
+ * same arrays; a peer that never arrives traps after 60 s. */
+#define TSA_IPC_HANDLE_BYTES 64
+TSA_API int tsa_ipc_alloc(size_t bytes, void** ptr, void* handle);
+TSA_API int tsa_ipc_open(const void* handle, void** ptr);
+TSA_API int tsa_ipc_close(void* ptr);
+TSA_API int tsa_ipc_free(void* ptr);
+TSA_API int tsa_peer_barrier(int32_t* const* signals, int32_t world, int32_t rank, int32_t epoch,
+                             void* stream);
 
 /* out[h, t] = +0.0 for every t with inv[h, t] < 0 (scatter_rows' zero rows). */
 TSA_API int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream);

@@ -26,8 +26,10 @@ EXPORTS = (
     "tsa_dense_attention", "tsa_sparse_attention_layer", "tsa_rms_norm", "tsa_rope_table",
     "tsa_split_heads_rope", "tsa_heads_concat", "tsa_sparse_attention_layer_host",
     "tsa_layer_drift", "tsa_select_sparse_layers", "tsa_gather_zero_replicas",
-    "tsa_attend_indexed_replicas", "tsa_score_replicas",
+    "tsa_attend_indexed_replicas", "tsa_score_replicas", "tsa_ipc_alloc", "tsa_ipc_open",
+    "tsa_ipc_close", "tsa_ipc_free", "tsa_peer_barrier",
 )
+TSA_IPC_HANDLE_BYTES = 64
 TSA_MAX_REPLICAS = 8
 
 
@@ -99,6 +101,11 @@ def load() -> C.CDLL:
         "tsa_gather_zero": (C.c_int, [D, P, P, P, P, P, P, P, P, P]),
         "tsa_gather_zero_replicas": (C.c_int, [D, P, P, P, P, P, P, P, P, I, P]),
         "tsa_score_replicas": (C.c_int, [D, P, P, P, I, P, P]),
+        "tsa_ipc_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p), P]),
+        "tsa_ipc_open": (C.c_int, [P, C.POINTER(C.c_void_p)]),
+        "tsa_ipc_close": (C.c_int, [P]),
+        "tsa_ipc_free": (C.c_int, [P]),
+        "tsa_peer_barrier": (C.c_int, [P, I, I, I, P]),
         "tsa_attend_indexed_replicas": (C.c_int, [D, P, P, P, P, P, P, P, P, I, P]),
         "tsa_scatter_rows": (C.c_int, [D, P, P, P, P, P, P]),
         "tsa_check": (C.c_int, [D, P, P]),

@@ -14,19 +14,19 @@ score / select / gather / attend / scatter are local.  Two exchanges:
 The exchanges have two forms (``c2`` selects; "auto" = peer when possible):
 
   ``c2="peer"``  both exchanges fused into the kernels that produce the rows:
-                 the scores [H, L] and the output [H, L, d] are symmetric
-                 buffers on every rank (torch symmetric memory: CUDA IPC
-                 mappings over NVLink); the pool pass of the scoring, the
+                 the scores [H, L] and the output [H, L, d] are peer buffers
+                 on every rank (``PeerBuffers``: tsa_ipc_alloc / tsa_ipc_open,
+                 CUDA IPC mappings over NVLink); the pool pass of the scoring, the
                  zero-row pass and the attention epilogue store each row of
                  this rank's heads to every rank's buffer (tsa_*_replicas), so
                  the output exchange overlaps the attention tile by tile;
-                 device-side barriers over the signal pads order the budget
+                 device-side barriers (tsa_peer_barrier) order the budget
                  after the scores and end the step (and one starts it, so no
                  rank overwrites a buffer a peer is still reading);
   ``c2="nccl"``  ``all_gather_into_tensor`` after the scoring and after the
                  attention through torch.distributed (the gloo
                  tests, the unfused f32 / d != 128 path, and the fallback when
-                 symmetric memory cannot be set up).
+                 peer mapping cannot be set up).
 
 The per-stage compute is a pluggable backend: ``CudaBackend`` (the C ABI, the
 product) or a test backend; the orchestration is shared.
@@ -171,6 +171,76 @@ class CudaBackend:
                                                 _ptr(out_local), _stream(self.device)))
 
 
+class _CudaArray:
+    """A raw device pointer as a torch tensor (__cuda_array_interface__; the
+    memory stays owned by PeerBuffers)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+class PeerBuffers:
+    """Named device buffers every rank allocates with tsa_ipc_alloc and maps
+    from every peer with tsa_ipc_open (handles exchanged through the process
+    group), plus per-channel signal slots for tsa_peer_barrier.  ``ptrs[name]``
+    lists the buffer's base address on every rank, in rank order, as seen from
+    this device."""
+
+    CHANNELS = 3
+
+    def __init__(self, sizes: dict, rank: int, world: int, device):
+        self.lib, self.rank, self.world, self.device = _lib.load(), rank, world, device
+        if world > _lib.TSA_MAX_REPLICAS:
+            raise RuntimeError(f"peer exchange: world {world} > {_lib.TSA_MAX_REPLICAS}")
+        self._own, self._opened = [], []
+        sizes = dict(sizes, _signals=self.CHANNELS * world * 4)
+        mine = {}
+        with torch.cuda.device(device):
+            for name, nbytes in sizes.items():
+                ptr, h = C.c_void_p(), (C.c_char * _lib.TSA_IPC_HANDLE_BYTES)()
+                _lib.check(self.lib.tsa_ipc_alloc(nbytes, C.byref(ptr), h))
+                self._own.append(ptr.value)
+                mine[name] = (ptr.value, bytes(h))
+            every = [None] * world
+            if world > 1:
+                dist.all_gather_object(every, {k: v[1] for k, v in mine.items()})
+            self.ptrs = {}
+            for name in sizes:
+                row = []
+                for r in range(world):
+                    if r == rank:
+                        row.append(mine[name][0])
+                        continue
+                    ptr = C.c_void_p()
+                    h = (C.c_char * _lib.TSA_IPC_HANDLE_BYTES).from_buffer_copy(every[r][name])
+                    _lib.check(self.lib.tsa_ipc_open(h, C.byref(ptr)))
+                    self._opened.append(ptr.value)
+                    row.append(ptr.value)
+                self.ptrs[name] = row
+        self._epoch = [0] * self.CHANNELS
+        self._sig = [(C.c_void_p * _lib.TSA_MAX_REPLICAS)(
+            *[p + c * world * 4 for p in self.ptrs["_signals"]]) for c in range(self.CHANNELS)]
+
+    def tensor(self, name, shape, dtype):
+        """This rank's buffer as a tensor (bf16 through an int16 view)."""
+        ts = {torch.float32: "<f4", torch.bfloat16: "<i2", torch.int32: "<i4"}[dtype]
+        t = torch.as_tensor(_CudaArray(self.ptrs[name][self.rank], shape, ts), device=self.device)
+        return t.view(dtype) if dtype == torch.bfloat16 else t
+
+    def barrier(self, channel: int, stream=None):
+        self._epoch[channel] += 1
+        _lib.check(self.lib.tsa_peer_barrier(self._sig[channel], self.world, self.rank,
+                                             self._epoch[channel], _stream(self.device)))
+
+    def close(self):
+        for p in self._opened:
+            self.lib.tsa_ipc_close(C.c_void_p(p))
+        for p in self._own:
+            self.lib.tsa_ipc_free(C.c_void_p(p))
+        self._opened, self._own = [], []
+
+
 class ShardedSparseAttention:
     """One attention layer's sparse branch (model.cpp:169-183), head-sharded.
 
@@ -193,61 +263,72 @@ class ShardedSparseAttention:
         sh = self.shard
         self.s_local = torch.zeros((sh.h_per, L), dtype=torch.float32, device=device)
         self.s_full = self.s_local if world == 1 else torch.zeros((H, L), dtype=torch.float32,
-                                                                  device=device)  # peer: symmetric
+                                                                  device=device)  # peer: mapped
         self.out_local = torch.empty((sh.h_per, L, d), dtype=dtype, device=device)
         self.c2 = "nccl"
-        self._symm = None
+        self._peer = None
         if c2 not in ("auto", "nccl", "peer"):
             raise _lib.InvalidArgument(f"dist: c2 must be auto, nccl or peer, got {c2!r}")
         want_peer = ((world > 1 or c2 == "peer") and gather_output and c2 != "nccl"
                      and getattr(self.backend, "fused", False)
-                     and dist.is_initialized() and dist.get_backend() == "nccl")
+                     and (world == 1 or dist.is_initialized())
+                     and device is not None and torch.device(device).type == "cuda")
         if c2 == "peer" and not want_peer:
-            raise _lib.InvalidArgument("dist: c2='peer' needs an NCCL process group, the "
-                                       "gathered output and the fused bf16 / d = 128 path")
+            raise _lib.InvalidArgument("dist: c2='peer' needs CUDA devices, a process group "
+                                       "for world > 1, the gathered output and the fused "
+                                       "bf16 / d = 128 path")
         if want_peer:
             err = None
             try:
                 self._setup_peer(H, L, d, dtype, device)
-                self._symm.barrier(channel=0)  # the device barriers work on this node
-                self._symm_s.barrier(channel=0)
+                self._peer.barrier(0)  # the device barrier works between these ranks
                 torch.cuda.synchronize(device)
-            except Exception as e:  # symmetric memory unavailable: all-gather instead
+            except Exception as e:  # peer mapping unavailable: all-gathers instead
                 if c2 == "peer":
                     raise
                 err = f"{type(e).__name__}: {e}"
             if world > 1:  # every rank must take the same form of the exchange
-                ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=device)
+                ok = torch.tensor([0 if err else 1], dtype=torch.int32)
+                if dist.get_backend() == "nccl":
+                    ok = ok.to(device)
                 dist.all_reduce(ok, op=dist.ReduceOp.MIN)
                 if not int(ok.item()) and not err:
-                    err = "symmetric memory failed on another rank"
+                    err = "peer mapping failed on another rank"
             if err:
-                self.c2, self._symm = "nccl", None
+                if self._peer is not None:
+                    self._peer.close()
+                self.c2, self._peer = "nccl", None
                 self.c2_error = err
         if self.c2 != "peer":
             self.out_full = self.out_local if world == 1 or not gather_output else torch.empty(
                 (H, L, d), dtype=dtype, device=device)
 
     def _setup_peer(self, H, L, d, dtype, device):
-        import torch.distributed._symmetric_memory as symm_mem
-        world = self.shard.world
-        if world > _lib.TSA_MAX_REPLICAS:
-            raise RuntimeError(f"peer exchange: world {world} > {_lib.TSA_MAX_REPLICAS}")
-        out = symm_mem.empty((H, L, d), dtype=dtype, device=device)
-        hdl = symm_mem.rendezvous(out, dist.group.WORLD)
-        s_full = symm_mem.empty((H, L), dtype=torch.float32, device=device)
-        hdl_s = symm_mem.rendezvous(s_full, dist.group.WORLD)
-        ptrs, sptrs = list(hdl.buffer_ptrs), list(hdl_s.buffer_ptrs)
-        if len(ptrs) != world or len(sptrs) != world:
-            raise RuntimeError(f"symmetric memory: {len(ptrs)} buffers for world {world}")
-        self.out_full, self._symm = out, hdl
-        self.s_full, self._symm_s = s_full, hdl_s
-        self._replicas = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(*ptrs)
-        # this rank's score rows start at row h0 of every rank's [H, L] buffer
-        off = self.shard.h0 * L * 4
-        self._s_replicas = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(*[p + off for p in sptrs])
-        self._n_replicas = world
+        sh = self.shard
+        eb = 2 if dtype == torch.bfloat16 else 4
+        self._peer = PeerBuffers({"out": H * L * d * eb, "s": H * L * 4}, sh.rank, sh.world,
+                                 device)
+        self.out_full = self._peer.tensor("out", (H, L, d), dtype)
+        self.s_full = self._peer.tensor("s", (H, L), torch.float32)
+        # the shard's descriptor numbers its heads from 0: its output rows start at
+        # head h0 of every rank's [H, L, d] buffer, its score rows at row h0 of [H, L]
+        out_off = sh.h0 * L * d * eb
+        self._replicas = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(
+            *[p + out_off for p in self._peer.ptrs["out"]])
+        off = sh.h0 * L * 4
+        self._s_replicas = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(
+            *[p + off for p in self._peer.ptrs["s"]])
+        self._n_replicas = sh.world
         self.c2 = "peer"
+
+    def __del__(self):
+        peer = getattr(self, "_peer", None)
+        if peer is not None:
+            try:
+                torch.cuda.synchronize(self.device)
+                peer.close()
+            except Exception:
+                pass
 
     def _all_gather(self, dst, src):
         if self.shard.world == 1:
@@ -263,7 +344,7 @@ class ShardedSparseAttention:
         these input buffers: the chain never waits on the host (k_keep stays
         on the device), so the launch sequence is fixed and one graph launch
         replaces ~8 host launches and their gaps.  Single-process only (the
-        NCCL all-gathers and symmetric-memory barriers of a sharded step run
+        NCCL all-gathers and peer barriers of a sharded step run
         eagerly)."""
         if self.shard.world > 1 or self.c2 == "peer":
             return self.step(q, k, v, dense=dense)
@@ -301,10 +382,10 @@ class ShardedSparseAttention:
         if self.c2 == "peer":
             # no rank writes into a buffer a peer still reads; then the score
             # rows go to every rank's [H, L] buffer from the pool kernel
-            self._symm.barrier(channel=0)
+            self._peer.barrier(0)
             b.score_replicas(q, k, self._s_replicas, self._n_replicas)
             mark("score")
-            self._symm_s.barrier(channel=2)
+            self._peer.barrier(2)
             mark("c1_barrier")
             s_local = self.s_full[self.shard.h0:self.shard.h1]
         else:
@@ -319,12 +400,12 @@ class ShardedSparseAttention:
         mark("select")
         if self.c2 == "peer":
             # C2 fused into the producers: zero rows and attention output rows
-            # go to every rank's symmetric buffer over NVLink
+            # go to every rank's peer buffer over NVLink
             b.gather_kv_zero_replicas(k, v, k_keep, self._replicas, self._n_replicas)
             mark("gather_zero")
             b.attend_indexed_replicas(q, k, v, k_keep, self._replicas, self._n_replicas)
             mark("attend")
-            self._symm.barrier(channel=1)
+            self._peer.barrier(1)
             mark("c2_barrier")
             return self.out_full
         if getattr(b, "fused", False):

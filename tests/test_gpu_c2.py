@@ -2,8 +2,9 @@
 dist.py ``c2="peer"``): the zero-row pass and the attention epilogue store
 every output row to each replica of the [H, L, d] output.  One GPU is
 available to these tests, so the replicas are local buffers here and, in the
-symmetric-memory test, a world-size-1 NCCL group whose single buffer is
-mapped through the same rendezvous / barrier calls the 8-GPU run makes."""
+peer-buffer test, a world-size-1 group whose single buffer goes through the
+same IPC allocation and device barrier the 8-GPU run uses (the cross-process
+form runs in tests/test_gpu_dist.py with several ranks on one GPU)."""
 import os
 import subprocess
 import sys

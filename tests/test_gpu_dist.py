@@ -15,7 +15,7 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-def _rank(rank, world, port, out_path, tau, c):
+def _rank(rank, world, port, out_path, tau, c, c2):
     import paper_2602_03216_b200 as tsa
     from paper_2602_03216_b200 import workloads
     from paper_2602_03216_b200.dist import ShardedSparseAttention
@@ -25,11 +25,19 @@ def _rank(rank, world, port, out_path, tau, c):
     q, k, v = workloads.heavy_tailed_heads(c["H"], c["Hkv"], c["L"], 128, seed=c["seed"])
     plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
     lay = ShardedSparseAttention(c["H"], c["Hkv"], c["L"], 128, torch.bfloat16, plan, rank=rank,
-                                 world=world, device=q.device)
+                                 world=world, device=q.device, c2=c2)
     sh = lay.shard
-    out = lay.step(q[sh.h0:sh.h1].contiguous(), k[sh.kv0:sh.kv1].contiguous(),
-                   v[sh.kv0:sh.kv1].contiguous())
-    torch.cuda.synchronize()
+    args = (q[sh.h0:sh.h1].contiguous(), k[sh.kv0:sh.kv1].contiguous(),
+            v[sh.kv0:sh.kv1].contiguous())
+    for _ in range(3):  # repeated steps: barrier epochs, buffers rewritten in place
+        if lay.c2 == "peer":
+            lay.out_full.fill_(float("nan"))
+            lay.s_full.fill_(float("nan"))
+            torch.cuda.synchronize()
+            dist.barrier()  # no rank refills after a peer's kernels started writing
+        out = lay.step(*args)
+        torch.cuda.synchronize()
+        dist.barrier()
     if rank == 0:
         np.savez(out_path, out=out.view(torch.int16).cpu().numpy(), k_keep=lay.k_keep,
                  s=lay.s_full.cpu().numpy(), c2=lay.c2)
@@ -43,15 +51,19 @@ def _port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("c2", ["nccl", "peer"])
 @pytest.mark.parametrize("world,H,Hkv,tau", [(2, 8, 2, 0.02), (2, 8, 2, 0.0), (4, 16, 4, 0.02)])
-def test_multi_rank_cuda_sharding_matches_single_process(cuda, tmp_path, world, H, Hkv, tau):
+def test_multi_rank_cuda_sharding_matches_single_process(cuda, tmp_path, world, H, Hkv, tau, c2):
+    """c2="nccl": the all-gathers (over gloo here); c2="peer": the score and
+    output rows stored by the kernels into the other processes' IPC-mapped
+    buffers, with device barriers -- the fused exchange across processes."""
     import paper_2602_03216_b200 as tsa
     from paper_2602_03216_b200 import workloads
     from paper_2602_03216_b200.dist import ShardedSparseAttention
     out_path = str(tmp_path / "r0.npz")
     c = dict(H=H, Hkv=Hkv, L=2500, seed=41)
-    mp.start_processes(_rank, args=(world, _port(), out_path, tau, c), nprocs=world, join=True,
-                       start_method="spawn")
+    mp.start_processes(_rank, args=(world, _port(), out_path, tau, c, c2), nprocs=world,
+                       join=True, start_method="spawn")
     got = np.load(out_path)
     q, k, v = workloads.heavy_tailed_heads(c["H"], c["Hkv"], c["L"], 128, seed=c["seed"])
     plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
@@ -59,7 +71,7 @@ def test_multi_rank_cuda_sharding_matches_single_process(cuda, tmp_path, world, 
                                  device=q.device)
     ref = one.step(q, k, v)
     torch.cuda.synchronize()
-    assert str(got["c2"]) == "nccl"  # gloo: the all-gather form
+    assert str(got["c2"]) == c2
     assert int(got["k_keep"]) == one.k_keep
     assert np.array_equal(got["s"].view(np.uint32), one.s_full.cpu().numpy().view(np.uint32))
     assert np.array_equal(got["out"], ref.view(torch.int16).cpu().numpy())
