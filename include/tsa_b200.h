@@ -164,11 +164,12 @@ TSA_API int tsa_gather_zero(const tsa_desc* d, const void* k, const void* v, con
  * every rank.  Instead of all-gathers between the kernels, the kernels that
  * write score rows (the pool pass of tsa_score) and output rows (the zero rows
  * and the attention epilogue) store each row of the shard's heads to all
- * n_outs bases: outs[i] points at this shard's first head inside an
- * [H x L x d] buffer -- this rank's and each peer's buffer mapped into this
- * device's address space over NVLink (CUDA IPC: tsa_ipc_alloc / tsa_ipc_open
- * below) -- and head h of the descriptor (numbered from its head_begin) lands
- * at outs[i] + (h L + t) d, the same offset in each.  The kernels end with a
+ * n_outs bases: row t of the descriptor's head h (head_begin <= h < head_end)
+ * lands at outs[i] + (h L + t) d in each -- outs[i] is the base of an
+ * [H x L x d] buffer, this rank's and each peer's mapped into this device's
+ * address space over NVLink (CUDA IPC: tsa_ipc_alloc / tsa_ipc_open below),
+ * offset by h0 L d when the descriptor numbers a shard's heads from 0 (as
+ * dist.py's per-rank descriptors do).  The kernels end with a
  * system-scope fence; the caller orders the peers' reads after them with a
  * cross-rank barrier on the stream.  1 <= n_outs <= TSA_MAX_REPLICAS. */
 #define TSA_MAX_REPLICAS 8
