@@ -166,10 +166,18 @@ def run_ours(args):
     rank, world, local = rank_world()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # TSA_BENCH_SHARED_DEVICE=1: every rank on cuda:0 with gloo collectives -- a
+    # functional check of the N > 1 code path on a one-GPU box (timings meaningless)
+    shared = os.environ.get("TSA_BENCH_SHARED_DEVICE") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
     L, Hq, Hk = args.seq_len, args.heads, args.kv_heads
     sigma = args.sigma if args.sigma is not None else workloads.DEFAULT_SIGMA
     q, k, v = workloads.heavy_tailed_heads(Hq, Hk, L, D, sigma=sigma, seed=2602, device=device)
