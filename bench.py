@@ -144,6 +144,60 @@ def f_attn(k, d, heads):
     return 2.0 * k * (k + 1) * d * heads
 
 
+def kernel_rooflines(stages, H, Hkv, L, k, d=128, b=2, lq=64):
+    """Per-kernel roofline of one sparse step (SURVEY §8(d) work per unit):
+    achieved GB/s or TFLOP/s of each stage's algorithmic work over its event
+    time, against the measured HBM copy / sustained bf16 peaks."""
+    hbm, _, tf_sust, _ = measured_peaks()
+    work = {
+        # K read in two passes per KV group + Q tails + score rows; 2 passes x 2 lq L d H flop
+        "score": ("hbm", 2 * Hkv * L * d * b + H * lq * d * b + 4 * H * L, 4.0 * lq * L * d * H),
+        "budget": ("latency", 4 * H * L + 8 * L, None),
+        "select": ("latency", 4 * H * L + 8 * H * L, None),
+        # DRAM-minimal bytes: the selected K/V rows read once per KV group (the g
+        # query heads of a group read them through L2), the compressed rows written
+        # per query head, the dropped output rows zeroed, index / inverse maps
+        "gather_zero": ("hbm", 2 * Hkv * k * d * b + 2 * H * k * d * b + H * (L - k) * d * b
+                        + 4 * H * k + 4 * H * L, None),
+        "attend": ("tensor", None, f_attn(k, d, H)),
+    }
+    out = {}
+    for name, (bound, nbytes, flops) in work.items():
+        ms = stages.get(name)
+        if not ms:
+            continue
+        row = {"ms": round(ms, 4), "bound": bound}
+        if nbytes:
+            gbs = nbytes / (ms * 1e-3) / 1e9
+            row.update({"GB/s": round(gbs, 1), "hbm_frac": round(gbs / hbm, 4)})
+        if flops:
+            tfs = flops / (ms * 1e-3) / 1e12
+            row.update({"TFLOP/s": round(tfs, 1), "tensor_frac": round(tfs / tf_sust, 4)})
+        out[name] = row
+    return out
+
+
+def eager_stages(layer, ql, kl, vl, device, reps=3):
+    """Per-stage CUDA-event times of an eager sparse step (mean of reps)."""
+    stream = torch.cuda.current_stream(device)
+    acc = {}
+    layer.step(ql, kl, vl)
+    for _ in range(reps):
+        names, evs = [], []
+
+        def mark(n):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            names.append(n)
+            evs.append(e)
+        layer.step(ql, kl, vl, marks=mark)
+        torch.cuda.synchronize()
+        for i in range(1, len(evs)):
+            if names[i] != "start":
+                acc[names[i]] = acc.get(names[i], 0.0) + evs[i - 1].elapsed_time(evs[i]) / reps
+    return acc
+
+
 def barrier(world):
     if world > 1:
         dist.barrier()
@@ -336,7 +390,9 @@ def run_ours(args):
             "speedup_vs_dense": round(dense_ms / sparse_ms, 3) if dense_ms else None,
             "tau_sweep": sweep, "eager_ms": round(eager_ms, 3),
             "stages_ms": {kk: round(vv, 4) for kk, vv in stages.items()},
-            "hbm_stages": hbm_rows, "roofline": roofline, "e2e": e2e,
+            "hbm_stages": hbm_rows, "roofline": roofline,
+            "kernel_rooflines": kernel_rooflines(stages, sh.h_per, sh.kv_per, L, k_keep),
+            "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
             "other_configs": extras,
         }
@@ -560,9 +616,12 @@ def run_extra(name, args, tsa, workloads, Sharded, rank, world, device):
         ql, kl, vl = q[:g].contiguous(), k[:1].contiguous(), v[:1].contiguous()
         ms_sh = time_layer(lay, ql, kl, vl, steps, warm, 1, device)
         dense_sh = time_layer(lay, ql, kl, vl, steps, warm, 1, device, dense=True)
+        st_sh = eager_stages(lay, ql, kl, vl, device)
         out["per_rank_of_8"] = {"heads": f"{g} Q / 1 KV", "k_keep": lay.k_keep,
                                 "ms": round(ms_sh, 3), "dense_ms": round(dense_sh, 3),
                                 "speedup_vs_dense": round(dense_sh / ms_sh, 3),
+                                "kernel_rooflines": kernel_rooflines(st_sh, g, 1, L,
+                                                                     lay.k_keep),
                                 "note": "one GPU's share of the G=8 head-parallel layer "
                                         "(C1/C2 all-gathers not included)"}
         del lay, ql, kl, vl
