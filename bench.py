@@ -151,7 +151,8 @@ def kernel_rooflines(stages, H, Hkv, L, k, d=128, b=2, lq=64):
     hbm, _, tf_sust, _ = measured_peaks()
     work = {
         # K read in two passes per KV group + Q tails + score rows; 2 passes x 2 lq L d H flop
-        "score": ("hbm", 2 * Hkv * L * d * b + H * lq * d * b + 4 * H * L, 4.0 * lq * L * d * H),
+        "score": ("ridge (HBM ~ tensor; MUFU exp2 bound in practice)",
+                  2 * Hkv * L * d * b + H * lq * d * b + 4 * H * L, 4.0 * lq * L * d * H),
         "budget": ("latency", 4 * H * L + 8 * L, None),
         "select": ("latency", 4 * H * L + 8 * H * L, None),
         # DRAM-minimal bytes: the selected K/V rows read once per KV group (the g
