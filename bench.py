@@ -364,7 +364,7 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, tsa, ql, kl, vl, rank, world, device, args.tau)
+        e2e = run_e2e(args, tsa, ql, kl, vl, rank, world, device, args.tau, layer=layer)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -640,17 +640,30 @@ def profile_traffic(kernel):
         return None
 
 
-def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau):
-    """Through the public host-tensor API (sparse_attention_layer_host -> the
-    C-ABI tsa_sparse_attention_layer_host): every step copies this rank's q/k/v
-    from pinned host memory and its output back, pipelined with the compute."""
+def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau, layer=None):
+    """End to end with host buffers.  One GPU: the public host-tensor API
+    (sparse_attention_layer_host -> the C-ABI tsa_sparse_attention_layer_host),
+    copies pipelined with the compute.  N GPUs: each rank copies its shard's
+    q/k/v from pinned host memory, runs the head-sharded step (global budget,
+    exchanges) and copies its heads' output rows back."""
     hq, hk, hv = (t.cpu().pin_memory() for t in (ql, kl, vl))
     hout = torch.empty(ql.shape, dtype=ql.dtype).pin_memory()
     plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
     stream = torch.cuda.current_stream(device)
+    sharded = world > 1 and layer is not None
+    if sharded:
+        dq, dk, dv = (torch.empty_like(t) for t in (ql, kl, vl))
+        h0, h1 = layer.shard.h0, layer.shard.h1
 
     def step():
-        tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan, device=device)
+        if sharded:
+            dq.copy_(hq, non_blocking=True)
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            out = layer.step(dq, dk, dv)
+            hout.copy_(out[h0:h1], non_blocking=True)
+        else:
+            tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan, device=device)
 
     for _ in range(args.warmup):
         step()
@@ -667,10 +680,11 @@ def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau):
     return {"value": round(ms, 3), "unit": "ms",
             "h2d_bytes_per_step": (nb(ql) + nb(kl) + nb(vl)) * world,
             "d2h_bytes_per_step": nb(ql) * world,
-            "api": "sparse_attention_layer_host (tsa_sparse_attention_layer_host): H2D of K and "
-                   "the Q tails, then V and Q by head group (first and last group head by head), "
-                   "and D2H of each finished chunk overlap the compute",
-            "note": "per-rank head shard; world>1 runs the single-GPU layer call per rank"}
+            "api": ("ShardedSparseAttention.step on each rank's shard copied from pinned host "
+                    "memory, its heads' output rows copied back" if sharded else
+                    "sparse_attention_layer_host (tsa_sparse_attention_layer_host): H2D of K and "
+                    "the Q tails, then V and Q by head group (first and last group head by "
+                    "head), and D2H of each finished chunk overlap the compute")}
 
 
 # ----------------------------------------------------------- CPU baselines
