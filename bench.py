@@ -312,6 +312,7 @@ def run_ours(args):
         other = make(t)
         ms_t, _, _ = timed(other, max(2, args.steps // 2), 2, graph=True)
         sweep.append({"tau": t, "k_keep": other.k_keep, "ms": round(ms_t, 3)})
+        other.release()
         del other
     if dense_ms:
         for row in sweep:
@@ -601,6 +602,7 @@ def run_extra(name, args, tsa, workloads, Sharded, rank, world, device):
             dense_ms = 0.5 * (dense_ms + dense_after)
             for r in rows:
                 r["speedup_vs_dense"] = round(dense_ms / r["ms"], 3)
+        lay.release()
         del lay, ql, kl, vl
     out = {"workload": c["workload"], "seq_len": L, "n_heads": H_, "n_kv_heads": Hkv_,
            "heads_per_gpu": sh.h_per, "dense_ms": round(dense_ms, 3) if dense_ms else None,

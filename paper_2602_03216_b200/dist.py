@@ -233,12 +233,25 @@ class PeerBuffers:
         _lib.check(self.lib.tsa_peer_barrier(self._sig[channel], self.world, self.rank,
                                              self._epoch[channel], _stream(self.device)))
 
-    def close(self):
+    def close_mappings(self):
+        """Unmap the peers' buffers (local; safe at any time after the last step)."""
         for p in self._opened:
             self.lib.tsa_ipc_close(C.c_void_p(p))
+        self._opened = []
+
+    def release(self):
+        """Collective: every rank unmaps the peers' buffers, then frees its own
+        (an exporter may only free after every importer has closed)."""
+        torch.cuda.synchronize(self.device)
+        self.close_mappings()
+        if self.world > 1:
+            dist.barrier()
+        self.free_own()
+
+    def free_own(self):
         for p in self._own:
             self.lib.tsa_ipc_free(C.c_void_p(p))
-        self._opened, self._own = [], []
+        self._own = []
 
 
 class ShardedSparseAttention:
@@ -294,9 +307,14 @@ class ShardedSparseAttention:
                 dist.all_reduce(ok, op=dist.ReduceOp.MIN)
                 if not int(ok.item()) and not err:
                     err = "peer mapping failed on another rank"
-            if err:
+            if err:  # every rank reaches this branch together (same collective sequence)
                 if self._peer is not None:
-                    self._peer.close()
+                    torch.cuda.synchronize(device)
+                    self._peer.close_mappings()
+                if world > 1:
+                    dist.barrier()
+                if self._peer is not None:
+                    self._peer.free_own()
                 self.c2, self._peer = "nccl", None
                 self.c2_error = err
         if self.c2 != "peer":
@@ -321,12 +339,21 @@ class ShardedSparseAttention:
         self._n_replicas = sh.world
         self.c2 = "peer"
 
+    def release(self):
+        """Collective (all ranks together): frees the peer buffers.  Without it
+        a dropped layer only unmaps the peers' buffers and keeps its own until
+        the process exits -- freeing needs every importer closed first, and
+        garbage collection does not run in step across ranks."""
+        if self._peer is not None:
+            self._peer.release()
+            self._peer = None
+
     def __del__(self):
         peer = getattr(self, "_peer", None)
         if peer is not None:
             try:
                 torch.cuda.synchronize(self.device)
-                peer.close()
+                peer.close_mappings()
             except Exception:
                 pass
 
