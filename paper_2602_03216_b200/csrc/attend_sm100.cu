@@ -557,11 +557,15 @@ bool attend_sm100_supported(const tsa_desc& d) { return d.dtype == TSA_BF16 && d
 namespace {
 
 // Which exponential pairs of each 32-key chunk run on the FMA pipe
-// (TSA_EXP_POLY = 0 / 25 / 37 / 50 percent; a tuning knob, default 0: measured slower on B200, profiles/r1/poly_sweep.log).
+// (TSA_EXP_POLY = 0 / 25 / 37 / 50 percent).  Default 25: with the current
+// kernel a quarter of the off-diagonal exponentials on the FMA pipe measured
+// -1.8 % at 128K (dense -1.3 %; profiles/r1/ab_exp_poly.log), 37 / 50 slower;
+// the diagonal tile always uses MUFU.  (An earlier revision measured 25 %
+// slower: profiles/r1/poly_sweep.log.)
 uint32_t poly_mask() {
     static const uint32_t m = [] {
         const char* e = std::getenv("TSA_EXP_POLY");
-        const int pct = e ? std::atoi(e) : 0;
+        const int pct = e ? std::atoi(e) : 25;
         return pct <= 0 ? 0x0000u : pct <= 25 ? 0x1111u : pct <= 37 ? 0x2929u : 0x5555u;
     }();
     return m;

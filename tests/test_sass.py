@@ -23,7 +23,8 @@ def attend_sass():
     out = {}
     for part in re.split(r"\n\s*Function : ", txt):
         name = part.split("\n", 1)[0]
-        m = re.search(r"attend_sm100_kernelILb([01])ELj0EE", name)  # default (no poly) variants
+        # the default instantiation: a quarter of the exponentials on the FMA pipe
+        m = re.search(r"attend_sm100_kernelILb([01])ELj4369EE", name)
         if m:
             out["indexed" if m.group(1) == "1" else "dense"] = part
     assert set(out) == {"indexed", "dense"}, list(out)
