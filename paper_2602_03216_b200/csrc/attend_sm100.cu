@@ -559,7 +559,8 @@ namespace {
 // Which exponential pairs of each 32-key chunk run on the FMA pipe
 // (TSA_EXP_POLY = 0 / 25 / 37 / 50 percent).  Default 25: with the current
 // kernel a quarter of the off-diagonal exponentials on the FMA pipe measured
-// -1.8 % at 128K (dense -1.3 %; profiles/r1/ab_exp_poly.log), 37 / 50 slower;
+// -1.8 % at 128K (dense -1.3 %; profiles/r1/ab_exp_poly.log); 12.5 / 18.75 /
+// 37.5 / 50 % all measured slower than 25 %;
 // the diagonal tile always uses MUFU.  (An earlier revision measured 25 %
 // slower: profiles/r1/poly_sweep.log.)
 uint32_t poly_mask() {
