@@ -58,7 +58,7 @@ def parse():
     p.add_argument("--scoring", type=int, default=0, help="0 default, 1 reference-order, 2 fast")
     p.add_argument("--c2", choices=["auto", "nccl", "peer"], default="auto",
                    help="multi-GPU output exchange: peer-memory stores fused into the kernels "
-                        "(auto: when symmetric memory is available) or an NCCL all-gather")
+                        "(auto: when the CUDA IPC peer mapping can be set up) or an NCCL all-gather")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-dense", action="store_true")

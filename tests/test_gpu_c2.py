@@ -111,7 +111,7 @@ SCRIPT = textwrap.dedent("""
 """)
 
 
-def test_peer_c2_symmetric_memory_world1(cuda, tmp_path):
+def test_peer_c2_ipc_buffers_world1(cuda, tmp_path):
     import socket
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
