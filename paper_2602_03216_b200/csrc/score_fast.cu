@@ -206,7 +206,11 @@ score_pass1(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
                     float y0, y1;
                     f2_split(fma2(f2(__uint_as_float(x[c]), __uint_as_float(x[c + 1])), sc2, nm2), y0,
                              y1);
-                    ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], f2(ex2_approx(y0), ex2_approx(y1)));
+                    // every 4th pair on the FMA pipe (the kernel is MUFU-bound)
+                    const uint64_t e = ((c >> 1) & 3) == 3
+                                           ? ex2_poly2(f2(fmaxf(y0, -127.0f), fmaxf(y1, -127.0f)))
+                                           : f2(ex2_approx(y0), ex2_approx(y1));
+                    ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
                 }
                 float s0, s1;
                 f2_split(add2(add2(ps[0], ps[1]), add2(ps[2], ps[3])), s0, s1);
@@ -283,8 +287,17 @@ score_pass2(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
                                   f2(off.x, off.y)), y0, y1);
                     f2_split(fma2(f2(__uint_as_float(x[c + 2]), __uint_as_float(x[c + 3])), sc2,
                                   f2(off.z, off.w)), y2, y3);
-                    float p0 = ex2_approx(y0), p1 = ex2_approx(y1), p2 = ex2_approx(y2),
-                          p3 = ex2_approx(y3);
+                    float p0, p1, p2, p3;
+                    if ((rr & 12) == 12) {  // a quarter of the pairs on the FMA pipe
+                        f2_split(ex2_poly2(f2(fmaxf(y0, -127.0f), fmaxf(y1, -127.0f))), p0, p1);
+                        p2 = ex2_approx(y2);
+                        p3 = ex2_approx(y3);
+                    } else {
+                        p0 = ex2_approx(y0);
+                        p1 = ex2_approx(y1);
+                        p2 = ex2_approx(y2);
+                        p3 = ex2_approx(y3);
+                    }
                     if (!tile_full) {
                         p0 = rr + 0 >= r_first ? p0 : 0.0f;
                         p1 = rr + 1 >= r_first ? p1 : 0.0f;
