@@ -317,6 +317,8 @@ class ShardedSparseAttention:
                     self._peer.free_own()
                 self.c2, self._peer = "nccl", None
                 self.c2_error = err
+                self.s_full = self.s_local if world == 1 else torch.zeros(
+                    (H, L), dtype=torch.float32, device=device)  # not the freed peer buffer
         if self.c2 != "peer":
             self.out_full = self.out_local if world == 1 or not gather_output else torch.empty(
                 (H, L, d), dtype=dtype, device=device)
