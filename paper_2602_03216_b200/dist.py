@@ -34,6 +34,7 @@ product) or a test backend; the orchestration is shared.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -294,10 +295,10 @@ class ShardedSparseAttention:
             err = None
             try:
                 self._setup_peer(H, L, d, dtype, device)
-                self._peer.barrier(0)  # the device barrier works between these ranks
-                torch.cuda.synchronize(device)
+                if os.environ.get("TSA_TEST_PEER_FAIL_RANK") == str(rank):  # test hook
+                    raise RuntimeError("injected peer setup failure")
             except Exception as e:  # peer mapping unavailable: all-gathers instead
-                if c2 == "peer":
+                if c2 == "peer" and world == 1:
                     raise
                 err = f"{type(e).__name__}: {e}"
             if world > 1:  # every rank must take the same form of the exchange
@@ -319,6 +320,11 @@ class ShardedSparseAttention:
                 self.c2_error = err
                 self.s_full = self.s_local if world == 1 else torch.zeros(
                     (H, L), dtype=torch.float32, device=device)  # not the freed peer buffer
+                if c2 == "peer":
+                    raise RuntimeError(f"dist: c2='peer' could not be set up: {err}")
+            else:  # every rank mapped every peer: the device barrier works between them
+                self._peer.barrier(0)
+                torch.cuda.synchronize(device)
         if self.c2 != "peer":
             self.out_full = self.out_local if world == 1 or not gather_output else torch.empty(
                 (H, L, d), dtype=dtype, device=device)

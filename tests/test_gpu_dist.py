@@ -16,6 +16,9 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 def _rank(rank, world, port, out_path, tau, c, c2):
+    if c2 == "auto-fail":  # the last rank's peer setup fails: every rank falls back together
+        os.environ["TSA_TEST_PEER_FAIL_RANK"] = str(world - 1)
+        c2 = "auto"
     import paper_2602_03216_b200 as tsa
     from paper_2602_03216_b200 import workloads
     from paper_2602_03216_b200.dist import ShardedSparseAttention
@@ -51,7 +54,7 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("c2", ["nccl", "peer"])
+@pytest.mark.parametrize("c2", ["nccl", "peer", "auto-fail"])
 @pytest.mark.parametrize("world,H,Hkv,tau", [(2, 8, 2, 0.02), (2, 8, 2, 0.0), (4, 16, 4, 0.02)])
 def test_multi_rank_cuda_sharding_matches_single_process(cuda, tmp_path, world, H, Hkv, tau, c2):
     """c2="nccl": the all-gathers (over gloo here); c2="peer": the score and
@@ -71,7 +74,7 @@ def test_multi_rank_cuda_sharding_matches_single_process(cuda, tmp_path, world, 
                                  device=q.device)
     ref = one.step(q, k, v)
     torch.cuda.synchronize()
-    assert str(got["c2"]) == c2
+    assert str(got["c2"]) == ("nccl" if c2 == "auto-fail" else c2)
     assert int(got["k_keep"]) == one.k_keep
     assert np.array_equal(got["s"].view(np.uint32), one.s_full.cpu().numpy().view(np.uint32))
     assert np.array_equal(got["out"], ref.view(torch.int16).cpu().numpy())
