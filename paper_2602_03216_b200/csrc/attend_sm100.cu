@@ -55,7 +55,7 @@ struct __align__(1024) AttnSmem {
     uint8_t v[NS][TILE_BYTES];
     uint64_t q_full;
     uint64_t k_full[NS], v_full[NS], k_empty[NS], v_empty[NS];
-    uint64_t s_full[2], p_full[2][2], o_done[2];  // p_full[tile][half]
+    uint64_t s_full[2], p_full[2][4], o_done[2];  // p_full[tile][quarter]
     uint32_t tmem_base;
 };
 
@@ -82,6 +82,19 @@ __device__ __forceinline__ void issue_s(uint32_t t_s, uint32_t q_base, uint32_t 
     }
 }
 
+// O += P[:, 32q .. 32q+31] V[32q .. 32q+31, :] (quarter q of the 128-key tile).
+__device__ __forceinline__ void issue_pv_quarter(uint32_t t_o, uint32_t t_p, uint32_t v_base,
+                                                 uint32_t idesc, bool accumulate, int q,
+                                                 uint32_t leader) {
+    const uint32_t vlo = sdesc_lo(v_base, HALF_BYTES);
+#pragma unroll
+    for (int k2 = 0; k2 < 2; ++k2) {
+        const int kk = q * 2 + k2;
+        mma_bf16_ts_p(t_o, t_p + kk * 8, sdesc_from_lo(vlo + ((kk * 2048) >> 4)), idesc,
+                      (accumulate || kk > 0) ? 1u : 0u, leader);
+    }
+}
+
 // O += P[:, 64h .. 64h+63] V[64h .. 64h+63, :] (half h of the 128-key tile).
 __device__ __forceinline__ void issue_pv_half(uint32_t t_o, uint32_t t_p, uint32_t v_base,
                                               uint32_t idesc, bool accumulate, int half,
@@ -100,8 +113,10 @@ __device__ __forceinline__ void issue_pv_half(uint32_t t_o, uint32_t t_p, uint32
 // the FMA pipe (pairs set in kPolyMask, per 32-key chunk; the diagonal tile,
 // which carries the -inf causal mask, uses kPolyMask = 0), 4 packed partial
 // row sums, bf16 pack into S columns [0, 64) (tcgen05.st) with P released to
-// the MMA warp in two 64-key halves (p_full[0], p_full[1]) so PV on keys 0..63
-// overlaps the exponentials of keys 64..127.
+// the MMA warp in four 32-key quarters (p_full[0..3]) so the PV of the first
+// keys overlaps the exponentials of the later ones and only a quarter of the
+// PV remains after the last exponential (halves: +2 % at 128K,
+// profiles/r1/ab_p_quarters.log).
 template <uint32_t kPolyMask>
 __device__ __forceinline__ void exp_pack_row(const uint32_t (&r)[BN], uint64_t sc2, uint64_t nm2,
                                              uint32_t t_s, uint64_t* p_full, uint64_t (&ps)[4]) {
@@ -125,18 +140,18 @@ __device__ __forceinline__ void exp_pack_row(const uint32_t (&r)[BN], uint64_t s
             ps[e & 3] = add2(ps[e & 3], x);
             pk[e] = pack_bf16x2(p0, p1);
         }
-        // keys 0..63 are released once the next chunk's exponentials are in
-        // registers, so the wait for their TMEM stores overlaps that work
-        if (c0 == 64) {
+        // each 32-key quarter is released once the next chunk's exponentials are
+        // in registers, so the wait for its TMEM store overlaps that work
+        if (c0 > 0) {
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&p_full[0]);
+            mbar_arrive(&p_full[c0 / 32 - 1]);
         }
         tmem_st16(t_s + c0 / 2, pk);
         if (c0 == 96) {
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&p_full[1]);
+            mbar_arrive(&p_full[3]);
         }
     }
 }
@@ -318,8 +333,7 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&sm.s_full[b], 1);
-            mbar_init(&sm.p_full[b][0], 128);
-            mbar_init(&sm.p_full[b][1], 128);
+            for (int qq = 0; qq < 4; ++qq) mbar_init(&sm.p_full[b][qq], 128);
             mbar_init(&sm.o_done[b], 1);
         }
         fence_barrier_init();
@@ -458,12 +472,12 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const uint32_t v_base = smem_u32(sm.v[st]);
                 const bool k1_needed = (j1 < nkv) && (doA(j1) || doB(j1));
                 if (doA(j)) {
-                    mbar_wait(&sm.p_full[0][0], j & 1);
-                    tc_fence_after();
-                    issue_pv_half(tO[0], tS[0], v_base, idesc_o, j > 0, 0, L1);
-                    mbar_wait(&sm.p_full[0][1], j & 1);
-                    tc_fence_after();
-                    issue_pv_half(tO[0], tS[0], v_base, idesc_o, j > 0, 1, L1);
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        mbar_wait(&sm.p_full[0][qq], j & 1);
+                        tc_fence_after();
+                        issue_pv_quarter(tO[0], tS[0], v_base, idesc_o, j > 0, qq, L1);
+                    }
                     mma_commit_p(&sm.o_done[0], L1);
                     if (doA(j1)) {
                         mbar_wait(&sm.k_full[st1], (j1 / NS) & 1);
@@ -473,12 +487,12 @@ attend_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                 }
                 if (doB(j)) {
-                    mbar_wait(&sm.p_full[1][0], j & 1);
-                    tc_fence_after();
-                    issue_pv_half(tO[1], tS[1], v_base, idesc_o, j > 0, 0, L1);
-                    mbar_wait(&sm.p_full[1][1], j & 1);
-                    tc_fence_after();
-                    issue_pv_half(tO[1], tS[1], v_base, idesc_o, j > 0, 1, L1);
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        mbar_wait(&sm.p_full[1][qq], j & 1);
+                        tc_fence_after();
+                        issue_pv_quarter(tO[1], tS[1], v_base, idesc_o, j > 0, qq, L1);
+                    }
                     mma_commit_p(&sm.o_done[1], L1);
                     if (doB(j1)) {
                         mbar_wait(&sm.k_full[st1], (j1 / NS) & 1);
