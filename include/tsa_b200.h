@@ -50,8 +50,11 @@ enum tsa_mode { TSA_MODE_DENSE = 0, TSA_MODE_DYNAMIC = 1, TSA_MODE_FIXED = 2 };
 enum tsa_forced_policy { TSA_FORCED_FINAL_TOKEN = 0, TSA_FORCED_RECENT_WINDOW = 1 };
 enum tsa_status { TSA_OK = 0, TSA_ERR_INVALID = 1, TSA_ERR_CUDA = 2 };
 /* Scoring arithmetic: REFERENCE reproduces the reference's f32 operation
- * order (exact logits, sequential softmax sums); FAST runs Q K^T on the
- * tensor cores (bf16 only).  DEFAULT = REFERENCE for f32, FAST for bf16. */
+ * order bit for bit (sequential-order logits, glibc's expf, sequential softmax
+ * sums; bf16 d = 128 runs the fused kernels of score_exact.cu); FAST runs
+ * Q K^T on the tensor cores with approximate exponentials (bf16 only; scores
+ * within ~1e-5 relative, so k_keep / index sets may differ at near ties).
+ * DEFAULT = REFERENCE for f32, FAST for bf16. */
 enum tsa_scoring { TSA_SCORING_DEFAULT = 0, TSA_SCORING_REFERENCE = 1, TSA_SCORING_FAST = 2 };
 
 /* One attention layer's geometry plus the SparsePlan parameters
@@ -95,6 +98,12 @@ TSA_API int tsa_workspace_size(const tsa_desc* d, size_t* bytes);
 /* score_tokens (token_coverage.hpp:32 / token_coverage.cpp:16-50).
  * Writes s[h, :] for h in the shard; s is [H x L] f32. */
 TSA_API int tsa_score(const tsa_desc* d, const void* q, const void* k, float* s, void* ws, void* stream);
+
+/* The softmax exponential of REFERENCE scoring, elementwise on the device:
+ * y[i] = expf(x[i]) exactly as glibc computes it (std::exp(float),
+ * tensor_ops.cpp:62), for x <= 0.  Exported so the parity suite can pin the
+ * port against the host libm. */
+TSA_API int tsa_expf(const float* x, float* y, int64_t n, void* stream);
 
 /* aggregate_scores + coverage_budget (token_coverage.cpp:52-96) for
  * TSA_MODE_DYNAMIC, fixed_budget (:98-109) for TSA_MODE_FIXED, L for

@@ -86,6 +86,8 @@ class Oracle:
             L.tsa_oracle_compute_drift.argtypes = [_f32p, _I, _I, _I, _D, _f64p]
             L.tsa_oracle_select_sparse_layers.argtypes = [_f64p, _I, _D, _f64p, _i32p, C.POINTER(_I)]
             L.tsa_oracle_rng_new.restype = C.c_void_p
+            L.tsa_oracle_expf.argtypes = [_f32p, _f32p, C.c_int64]
+            L.tsa_oracle_expf.restype = None
             L.tsa_oracle_rng_new.argtypes = [C.c_uint64]
             L.tsa_oracle_rng_free.argtypes = [C.c_void_p]
             L.tsa_oracle_rng_fill.argtypes = [C.c_void_p, C.c_int64, C.c_float, _f32p]
@@ -137,6 +139,13 @@ class Oracle:
         else:
             self._check(self.lib.tsa_ref_score_tokens(q, k, H, Hkv, L, d, last_q, kernel, s))
         return s
+
+    def expf(self, x):
+        """The host libm's expf, elementwise (std::exp(float), tensor_ops.cpp:62)."""
+        x = _f32(x)
+        y = np.empty_like(x)
+        self.lib.tsa_oracle_expf(x.ravel(), y.ravel(), x.size) if self.kind == "port" else None
+        return y
 
     def aggregate_scores(self, s):
         """token_coverage.cpp:52-66 -> s_l [L] f32."""

@@ -757,3 +757,10 @@ EXPORT int tsa_oracle_select_sparse_layers(const double* R, int n, double delta,
     *n_layers = m;
     return 0;
 }
+
+/* The softmax exponential as the reference evaluates it: std::exp(float) is
+ * the host libm's expf (tensor_ops.cpp:62).  Batch form for the GPU parity
+ * test of the exact scorer's expf port (tests/test_gpu_exact.py). */
+EXPORT void tsa_oracle_expf(const float* x, float* y, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) y[i] = expf(x[i]);
+}

@@ -27,7 +27,7 @@ EXPORTS = (
     "tsa_split_heads_rope", "tsa_heads_concat", "tsa_sparse_attention_layer_host",
     "tsa_layer_drift", "tsa_select_sparse_layers", "tsa_gather_zero_replicas",
     "tsa_attend_indexed_replicas", "tsa_score_replicas", "tsa_ipc_alloc", "tsa_ipc_open",
-    "tsa_ipc_close", "tsa_ipc_free", "tsa_peer_barrier",
+    "tsa_ipc_close", "tsa_ipc_free", "tsa_peer_barrier", "tsa_expf",
 )
 TSA_IPC_HANDLE_BYTES = 64
 TSA_MAX_REPLICAS = 8
@@ -89,6 +89,7 @@ def load() -> C.CDLL:
         "tsa_sparse_attention_layer_host": (C.c_int, [D, P, P, P, P, P, P, P, P, P, P, P, P, I, P]),
         "tsa_workspace_size": (C.c_int, [D, C.POINTER(C.c_size_t)]),
         "tsa_score": (C.c_int, [D, P, P, P, P, P]),
+        "tsa_expf": (C.c_int, [P, P, C.c_int64, P]),
         "tsa_budget": (C.c_int, [D, P, P, P, P]),
         "tsa_aggregate_scores": (C.c_int, [D, P, P, P, P]),
         "tsa_coverage_budget": (C.c_int, [D, P, I, P, P, P]),

@@ -334,12 +334,8 @@ int launch_tiled_d128_f32(const tsa_desc& d, const void* q, const void* k, const
     const int nh = d.head_end - d.head_begin;
     dim3 grid((d.seq_len + TR - 1) / TR, nh);
     const int smem = (TD * TR + 2 * TD * TK + 2 * TK * TD + TK * TR) * (int)sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(attend_tiled_d128<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem);
-        attr = true;
-    }
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(attend_tiled_d128<float>), smem))
+        return rc;
     attend_tiled_d128<float><<<grid, 128, smem, st>>>((const float*)q, (const float*)k,
                                                       (const float*)v, n_dev, n_const, kv_group,
                                                       rph, kvrph, d.head_begin,

@@ -544,6 +544,24 @@ int make_bf16_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t b
     return 0;
 }
 
+// 2-D map over an f32 matrix [rows x inner] (row pitch row_stride_bytes, a
+// multiple of 16), box_inner x box_rows boxes, no swizzle (score_exact.cu).
+int make_f32_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows,
+                    uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return invalid("tsa: cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {row_stride_bytes};
+    cuuint32_t box[2] = {box_inner, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return invalid("tsa: f32 tensor map encode failed (" + std::to_string((int)r) + ")");
+    return 0;
+}
+
 // 3-D map over [heads x rows x 128] bf16 with the same 64 x 128 SW128 boxes,
 // used by the indexed kernel for a head's last, partial V tile: past the
 // head's last row it reads zeros (out of bounds), never the next head's rows
@@ -593,12 +611,7 @@ void run_kernel(dim3 grid, cudaStream_t st, const CUtensorMap& mq, const CUtenso
                 int32_t rows_per_head, int32_t kv_rows_per_head, int head_begin, float scale_log2,
                 const OutReplicas& o, const int32_t* idx) {
     const int smem = (int)sizeof(AttnSmem) + 1024;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(attend_sm100_kernel<kIndexed, kPolyMask>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_set = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(attend_sm100_kernel<kIndexed, kPolyMask>), smem);
     attend_sm100_kernel<kIndexed, kPolyMask><<<grid, kThreads, smem, st>>>(
         mq, mk, mv, mkd, mvd, mv3, mvd3, dense_group, n_dev, n_const, kv_group, rows_per_head,
         kv_rows_per_head, head_begin,

@@ -5,7 +5,10 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 
 #include "common.cuh"
 
@@ -30,6 +33,35 @@ int cuda_check(cudaError_t e, const char* what) {
     return TSA_ERR_CUDA;
 }
 
+int num_sms() {
+    static std::atomic<int> cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return kNumSMs;
+    if (dev < 64) {
+        const int c = cache[dev].load(std::memory_order_relaxed);
+        if (c > 0) return c;
+    }
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1)
+        n = kNumSMs;
+    if (dev < 64) cache[dev].store(n, std::memory_order_relaxed);
+    return n;
+}
+
+int ensure_smem_attr(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_check(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({dev, fn})) return 0;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute");
+    done.insert({dev, fn});
+    return 0;
+}
+
 Workspace workspace_layout(const tsa_desc& d) {
     Workspace w{};
     const size_t H = d.n_heads, L = d.seq_len, D = d.d_head;
@@ -43,8 +75,11 @@ Workspace workspace_layout(const tsa_desc& d) {
     w.status = take(4);
     w.k_keep = take(4);
     w.headsum = take(4 * L);
-    w.logits = take(4 * H * lq * L);
-    w.rowstat = take(8 * 128 * (2 * (size_t)kNumSMs + H + 8));  // fast-scoring row partials
+    w.logits = take(4 * H * lq * exact_logits_stride(d.seq_len));
+    w.rowstat = take(score_fast_rowstat_bytes(d));
+    w.rowmax = take(4 * H * lq);
+    w.rowsum = take(4 * H * lq);
+    w.colraw = take(4 * H * L);
     w.scores = take(4 * H * L);
     w.forced = take(4 * L);
     w.idx = take(4 * H * L);
@@ -182,8 +217,11 @@ static int score_impl(const tsa_desc* d, const void* q, const void* k, const Out
                       void* ws, void* stream) {
     const Workspace w = workspace_layout(*d);
     if (scoring_mode(*d) == TSA_SCORING_FAST)
-        return launch_score_fast(*d, q, k, s, at<float>(ws, w.logits), at<float>(ws, w.rowstat),
+        return launch_score_fast(*d, q, k, s, at<float>(ws, w.colraw), at<float>(ws, w.rowstat),
                                  S(stream));
+    if (score_exact_supported(*d) && lq_of(*d) <= 4096)
+        return launch_score_exact(*d, q, k, s, at<float>(ws, w.logits), at<int>(ws, w.rowmax),
+                                  at<float>(ws, w.rowsum), at<float>(ws, w.colraw), S(stream));
     return launch_score_reference(*d, q, k, s, at<float>(ws, w.logits), S(stream));
 }
 
@@ -193,6 +231,11 @@ int tsa_score(const tsa_desc* d, const void* q, const void* k, float* s, void* w
 }
 
 static int make_replicas(const char* who, void* const* outs, int32_t n_outs, OutReplicas* r);
+
+int tsa_expf(const float* x, float* y, int64_t n, void* stream) {
+    if (n < 0 || (n > 0 && (!x || !y))) return invalid("tsa_expf: bad arguments");
+    return launch_expf(x, y, n, S(stream));
+}
 
 int tsa_score_replicas(const tsa_desc* d, const void* q, const void* k, float* const* s_outs,
                        int32_t n_outs, void* ws, void* stream) {

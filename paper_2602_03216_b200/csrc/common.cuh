@@ -13,7 +13,14 @@
 
 namespace tsa {
 
-constexpr int kNumSMs = 148;
+constexpr int kNumSMs = 148;  // B200; grids that must fill the GPU use num_sms()
+
+// SM count of the current device (queried once per device).
+int num_sms();
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the current device,
+// set once per (device, kernel) -- the attribute is per device context -- and
+// thread safe.
+int ensure_smem_attr(const void* fn, int bytes);
 
 // Output replicas of the fused multi-GPU boundary: the same [H, L, d] layout
 // at up to TSA_MAX_REPLICAS bases (this rank's buffer and the peers'
@@ -79,8 +86,11 @@ struct Workspace {
     size_t status;    // int32 device status word (0 ok, else error code)
     size_t k_keep;    // int32 scratch k_keep for composite calls
     size_t headsum;   // f32 [L]        sum_h s[h, t]
-    size_t logits;    // f32 [H x lq x L] reference-order scoring rows (REFERENCE mode)
-    size_t rowstat;   // f32 [H x lq x 2] (fast scoring: row max / sum)
+    size_t logits;    // f32 [H x lq x Lp] reference-order logits (REFERENCE / EXACT mode)
+    size_t rowstat;   // float2 row partials of FAST scoring (score_fast_rowstat_bytes)
+    size_t rowmax;    // int32 [H x lq]  EXACT scoring: encoded row maxima
+    size_t rowsum;    // f32 [H x lq]    EXACT scoring: sequential row sums
+    size_t colraw;    // f32 [H x L]     raw column sums before the pool
     size_t scores;    // f32 [H x L]
     size_t forced;    // int32 [max(L, 1)]
     size_t idx;       // int32 [H x L]
@@ -95,6 +105,9 @@ inline int lq_of(const tsa_desc& d) { return d.last_q < d.seq_len ? d.last_q : d
 
 bool score_fast_available();
 bool score_fast_supported(const tsa_desc& d);
+size_t score_fast_rowstat_bytes(const tsa_desc& d);
+bool score_exact_supported(const tsa_desc& d);
+size_t exact_logits_stride(int L);
 
 inline int scoring_mode(const tsa_desc& d) {
     if (d.scoring == TSA_SCORING_DEFAULT)
@@ -110,6 +123,9 @@ int launch_score_reference(const tsa_desc& d, const void* q, const void* k, cons
                            float* logits, cudaStream_t st);
 int launch_score_fast(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s,
                       float* logits, float* rowstat, cudaStream_t st);
+int launch_expf(const float* x, float* y, int64_t n, cudaStream_t st);
+int launch_score_exact(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s,
+                       float* X, int* rowmax, float* rowsum, float* colraw, cudaStream_t st);
 // select.cu
 int launch_budget(const tsa_desc& d, const float* s, int32_t* k_keep, float* headsum,
                   int32_t* status, int min_keep, cudaStream_t st);

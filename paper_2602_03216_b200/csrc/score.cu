@@ -7,12 +7,14 @@
 //                                                                     (tensor_ops.cpp:47-69)
 //   colsum  c[j] = sum_r P[r, j]                                      r ascending (:43-46)
 //   pool    edge-clamped mean with Eigen's SSE2 segment-sum order     (tensor_ops.cpp:114-129)
-// so scores match the reference bit-for-bit except where glibc's expf and a
-// correctly rounded exp differ (<= 1 ulp, rare).  Three launches:
+// so scores match the reference bit for bit (expf is glibc's algorithm ported
+// exactly, expf_glibc.cuh).  This is the general path (f32 inputs, any d);
+// bf16 with d = 128 runs the fused kernels of score_exact.cu.  Three launches:
 //   score_logits_ref  -> logits[h, r, j] (only the causally allowed prefix)
 //   score_softmax_ref -> in place: P[h, r, j]
 //   score_colsum_ref  -> s[h, t] (column sums + pooling, halo of kernel/2)
 #include "common.cuh"
+#include "expf_glibc.cuh"
 
 namespace tsa {
 namespace {
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q,
     }
 }
 
-// One warp per (head, row): max, e = (float)exp((double)(x - max)), sequential
+// One warp per (head, row): max, e = expf(x - max) (glibc's), sequential
 // f32 sum in j order, then divide.  Masked entries (j >= allowed) untouched.
 __global__ void __launch_bounds__(256) score_softmax_ref(float* __restrict__ logits, int L, int lq,
                                                          int head_begin, int n_rows) {
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(256) score_softmax_ref(float* __restrict__ log
         const int j = j0 + lane;
         float e = 0.0f;
         if (j < allowed) {
-            e = (float)exp((double)__fsub_rn(row[j], mx));
+            e = tsa_dev::expf_glibc(__fsub_rn(row[j], mx));
             row[j] = e;
         }
         const int cnt = min(32, allowed - j0);

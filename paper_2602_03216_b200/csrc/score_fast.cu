@@ -327,11 +327,7 @@ template <int LQ>
 int launch_pass2(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
                  int L, int g, int hpt, int tpk, int n_chunks, float sl2, const float2* partial,
                  float* colraw) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(score_pass2<LQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(score_pass2<LQ>), smem)) return rc;
     score_pass2<LQ><<<grid, 192, smem, st>>>(mq, mk, L, g, hpt, tpk, n_chunks, sl2, partial, colraw);
     TSA_LAUNCH_CHECK("score_fast_pass2");
     return 0;
@@ -340,6 +336,37 @@ int launch_pass2(dim3 grid, int smem, cudaStream_t st, const CUtensorMap& mq, co
 }  // namespace
 
 bool score_fast_available() { return true; }
+
+namespace {
+struct FastGeom {
+    int lq, g, hpt, tiles_per_kv, kv_begin, n_kv, mtiles, n_ktiles;
+};
+FastGeom fast_geom(const tsa_desc& d) {
+    FastGeom f;
+    f.lq = lq_of(d);
+    f.g = d.n_heads / d.n_kv_heads;
+    f.hpt = std::min(128 / f.lq, f.g);
+    f.tiles_per_kv = (f.g + f.hpt - 1) / f.hpt;
+    f.kv_begin = d.head_begin / f.g;
+    f.n_kv = d.head_end / f.g - f.kv_begin;
+    f.mtiles = f.n_kv * f.tiles_per_kv;
+    f.n_ktiles = (d.seq_len + SF_BN - 1) / SF_BN;
+    return f;
+}
+}  // namespace
+
+// Row partials of pass 1: mtiles x n_chunks x 128 float2, n_chunks <= the
+// key-tile count and SF_MAX_CHUNKS -- sized for the whole layer (every shard
+// fits), independent of the device's SM count.
+size_t score_fast_rowstat_bytes(const tsa_desc& d) {
+    tsa_desc all = d;
+    all.head_begin = 0;
+    all.head_end = d.n_heads;
+    if (d.last_q < 1 || d.n_kv_heads < 1) return 0;
+    const FastGeom f = fast_geom(all);
+    if (f.lq > 128) return 0;
+    return (size_t)f.mtiles * std::min(f.n_ktiles, SF_MAX_CHUNKS) * SF_BM * sizeof(float2);
+}
 
 bool score_fast_supported(const tsa_desc& d) {
     const int lq = lq_of(d);
@@ -352,16 +379,15 @@ int launch_score_fast(const tsa_desc& d, const void* q, const void* k, const Out
     if (!score_fast_supported(d))
         return invalid("score_tokens: FAST scoring needs bf16, d_head 128 and last_q (clamped to "
                        "L) a multiple of 32 up to 128");
-    const int L = d.seq_len, lq = lq_of(d);
-    const int g = d.n_heads / d.n_kv_heads;
-    const int hpt = std::min(128 / lq, g);
-    const int tiles_per_kv = (g + hpt - 1) / hpt;
-    const int kv_begin = d.head_begin / g, kv_end = d.head_end / g;
-    const int n_kv = kv_end - kv_begin;
-    const int mtiles = n_kv * tiles_per_kv;
-    const int n_ktiles = (L + SF_BN - 1) / SF_BN;
+    const int L = d.seq_len;
+    const FastGeom f = fast_geom(d);
+    const int lq = f.lq, g = f.g, hpt = f.hpt, tiles_per_kv = f.tiles_per_kv;
+    const int kv_begin = f.kv_begin, n_kv = f.n_kv, mtiles = f.mtiles, n_ktiles = f.n_ktiles;
     const int n_chunks =
-        std::max(1, std::min({n_ktiles, SF_MAX_CHUNKS, (4 * kNumSMs + mtiles - 1) / mtiles}));
+        std::max(1, std::min({n_ktiles, SF_MAX_CHUNKS, (4 * num_sms() + mtiles - 1) / mtiles}));
+    // the workspace holds every chunk partial (score_fast_rowstat_bytes)
+    if ((size_t)mtiles * n_chunks * SF_BM * sizeof(float2) > score_fast_rowstat_bytes(d))
+        return invalid("score_fast: row-partial workspace too small");
     // shard-local views: heads [head_begin, head_end) start at kv_begin
     const size_t eb = 2;
     const uint8_t* qb = static_cast<const uint8_t*>(q) + (size_t)kv_begin * g * L * SF_HD * eb;
@@ -371,11 +397,7 @@ int launch_score_fast(const tsa_desc& d, const void* q, const void* k, const Out
     if ((rc = make_bf16_map_2d(&mq, qb, (uint64_t)n_kv * g * L, (uint32_t)lq))) return rc;
     if ((rc = make_bf16_map_2d(&mk, kb, (uint64_t)n_kv * L, 128))) return rc;
     const int smem = (int)sizeof(ScoreSmem) + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(score_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(score_pass1), smem))) return rc;
     const float sl2 = (1.0f / sqrtf((float)SF_HD)) * 1.4426950408889634f;
     float2* partial = reinterpret_cast<float2*>(partial_ws);
     float* colraw_local = colraw + (size_t)d.head_begin * L;  // indexed by local head

@@ -738,12 +738,8 @@ static void launch_budget_kernel(const float* v, int L, double tau, int min_keep
                                  cudaStream_t st) {
     const int slice = (L + CL - 1) / CL;
     if (slice <= kSliceMax) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(budget_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSliceMax * 4 + 4 * 2048 * 4);
-            attr = true;
-        }
+        ensure_smem_attr(reinterpret_cast<const void*>(budget_kernel<true>),
+                         kSliceMax * 4 + 4 * 2048 * 4);
         const int smem = (slice + 3) / 4 * 4 * 4 + 4 * 2048 * 4;  // slice + mass limbs
         budget_kernel<true><<<CL, BB, smem, st>>>(v, L, tau, min_keep, k_keep, status, mode,
                                                   sl_out, exact_total);
@@ -796,12 +792,7 @@ int launch_select(const tsa_desc& d, const float* s, const int32_t* k_keep, cons
     const int slice = (d.seq_len + CL - 1) / CL;
     if (slice <= kSliceMax) {
         const int smem = slice * 4;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(select_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSliceMax * 4);
-            attr = true;
-        }
+        ensure_smem_attr(reinterpret_cast<const void*>(select_smem_kernel), kSliceMax * 4);
         select_smem_kernel<<<dim3(CL, nh), BS, smem, st>>>(s, d.seq_len, k_keep, forced, n_forced,
                                                            forced_begin, d.head_begin, idx, inv);
     } else {
