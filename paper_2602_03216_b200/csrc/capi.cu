@@ -6,7 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <mutex>
-#include <set>
+#include <map>
 #include <string>
 #include <utility>
 
@@ -50,15 +50,16 @@ int num_sms() {
 
 int ensure_smem_attr(const void* fn, int bytes) {
     static std::mutex mu;
-    static std::set<std::pair<int, const void*>> done;
+    static std::map<std::pair<int, const void*>, int> set_to;  // largest value set so far
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_check(e, "cudaGetDevice");
     std::lock_guard<std::mutex> lock(mu);
-    if (done.count({dev, fn})) return 0;
+    auto it = set_to.find({dev, fn});
+    if (it != set_to.end() && it->second >= bytes) return 0;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute");
-    done.insert({dev, fn});
+    set_to[{dev, fn}] = bytes;
     return 0;
 }
 
@@ -219,7 +220,7 @@ static int score_impl(const tsa_desc* d, const void* q, const void* k, const Out
     if (scoring_mode(*d) == TSA_SCORING_FAST)
         return launch_score_fast(*d, q, k, s, at<float>(ws, w.colraw), at<float>(ws, w.rowstat),
                                  S(stream));
-    if (score_exact_supported(*d) && lq_of(*d) <= 4096)
+    if (score_exact_supported(*d) && lq_of(*d) <= 2048)
         return launch_score_exact(*d, q, k, s, at<float>(ws, w.logits), at<int>(ws, w.rowmax),
                                   at<float>(ws, w.rowsum), at<float>(ws, w.colraw), S(stream));
     return launch_score_reference(*d, q, k, s, at<float>(ws, w.logits), S(stream));

@@ -31,26 +31,37 @@ __device__ __constant__ const uint64_t kExp2fTab[32] = {
     0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull,
 };
 
-__device__ __forceinline__ float expf_glibc(float x) {
-    if (x < -0x1.9fe368p6f) return 0.0f;  // x < log(2^-150): glibc's __math_uflowf -> +0
-    constexpr double kInvLn2N = 0x1.71547652b82fep+0 * 32;
+// InvLn2N, C0, C1, C2 from constant memory: DFMA reads them as c[][]
+// operands (as immediates they would be rebuilt with MOV pairs per call).
+__device__ __constant__ double kExpfC[4] = {  // not const: no folding into immediates
+    0x1.71547652b82fep+0 * 32, 0x1.c6af84b912394p-5 / 32 / 32 / 32, 0x1.ebfce50fac4f3p-3 / 32 / 32,
+    0x1.62e42ff0c52d6p-1 / 32};
+
+// Call sites keep the table in shared memory (exp2f_table_to_smem): indexed
+// per thread, a __constant__ table would serialise a warp's distinct lookups.
+__device__ __forceinline__ void exp2f_table_to_smem(uint64_t* tab) {
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) tab[i] = kExp2fTab[i];
+}
+
+// Branch-free (the underflow case is a select at the end), so a thread's
+// independent exponentials interleave.
+__device__ __forceinline__ float expf_glibc(float x, const uint64_t* __restrict__ tab) {
+    const double kInvLn2N = kExpfC[0], kC0 = kExpfC[1], kC1 = kExpfC[2], kC2 = kExpfC[3];
     constexpr double kShift = 0x1.8p+52;
-    constexpr double kC0 = 0x1.c6af84b912394p-5 / 32 / 32 / 32;
-    constexpr double kC1 = 0x1.ebfce50fac4f3p-3 / 32 / 32;
-    constexpr double kC2 = 0x1.62e42ff0c52d6p-1 / 32;
-    const double xd = (double)x;
+    const double xd = (double)fmaxf(x, -104.0f);  // keeps the table index in range
     double kd = __fma_rn(kInvLn2N, xd, kShift);  // round(x N / ln2) in the low mantissa bits
     const uint64_t ki = (uint64_t)__double_as_longlong(kd);
     kd = __dsub_rn(kd, kShift);
     const double r = __fma_rn(kInvLn2N, xd, -kd);
-    const uint64_t t = kExp2fTab[ki & 31] + (ki << 47);
+    const uint64_t t = tab[ki & 31] + (ki << 47);
     const double s = __longlong_as_double((long long)t);
     const double z = __fma_rn(kC0, r, kC1);
     const double r2 = __dmul_rn(r, r);
     double y = __fma_rn(kC2, r, 1.0);
     y = __fma_rn(z, r2, y);
     y = __dmul_rn(y, s);
-    return __double2float_rn(y);
+    // x < log(2^-150): glibc's __math_uflowf -> +0
+    return x < -0x1.9fe368p6f ? 0.0f : __double2float_rn(y);
 }
 
 }  // namespace tsa_dev

@@ -90,6 +90,9 @@ __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q,
 // f32 sum in j order, then divide.  Masked entries (j >= allowed) untouched.
 __global__ void __launch_bounds__(256) score_softmax_ref(float* __restrict__ logits, int L, int lq,
                                                          int head_begin, int n_rows) {
+    __shared__ uint64_t tab[32];
+    tsa_dev::exp2f_table_to_smem(tab);
+    __syncthreads();
     const int warp = blockIdx.x * 8 + threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     if (warp >= n_rows) return;
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(256) score_softmax_ref(float* __restrict__ log
         const int j = j0 + lane;
         float e = 0.0f;
         if (j < allowed) {
-            e = tsa_dev::expf_glibc(__fsub_rn(row[j], mx));
+            e = tsa_dev::expf_glibc(__fsub_rn(row[j], mx), tab);
             row[j] = e;
         }
         const int cnt = min(32, allowed - j0);

@@ -25,12 +25,13 @@
 //     Lp = round_up(L, 64)) and the row maxima (order-independent, atomicMax
 //     on an ordered-int encoding).  34.4 G FMA at 128K / Llama-3-8B: the
 //     FP32 pipe is the roofline.
-//   score_exact_rowsum (XB): the sequential row sums, one CTA per 16 rows: X
-//     tiles arrive by TMA, 8 helper warps compute e into a transposed shared
-//     tile, one warp (lane = row) runs the f32 chain in key order.  The chain
-//     (L dependent FADDs per row) is this kernel's critical path.
-//   score_exact_colsum (XC): thread = key, P = e / sum_r accumulated over r in
-//     order -> raw column sums.
+//   score_exact_rowsum (XB): the sequential row sums, one CTA per ~n_rows/#SM
+//     rows (<= 16): X tiles arrive by TMA, 8 helper warps (thread = key)
+//     compute e into a transposed shared tile, one warp (lane = row) runs the
+//     f32 chain in key order -- L dependent FADDs per row, the floor of this
+//     kernel (0.27 ms at 128K).
+//   score_exact_colsum (XC): thread = key, e recomputed, P = e / sum_r
+//     accumulated over r in order -> raw column sums.
 //   pool: the shared edge-clamped pool kernel (score.cu).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -194,37 +195,75 @@ score_exact_logits(const __grid_constant__ CUtensorMap tm_k, const __nv_bfloat16
             for (int b = 0; b < 4; ++b) acc[a][b] = 0ull;
         const uint8_t* kb = sm.k[st];
         const float* qb = &sm.q[lr0 * XA_QS];
-#pragma unroll 1
-        for (int c = 0; c < 16; ++c) {
-            // keys kg + 8 i, d columns c*8 .. c*8+7: SW128 chunk (c & 7) ^ (key & 7) = (c & 7) ^ kg
-            const uint8_t* kc = kb + (c >> 3) * XA_KHALF + kg * 128 + (((c & 7) ^ kg) << 4);
-            uint4 kw[8];
+        // 16 blocks of 8 d-columns.  K words (8 keys x 8 columns, 8 x LDS.128) and
+        // Q values (8 rows x 2 columns, 8 x LDS.64) for the next block / column
+        // pair are loaded one step ahead into a second register set, so the
+        // FFMA2 stream does not wait on LDS latency with two warps per scheduler.
+        // K chunk c of key (kg + 8 i) sits at SW128 position (c & 7) ^ kg:
+        // base ^ ((c & 7) << 4) with the kg bits pre-set (tiles are 1 KB aligned).
+        const uint32_t kbase = smem_u32(kb) + kg * 128 + (kg << 4);
+        const uint32_t qbase = smem_u32(qb);
+        auto kaddr = [&](int c) { return (kbase ^ ((c & 7) << 4)) + (c >> 3) * XA_KHALF; };
+        auto lds128 = [](uint32_t a) {
+            uint4 v;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+            return v;
+        };
+        auto lds64f = [](uint32_t a) {
+            float2 v;
+            asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+            return v;
+        };
+        auto load_k = [&](int c, uint4 (&kw)[8]) {
+            const uint32_t a = kaddr(c);
 #pragma unroll
-            for (int i8 = 0; i8 < 8; ++i8) kw[i8] = *reinterpret_cast<const uint4*>(kc + i8 * 1024);
+            for (int i8 = 0; i8 < 8; ++i8) kw[i8] = lds128(a + i8 * 1024);
+        };
+        auto load_q = [&](int p2, float2 (&qv)[8]) {  // columns 2 p2, 2 p2 + 1
 #pragma unroll
-            for (int sub = 0; sub < 2; ++sub) {
-                float4 qv[8];
+            for (int a = 0; a < 8; ++a) qv[a] = lds64f(qbase + (4 * a * XA_QS + 2 * p2) * 4);
+        };
+        auto fma_col = [&](const uint4 (&kw)[8], int p8, float q0, int a, uint64_t (&kp)[4]) {
+            (void)kw; (void)p8;
+            const uint64_t qq = f2(q0, q0);
 #pragma unroll
-                for (int a = 0; a < 8; ++a)
-                    qv[a] = *reinterpret_cast<const float4*>(qb + 4 * a * XA_QS + c * 8 + sub * 4);
+            for (int i2 = 0; i2 < 4; ++i2) acc[a][i2] = fma2(qq, kp[i2], acc[a][i2]);
+        };
+        auto pairs = [&](const uint4 (&kw)[8], int p8, uint64_t (&kp)[4]) {  // column p8 of the block
 #pragma unroll
-                for (int pp = 0; pp < 4; ++pp) {
-                    const int wi = sub * 2 + (pp >> 1);
-                    uint64_t kp[4];  // key pairs (kg + 16 i2, kg + 16 i2 + 8)
+            for (int i2 = 0; i2 < 4; ++i2) {
+                const uint32_t w0 = word(kw[2 * i2], p8 >> 1), w1 = word(kw[2 * i2 + 1], p8 >> 1);
+                kp[i2] = (p8 & 1) ? f2(bf16_hi(w0), bf16_hi(w1)) : f2(bf16_lo(w0), bf16_lo(w1));
+            }
+        };
+        auto block = [&](const uint4 (&kw)[8], float2 (&qA)[8], float2 (&qB)[8], int c,
+                         bool prefetch_next) {
+            // columns 8c .. 8c+7 as 4 column pairs; q pair j+1 loads while pair j computes
 #pragma unroll
-                    for (int i2 = 0; i2 < 4; ++i2) {
-                        const uint32_t w0 = word(kw[2 * i2], wi), w1 = word(kw[2 * i2 + 1], wi);
-                        kp[i2] = (pp & 1) ? f2(bf16_hi(w0), bf16_hi(w1)) : f2(bf16_lo(w0), bf16_lo(w1));
-                    }
+            for (int j = 0; j < 4; ++j) {
+                float2 (&cur)[8] = (j & 1) ? qB : qA;
+                float2 (&nxt)[8] = (j & 1) ? qA : qB;
+                if (j < 3 || prefetch_next) load_q(4 * c + j + 1, nxt);
 #pragma unroll
-                    for (int a = 0; a < 8; ++a) {
-                        const float qs = comp(qv[a], pp);
-                        const uint64_t qq = f2(qs, qs);
+                for (int e = 0; e < 2; ++e) {
+                    uint64_t kp[4];
+                    pairs(kw, 2 * j + e, kp);
 #pragma unroll
-                        for (int i2 = 0; i2 < 4; ++i2) acc[a][i2] = fma2(qq, kp[i2], acc[a][i2]);
-                    }
+                    for (int a = 0; a < 8; ++a) fma_col(kw, 2 * j + e, e ? cur[a].y : cur[a].x, a, kp);
                 }
             }
+        };
+        uint4 kwA[8], kwB[8];
+        float2 qA[8], qB[8];
+        load_k(0, kwA);
+        load_q(0, qA);
+#pragma unroll 1
+        for (int c = 0; c < 16; c += 2) {
+            load_k(c + 1, kwB);
+            block(kwA, qA, qB, c, true);
+            if (c + 2 < 16) load_k(c + 2, kwA);
+            block(kwB, qA, qB, c + 1, c + 2 < 16);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[st]);
@@ -259,31 +298,36 @@ score_exact_logits(const __grid_constant__ CUtensorMap tm_k, const __nv_bfloat16
 }
 
 // ------------------------------------------------------------------ XB
-constexpr int XB_ROWS = 16;
+// Rows per CTA are chosen at run time (<= 16, one chain lane each) so the
+// exponentials -- the bulk of this kernel's work -- spread over every SM.
+constexpr int XB_MAXR = 16;
 constexpr int XB_KEYS = 256;
 constexpr int XB_STAGES = 4;
-constexpr int XB_HELP = 8;                        // helper warps (2 rows each)
+constexpr int XB_HELP = 8;                        // helper warps: thread = key column
 constexpr int XB_THREADS = 32 * (XB_HELP + 1);    // + the summing warp
-constexpr int XB_EP = XB_ROWS + 1;                // e tile row pitch (conflict-free transpose)
+constexpr int XB_EP = XB_MAXR + 1;                // e tile row pitch (conflict-free transpose)
 
 struct __align__(128) XbSmem {
-    float x[XB_STAGES][XB_ROWS * XB_KEYS];
-    float e[XB_STAGES][XB_KEYS * XB_EP];
-    float m[XB_ROWS];
-    int allowed[XB_ROWS];
+    float x[XB_STAGES][XB_MAXR * XB_KEYS];        // X tile (TMA), rows x keys
+    float e[XB_STAGES][XB_KEYS * XB_EP];          // e tile, keys x rows
+    uint64_t tab[32];                             // glibc's exp2f table
+    float m[XB_MAXR];
+    int allowed[XB_MAXR];
     uint64_t x_full[XB_STAGES], x_empty[XB_STAGES], e_full[XB_STAGES], e_empty[XB_STAGES];
 };
 
 __global__ void __launch_bounds__(XB_THREADS, 1)
 score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int n_rows,
-                   const int* __restrict__ rowmax, float* __restrict__ rowsum) {
+                   int rows_per_cta, const int* __restrict__ rowmax, float* __restrict__ rowsum) {
     extern __shared__ uint8_t smem_raw[];
     XbSmem& sm = smem_view<XbSmem, 128>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int row0 = blockIdx.x * XB_ROWS;  // rows of X: (local head, r) flattened
-    if (tid < XB_ROWS) {
+    const int R = rows_per_cta;
+    const int row0 = blockIdx.x * R;  // rows of X: (local head, r) flattened
+    exp2f_table_to_smem(sm.tab);
+    if (tid < XB_MAXR) {
         const int gr = row0 + tid;
-        const bool ok = gr < n_rows;
+        const bool ok = tid < R && gr < n_rows;
         sm.m[tid] = ok ? dec_max(rowmax[gr]) : 0.0f;
         sm.allowed[tid] = ok ? L - lq + gr % lq + 1 : 0;
     }
@@ -301,33 +345,39 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int 
     auto issue = [&](int t) {
         const int st = t % XB_STAGES;
         if (t >= XB_STAGES) mbar_wait(&sm.x_empty[st], ((t / XB_STAGES) - 1) & 1);
-        mbar_arrive_expect_tx(&sm.x_full[st], XB_ROWS * XB_KEYS * 4);
+        mbar_arrive_expect_tx(&sm.x_full[st], R * XB_KEYS * 4);
         tma_load_2d(sm.x[st], &tm_x, &sm.x_full[st], t * XB_KEYS, row0);
     };
     if (warp < XB_HELP) {
         if (tid == 0)
             for (int t = 0; t < min(n_tiles, XB_STAGES - 1); ++t) issue(t);
-        const int ra = warp * 2;
+        // thread = key column j of the tile: XB_MAXR independent exponentials per
+        // tile, unconditionally (rows >= R are padding the chain never reads), so
+        // they interleave
+        const int j = tid;
+        float mrow[XB_MAXR];
+        int arow[XB_MAXR];
+#pragma unroll
+        for (int row = 0; row < XB_MAXR; ++row) {
+            mrow[row] = sm.m[row];
+            arow[row] = sm.allowed[row];
+        }
         for (int t = 0; t < n_tiles; ++t) {
             if (tid == 0 && t + XB_STAGES - 1 < n_tiles) issue(t + XB_STAGES - 1);
             const int st = t % XB_STAGES;
             mbar_wait(&sm.x_full[st], (t / XB_STAGES) & 1);
             if (t >= XB_STAGES) mbar_wait(&sm.e_empty[st], ((t / XB_STAGES) - 1) & 1);
-            const float* xs = sm.x[st];
-            float* es = sm.e[st];
+            const float* xs = sm.x[st] + j;
+            float* es = sm.e[st] + j * XB_EP;
+            const int key = t * XB_KEYS + j;
+            float xv[XB_MAXR];
 #pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                const int row = ra + rr;
-                const float m = sm.m[row];
-                const int allowed = sm.allowed[row];
+            for (int row = 0; row < XB_MAXR; ++row) xv[row] = xs[row * XB_KEYS];
 #pragma unroll
-                for (int e8 = 0; e8 < XB_KEYS / 32; ++e8) {
-                    const int j = lane + 32 * e8;
-                    const float x = xs[row * XB_KEYS + j];
-                    // masked entries add +0 to the chain: exactly the reference's skip
-                    const float v = t * XB_KEYS + j < allowed ? expf_glibc(__fsub_rn(x, m)) : 0.0f;
-                    es[j * XB_EP + row] = v;
-                }
+            for (int row = 0; row < XB_MAXR; ++row) {
+                // masked entries add +0 to the chain: exactly the reference's skip
+                const float e = expf_glibc(__fsub_rn(xv[row], mrow[row]), sm.tab);
+                es[row] = key < arow[row] ? e : 0.0f;
             }
             __syncwarp();
             if (lane == 0) {
@@ -337,18 +387,18 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int 
         }
     } else {
         // the sequential f32 row sums, lane = row (tensor_ops.cpp:59-65)
-        const int row = lane & (XB_ROWS - 1);
+        const int row = lane & (XB_MAXR - 1);
         float s = 0.0f;
         for (int t = 0; t < n_tiles; ++t) {
             const int st = t % XB_STAGES;
             mbar_wait(&sm.e_full[st], (t / XB_STAGES) & 1);
             const float* es = sm.e[st] + row;
-#pragma unroll 16
+#pragma unroll
             for (int j = 0; j < XB_KEYS; ++j) s = __fadd_rn(s, es[j * XB_EP]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.e_empty[st]);
         }
-        if (lane < XB_ROWS && row0 + lane < n_rows) rowsum[row0 + lane] = s;
+        if (lane < R && row0 + lane < n_rows) rowsum[row0 + lane] = s;
     }
 }
 
@@ -358,37 +408,100 @@ __global__ void fill_int(int* __restrict__ p, int v, int n) {
 }
 
 // ------------------------------------------------------------------ XC
-constexpr int XC_T = 256;
+constexpr int XC_KEYS = 128;   // keys per CTA (thread = key)
+constexpr int XC_ROWS = 64;    // rows per TMA chunk
+constexpr int XC_STAGES = 2;
 
-__global__ void __launch_bounds__(XC_T)
-score_exact_colsum(const float* __restrict__ X, int L, int Lp, int lq, int head_begin,
+// e / sum, correctly rounded, from y = RN(1/sum): q = RN(e y), r = e - q sum
+// (exact, FMA), RN(q + r y) = RN(e / sum) (Markstein) -- valid while the
+// quotient is normal (e >= 2^-100 > 2^-126 * sum for sum <= 2^26).
+__device__ __forceinline__ float div_rn(float e, float sum, float y) {
+    const float q = __fmul_rn(e, y);
+    const float r = __fmaf_rn(-q, sum, e);
+    const float q1 = __fmaf_rn(r, y, q);
+    return e >= 0x1p-100f ? q1 : __fdiv_rn(e, sum);
+}
+
+// shared memory: [XcHead][rs: lq x float4][n_st x X chunk (32 KB)]
+struct __align__(128) XcHead {
+    uint64_t tab[32];
+    uint64_t full[XC_STAGES];
+};
+__host__ __device__ constexpr int xc_rs_bytes(int lq) { return (lq * 16 + 127) / 128 * 128; }
+
+// c[j] = sum over r (ascending) of expf(X[r, j] - m_r) / sum_r.  e is
+// recomputed from X (cheaper than writing it back and reading it again); X
+// chunks [64 rows x 128 keys] arrive by TMA, so many loads are in flight
+// without registers.
+__global__ void __launch_bounds__(XC_KEYS)
+score_exact_colsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int head_begin,
                    const int* __restrict__ rowmax, const float* __restrict__ rowsum,
                    float* __restrict__ colraw) {
-    extern __shared__ float st[];  // m[lq], sum[lq]
+    extern __shared__ uint8_t smem_raw[];
+    XcHead& sm = smem_view<XcHead, 128>(smem_raw);
+    float4* rs = reinterpret_cast<float4*>(&sm + 1);  // per row: m, sum, RN(1/sum)
+    float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(rs) + xc_rs_bytes(lq));
+    const int tid = threadIdx.x;
     const int hl = blockIdx.y;
-    for (int r = threadIdx.x; r < lq; r += XC_T) {
-        st[r] = dec_max(rowmax[hl * lq + r]);
-        st[lq + r] = rowsum[hl * lq + r];
+    const int k0 = blockIdx.x * XC_KEYS;
+    const int n_chunks = (lq + XC_ROWS - 1) / XC_ROWS;
+    const int n_st = min(n_chunks, XC_STAGES);
+    const int row_base = hl * lq;
+    if (tid == 0) {
+        for (int s = 0; s < XC_STAGES; ++s) mbar_init(&sm.full[s], 1);
+        fence_barrier_init();
+        for (int c = 0; c < n_st; ++c) {
+            mbar_arrive_expect_tx(&sm.full[c], XC_ROWS * XC_KEYS * 4);
+            tma_load_2d(xbuf + c * XC_ROWS * XC_KEYS, &tm_x, &sm.full[c], k0, row_base + c * XC_ROWS);
+        }
+    }
+    exp2f_table_to_smem(sm.tab);
+    for (int r = tid; r < lq; r += XC_KEYS) {
+        const float sum = rowsum[row_base + r];
+        rs[r] = make_float4(dec_max(rowmax[row_base + r]), sum, __frcp_rn(sum), 0.0f);
     }
     __syncthreads();
-    const int j = blockIdx.x * XC_T + threadIdx.x;
-    if (j >= L) return;
-    const float* x = X + (size_t)hl * lq * Lp + j;
+    const int j = k0 + tid;
     // row r sees key j iff j <= L - lq + r (token_coverage.cpp:36-41)
     const int r_first = max(0, j - (L - lq));
     float c = 0.0f;
-#pragma unroll 8
-    for (int r = r_first; r < lq; ++r) {
-        const float e = expf_glibc(__fsub_rn(x[(size_t)r * Lp], st[r]));
-        c = __fadd_rn(c, __fdiv_rn(e, st[lq + r]));
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        const int st = ch % n_st;
+        mbar_wait(&sm.full[st], (ch / n_st) & 1);
+        const float* xs = xbuf + st * XC_ROWS * XC_KEYS + tid;
+        const int r0 = ch * XC_ROWS;
+        const int rn = min(XC_ROWS, lq - r0);
+        if (r_first <= r0 && rn == XC_ROWS) {  // every row of the chunk sees the key
+#pragma unroll 16
+            for (int i = 0; i < XC_ROWS; ++i) {
+                const float4 w = rs[r0 + i];
+                const float e = expf_glibc(__fsub_rn(xs[i * XC_KEYS], w.x), sm.tab);
+                c = __fadd_rn(c, div_rn(e, w.y, w.z));
+            }
+        } else {
+            for (int i = max(0, r_first - r0); i < rn; ++i) {
+                const float4 w = rs[r0 + i];
+                const float e = expf_glibc(__fsub_rn(xs[i * XC_KEYS], w.x), sm.tab);
+                c = __fadd_rn(c, div_rn(e, w.y, w.z));
+            }
+        }
+        __syncthreads();  // the stage is refilled below
+        if (tid == 0 && ch + n_st < n_chunks) {
+            mbar_arrive_expect_tx(&sm.full[st], XC_ROWS * XC_KEYS * 4);
+            tma_load_2d(xbuf + st * XC_ROWS * XC_KEYS, &tm_x, &sm.full[st], k0,
+                        row_base + (ch + n_st) * XC_ROWS);
+        }
     }
-    colraw[(size_t)(head_begin + hl) * L + j] = c;
+    if (j < L) colraw[(size_t)(head_begin + hl) * L + j] = c;
 }
 
 __global__ void expf_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n) {
+    __shared__ uint64_t tab[32];
+    exp2f_table_to_smem(tab);
+    __syncthreads();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        y[i] = expf_glibc(x[i]);
+        y[i] = expf_glibc(x[i], tab);
 }
 
 }  // namespace
@@ -425,12 +538,14 @@ int launch_score_exact(const tsa_desc& d, const void* q, const void* k, const Ou
     int rc;
     if ((rc = make_bf16_map_2d(&mk, kb, (uint64_t)n_kv * L, XA_KEYS))) return rc;
     const int n_rows = nh * lq;
+    const int nsm = num_sms();
+    // rows per row-sum CTA: spread the rows over every SM (<= 16: one chain lane each)
+    const int rpc = std::min(XB_MAXR, std::max(1, (n_rows + nsm - 1) / nsm));
     if ((rc = make_f32_map_2d(&mx, X, (uint64_t)Lp, (uint64_t)n_rows, (uint64_t)Lp * 4, XB_KEYS,
-                              XB_ROWS)))
+                              (uint32_t)rpc)))
         return rc;
     fill_int<<<(n_rows + 255) / 256, 256, 0, st>>>(rowmax, INT_MIN, n_rows);  // below every encoding
     TSA_LAUNCH_CHECK("score_exact_fill");
-    const int nsm = num_sms();
     {
         const int smem = (int)sizeof(XaSmem) + 1024;
         if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(score_exact_logits), smem))) return rc;
@@ -444,14 +559,21 @@ int launch_score_exact(const tsa_desc& d, const void* q, const void* k, const Ou
     {
         const int smem = (int)sizeof(XbSmem) + 128;
         if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(score_exact_rowsum), smem))) return rc;
-        score_exact_rowsum<<<(n_rows + XB_ROWS - 1) / XB_ROWS, XB_THREADS, smem, st>>>(
-            mx, L, lq, n_rows, rowmax, rowsum);
+        score_exact_rowsum<<<(n_rows + rpc - 1) / rpc, XB_THREADS, smem, st>>>(
+            mx, L, lq, n_rows, rpc, rowmax, rowsum);
         TSA_LAUNCH_CHECK("score_exact_rowsum");
     }
     {
-        dim3 grid((L + XC_T - 1) / XC_T, nh);
-        score_exact_colsum<<<grid, XC_T, sizeof(float) * 2 * lq, st>>>(X, L, Lp, lq, d.head_begin,
-                                                                         rowmax, rowsum, colraw);
+        CUtensorMap mxc;
+        if ((rc = make_f32_map_2d(&mxc, X, (uint64_t)Lp, (uint64_t)n_rows, (uint64_t)Lp * 4,
+                                  XC_KEYS, XC_ROWS)))
+            return rc;
+        const int n_st = std::min((lq + XC_ROWS - 1) / XC_ROWS, XC_STAGES);
+        const int smem = (int)sizeof(XcHead) + 128 + xc_rs_bytes(lq) + n_st * XC_ROWS * XC_KEYS * 4;
+        if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(score_exact_colsum), smem))) return rc;
+        dim3 grid((L + XC_KEYS - 1) / XC_KEYS, nh);
+        score_exact_colsum<<<grid, XC_KEYS, smem, st>>>(mxc, L, lq, d.head_begin, rowmax, rowsum,
+                                                         colraw);
         TSA_LAUNCH_CHECK("score_exact_colsum");
     }
     tsa_desc pd = d;

@@ -1,65 +1,42 @@
-"""Condense an ncu --set full report into the metrics the roofline uses."""
+"""Summarise an ncu report: per kernel duration, pipe utilisation, stalls,
+DRAM bytes.  python tools/ncu_summary.py report.ncu-rep [kernel-regex]"""
 import csv
 import io
-import json
+import re
 import subprocess
 import sys
 
-METRICS = [
-    ("gpu__time_duration.sum", "duration"),
-    ("dram__bytes_read.sum", "dram_read"),
-    ("dram__bytes_write.sum", "dram_write"),
-    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
-    ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor_pipe_pct"),
-    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "xu_pct"),
-    ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue_pct"),
-    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_pct"),
-    ("lts__t_sector_hit_rate.pct", "l2_hit_pct"),
-    ("launch__registers_per_thread", "regs"),
-    ("launch__grid_size", "grid"),
-]
-
-
-def num(v):
-    return v if isinstance(v, float) else 0.0
-
-
-def main(rep, out_json):
-    if rep.endswith(".csv"):  # a saved `ncu -i ... --page raw --csv` dump
-        raw = open(rep).read()
-    else:
-        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                             text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units = rows[0], rows[1]
-    res = {}
-    for r in rows[2:]:
-        name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
-        name = name.replace("(anonymous namespace)::", "").replace("tsa::", "")
-        d = {}
-        for m, short in METRICS:
-            col = next((i for i, h in enumerate(hdr) if h == m or h.endswith("." + m)), None)
-            if col is not None:
-                v = r[col].replace(",", "")
-                try:
-                    v = float(v)
-                except ValueError:
-                    pass
-                d[short] = v
-                d[short + "_unit"] = units[col]
-        res[name] = d
-    print(f"{'kernel':40s} {'ms':>8s} {'DRAM GB':>8s} {'dram%':>6s} {'tensor%':>7s} {'xu%':>5s} {'issue%':>6s}")
-    for k, d in res.items():
-        scale = {"ms": 1, "us": 1e-3, "ns": 1e-6, "usecond": 1e-3, "msecond": 1}.get(d.get("duration_unit"), 1)
-        gb = {"Gbyte": 1, "Mbyte": 1e-3, "Kbyte": 1e-6, "byte": 1e-9}
-        rd = num(d.get("dram_read", 0)) * gb.get(d.get("dram_read_unit"), 1)
-        wr = num(d.get("dram_write", 0)) * gb.get(d.get("dram_write_unit"), 1)
-        d["dram_GB_per_launch"] = round(rd + wr, 4)
-        print(f"{k[:40]:40s} {num(d.get('duration', 0)) * scale:8.3f} {rd + wr:8.3f} "
-              f"{num(d.get('dram_pct', 0)):6.1f} {num(d.get('tensor_pipe_pct', 0)):7.1f} "
-              f"{num(d.get('xu_pct', 0)):5.1f} {num(d.get('issue_pct', 0)):6.1f}")
-    json.dump(res, open(out_json, "w"), indent=1)
-
-
-if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+rep = sys.argv[1]
+pat = re.compile(sys.argv[2]) if len(sys.argv) > 2 else None
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr = rows[0]
+KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__instruction_throughput.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size"]
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    name = d.get("Kernel Name", "")
+    if pat and not pat.search(name):
+        continue
+    print("==", name[:90])
+    for k in KEYS:
+        if k in d:
+            print(f"   {k:70s} {d[k]}")
+    st = {k: d[k] for k in d if k.startswith("smsp__average_warps_issue_stalled") and
+          k.endswith("per_issue_active.ratio")}
+    top = sorted(st.items(), key=lambda kv: -float(kv[1] or 0))[:6]
+    print("   stalls:", ", ".join(f"{k.split('stalled_')[1].split('_per')[0]}={float(v):.2f}"
+                                   for k, v in top))
