@@ -302,18 +302,19 @@ score_exact_logits(const __grid_constant__ CUtensorMap tm_k, const __nv_bfloat16
 // exponentials -- the bulk of this kernel's work -- spread over every SM.
 constexpr int XB_MAXR = 16;
 constexpr int XB_KEYS = 256;
-constexpr int XB_STAGES = 4;
-constexpr int XB_HELP = 8;                        // helper warps: thread = key column
+constexpr int XB_STAGES = 4;                      // e tiles in flight
+constexpr int XB_XST = 8;                         // X tiles in flight (HBM latency x bandwidth)
+constexpr int XB_HELP = 16;                       // helper warps: thread = (key, half of the rows)
 constexpr int XB_THREADS = 32 * (XB_HELP + 1);    // + the summing warp
 constexpr int XB_EP = XB_MAXR + 1;                // e tile row pitch (conflict-free transpose)
 
 struct __align__(128) XbSmem {
-    float x[XB_STAGES][XB_MAXR * XB_KEYS];        // X tile (TMA), rows x keys
+    float x[XB_XST][XB_MAXR * XB_KEYS];           // X tile (TMA), rows x keys
     float e[XB_STAGES][XB_KEYS * XB_EP];          // e tile, keys x rows
     uint64_t tab[32];                             // glibc's exp2f table
     float m[XB_MAXR];
     int allowed[XB_MAXR];
-    uint64_t x_full[XB_STAGES], x_empty[XB_STAGES], e_full[XB_STAGES], e_empty[XB_STAGES];
+    uint64_t x_full[XB_XST], x_empty[XB_XST], e_full[XB_STAGES], e_empty[XB_STAGES];
 };
 
 __global__ void __launch_bounds__(XB_THREADS, 1)
@@ -332,9 +333,11 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int 
         sm.allowed[tid] = ok ? L - lq + gr % lq + 1 : 0;
     }
     if (tid == 0) {
-        for (int s = 0; s < XB_STAGES; ++s) {
+        for (int s = 0; s < XB_XST; ++s) {
             mbar_init(&sm.x_full[s], 1);
             mbar_init(&sm.x_empty[s], XB_HELP);
+        }
+        for (int s = 0; s < XB_STAGES; ++s) {
             mbar_init(&sm.e_full[s], XB_HELP);
             mbar_init(&sm.e_empty[s], 1);
         }
@@ -343,45 +346,46 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int 
     __syncthreads();
     const int n_tiles = (L + XB_KEYS - 1) / XB_KEYS;
     auto issue = [&](int t) {
-        const int st = t % XB_STAGES;
-        if (t >= XB_STAGES) mbar_wait(&sm.x_empty[st], ((t / XB_STAGES) - 1) & 1);
+        const int st = t % XB_XST;
+        if (t >= XB_XST) mbar_wait(&sm.x_empty[st], ((t / XB_XST) - 1) & 1);
         mbar_arrive_expect_tx(&sm.x_full[st], R * XB_KEYS * 4);
         tma_load_2d(sm.x[st], &tm_x, &sm.x_full[st], t * XB_KEYS, row0);
     };
     if (warp < XB_HELP) {
         if (tid == 0)
-            for (int t = 0; t < min(n_tiles, XB_STAGES - 1); ++t) issue(t);
+            for (int t = 0; t < min(n_tiles, XB_XST - 1); ++t) issue(t);
         // thread = key column j of the tile: XB_MAXR independent exponentials per
         // tile, unconditionally (rows >= R are padding the chain never reads), so
         // they interleave
-        const int j = tid;
-        float mrow[XB_MAXR];
-        int arow[XB_MAXR];
+        constexpr int RH = XB_MAXR / 2;
+        const int j = tid & (XB_KEYS - 1), rbase = (tid / XB_KEYS) * RH;
+        float mrow[RH];
+        int arow[RH];
 #pragma unroll
-        for (int row = 0; row < XB_MAXR; ++row) {
-            mrow[row] = sm.m[row];
-            arow[row] = sm.allowed[row];
+        for (int i = 0; i < RH; ++i) {
+            mrow[i] = sm.m[rbase + i];
+            arow[i] = sm.allowed[rbase + i];
         }
         for (int t = 0; t < n_tiles; ++t) {
-            if (tid == 0 && t + XB_STAGES - 1 < n_tiles) issue(t + XB_STAGES - 1);
-            const int st = t % XB_STAGES;
-            mbar_wait(&sm.x_full[st], (t / XB_STAGES) & 1);
+            if (tid == 0 && t + XB_XST - 1 < n_tiles) issue(t + XB_XST - 1);
+            const int xt = t % XB_XST, st = t % XB_STAGES;
+            mbar_wait(&sm.x_full[xt], (t / XB_XST) & 1);
             if (t >= XB_STAGES) mbar_wait(&sm.e_empty[st], ((t / XB_STAGES) - 1) & 1);
-            const float* xs = sm.x[st] + j;
-            float* es = sm.e[st] + j * XB_EP;
+            const float* xs = sm.x[xt] + rbase * XB_KEYS + j;
+            float* es = sm.e[st] + j * XB_EP + rbase;
             const int key = t * XB_KEYS + j;
-            float xv[XB_MAXR];
+            float xv[RH];
 #pragma unroll
-            for (int row = 0; row < XB_MAXR; ++row) xv[row] = xs[row * XB_KEYS];
+            for (int i = 0; i < RH; ++i) xv[i] = xs[i * XB_KEYS];
 #pragma unroll
-            for (int row = 0; row < XB_MAXR; ++row) {
+            for (int i = 0; i < RH; ++i) {
                 // masked entries add +0 to the chain: exactly the reference's skip
-                const float e = expf_glibc(__fsub_rn(xv[row], mrow[row]), sm.tab);
-                es[row] = key < arow[row] ? e : 0.0f;
+                const float e = expf_glibc(__fsub_rn(xv[i], mrow[i]), sm.tab);
+                es[i] = key < arow[i] ? e : 0.0f;
             }
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&sm.x_empty[st]);
+                mbar_arrive(&sm.x_empty[xt]);
                 mbar_arrive(&sm.e_full[st]);
             }
         }
@@ -393,8 +397,22 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int 
             const int st = t % XB_STAGES;
             mbar_wait(&sm.e_full[st], (t / XB_STAGES) & 1);
             const float* es = sm.e[st] + row;
+            // the next 32 values load while the current 32 are added (the loads
+            // stay off the FADD chain)
+            float cur[32], nxt[32];
 #pragma unroll
-            for (int j = 0; j < XB_KEYS; ++j) s = __fadd_rn(s, es[j * XB_EP]);
+            for (int i = 0; i < 32; ++i) cur[i] = es[i * XB_EP];
+#pragma unroll
+            for (int c = 0; c < XB_KEYS / 32; ++c) {
+                if (c + 1 < XB_KEYS / 32) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) nxt[i] = es[((c + 1) * 32 + i) * XB_EP];
+                }
+#pragma unroll
+                for (int i = 0; i < 32; ++i) s = __fadd_rn(s, cur[i]);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) cur[i] = nxt[i];
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.e_empty[st]);
         }
