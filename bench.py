@@ -55,7 +55,10 @@ def parse():
     p.add_argument("--sweep", type=str, default="0,0.005,0.008,0.01,0.02",
                    help="extra tau levels reported in tau_sweep (comma list, '' = none)")
     p.add_argument("--sigma", type=float, default=None)
-    p.add_argument("--scoring", type=int, default=0, help="0 default, 1 reference-order, 2 fast")
+    p.add_argument("--scoring", type=int, default=0,
+                   help="0 default (= 1), 1 reference order (bit-exact scores), 2 fast")
+    p.add_argument("--no-fast", action="store_true", help="skip the FAST-scoring comparison")
+    p.add_argument("--no-parity", action="store_true", help="skip the oracle parity check")
     p.add_argument("--c2", choices=["auto", "nccl", "peer"], default="auto",
                    help="multi-GPU output exchange: peer-memory stores fused into the kernels "
                         "(auto: when the CUDA IPC peer mapping can be set up) or an NCCL all-gather")
@@ -363,6 +366,32 @@ def run_ours(args):
                                  device)
         torch.cuda.empty_cache()
 
+    # the FAST (tensor-core, approximate-exponential) scoring of the same step, for
+    # comparison: latency and parity; the headline uses the default (exact) scoring
+    fast = None
+    if args.scoring != 2 and not args.no_fast:
+        fast_layer = ShardedSparseAttention(Hq, Hk, L, D, torch.bfloat16,
+                                            tsa.SparsePlan(mode=tsa.SparseMode.kDynamic,
+                                                           sparse_layers=[0], tau=args.tau),
+                                            rank=rank, world=world, device=device, scoring=2,
+                                            c2=args.c2 if world > 1 else "auto")
+        fast_ms, _, _ = timed(fast_layer, args.steps, args.warmup, graph=True)
+        fast = {"scoring": "FAST (tcgen05 logits, ex2.approx + polynomial exponentials)",
+                "ms": round(fast_ms, 3), "k_keep": fast_layer.k_keep,
+                "speedup_vs_dense": round(dense_ms / fast_ms, 3) if dense_ms else None}
+    parity = None
+    if rank == 0 and world == 1 and not args.no_parity:
+        mode_name = {0: "REFERENCE (default: exact f32 order)", 1: "REFERENCE (exact f32 order)",
+                     2: "FAST"}[args.scoring]
+        layers = {"headline": (layer, mode_name)}
+        if fast:
+            layers["fast"] = (fast_layer, fast["scoring"])
+        parity = parity_check(tsa, q, k, v, layers, L, Hq, args.tau)
+    if fast:
+        fast_layer.release()
+        del fast_layer
+        torch.cuda.empty_cache()
+
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, tsa, ql, kl, vl, rank, world, device, args.tau, layer=layer)
@@ -394,6 +423,11 @@ def run_ours(args):
             "stages_ms": {kk: round(vv, 4) for kk, vv in stages.items()},
             "hbm_stages": hbm_rows, "roofline": roofline,
             "kernel_rooflines": kernel_rooflines(stages, sh.h_per, sh.kv_per, L, k_keep),
+            "scoring": {0: "REFERENCE (default): the reference's f32 operation order, bit-exact "
+                           "scores (exact-order FFMA2 logits, glibc expf port, sequential "
+                           "sums)", 1: "REFERENCE (exact f32 order)",
+                        2: "FAST (tcgen05 logits, approximate exponentials)"}[args.scoring],
+            "fast_scoring": fast, "parity": parity,
             "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
             "other_configs": extras,
@@ -687,6 +721,69 @@ def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau, layer=None):
                     "sparse_attention_layer_host (tsa_sparse_attention_layer_host): H2D of K and "
                     "the Q tails, then V and Q by head group (first and last group head by "
                     "head), and D2H of each finished chunk overlap the compute")}
+
+
+# ------------------------------------------------------------ parity check
+def parity_check(tsa, q, k, v, layers, L, H, tau):
+    """Checker (outside every timed region): the benchmarked selections and
+    outputs against the CPU oracle (oracle/tsa_oracle.c, pinned bit-exact to the
+    reference compiled from its sources) on the same inputs.  For each scoring
+    mode: score bits identical, k_keep vs the reference's, index sets at the
+    REFERENCE's k_keep (heads / tokens differing and the largest relative gap of
+    a differing token's oracle score to that head's threshold), and the output
+    deviation (rel_l2, bench.cpp:199-214) of sampled rows against the oracle run
+    with the reference's own selection."""
+    from oracle.oracle import Oracle, n_threads_default
+    port = Oracle("port")
+    T = n_threads_default()
+    t0 = time.perf_counter()
+    qn, kn = q.float().cpu().numpy(), k.float().cpu().numpy()
+    s_ref = port.score_tokens(qn, kn, 64, 7, n_threads=T)
+    k_ref = port.coverage_budget(port.aggregate_scores(s_ref), tau, 1)
+    idx_ref = port.select_tokens(s_ref, k_ref, [L - 1], n_threads=T)
+    # sampled output rows: the last 256 compressed rows (the costliest, at the end
+    # of the causal range) of heads 0 and H/2, attention over the reference's selection
+    hs = (0, H // 2)
+    ref_out = port.token_sparse_attention_sampled(qn, kn, v.float().cpu().numpy(), idx_ref,
+                                                  head_stride=H // 2, r0=k_ref - 256, r1=k_ref,
+                                                  n_threads=T)
+    out = {"reference": "oracle port (bit-exact to the compiled reference, tests/test_oracle.py)",
+           "k_keep_reference": int(k_ref), "checker_s": None}
+    bits = lambda a: np.ascontiguousarray(a, np.float32).view(np.uint32)
+    for name, (layer, scoring) in layers.items():
+        o = layer.step(q, k, v)  # fresh sparse step (the bench ran dense / sweeps since)
+        torch.cuda.synchronize()
+        s_gpu = layer.s_full.float().cpu().numpy()
+        k_gpu = layer.k_keep
+        if k_gpu == k_ref:
+            idx_gpu = layer.backend.idx[:, :k_ref].cpu().numpy()
+        else:  # the mode's scores selected at the reference's budget
+            idx_gpu = tsa.select_tokens(tsa.HeadScores(layer.s_full), k_ref, [L - 1]).indices
+            idx_gpu = idx_gpu.cpu().numpy()
+        heads_diff, tok_diff, max_gap = 0, 0, 0.0
+        for h in range(H):
+            a, b = set(idx_gpu[h].tolist()), set(idx_ref[h].tolist())
+            if a == b:
+                continue
+            heads_diff += 1
+            d = a ^ b
+            tok_diff += len(d)
+            thr = min(float(s_ref[h, t]) for t in b if t != L - 1)
+            max_gap = max(max_gap, max(abs(float(s_ref[h, t]) - thr) / thr for t in d))
+        dev = []
+        for h in hs:
+            rows = idx_ref[h, k_ref - 256:k_ref]
+            g = o[h][torch.from_numpy(rows).to(o.device).long()].float().cpu().numpy()
+            r = ref_out[h][rows]
+            dev.append(float(np.sqrt(((g - r) ** 2).sum() / (r ** 2).sum())))
+        out[name] = {"scoring": scoring, "k_keep": int(k_gpu),
+                     "scores_bit_identical": round(float(np.mean(bits(s_gpu) == bits(s_ref))), 6),
+                     "heads_differing": heads_diff, "tokens_differing": tok_diff,
+                     "max_rel_gap_of_differing_tokens": max_gap,
+                     "out_rel_l2_vs_reference_selection": max(dev),
+                     "out_rows_checked": f"heads {list(hs)}, compressed rows [k-256, k)"}
+    out["checker_s"] = round(time.perf_counter() - t0, 1)
+    return out
 
 
 # ----------------------------------------------------------- CPU baselines

@@ -54,7 +54,7 @@ enum tsa_status { TSA_OK = 0, TSA_ERR_INVALID = 1, TSA_ERR_CUDA = 2 };
  * sums; bf16 d = 128 runs the fused kernels of score_exact.cu); FAST runs
  * Q K^T on the tensor cores with approximate exponentials (bf16 only; scores
  * within ~1e-5 relative, so k_keep / index sets may differ at near ties).
- * DEFAULT = REFERENCE for f32, FAST for bf16. */
+ * DEFAULT = REFERENCE. */
 enum tsa_scoring { TSA_SCORING_DEFAULT = 0, TSA_SCORING_REFERENCE = 1, TSA_SCORING_FAST = 2 };
 
 /* One attention layer's geometry plus the SparsePlan parameters

@@ -109,10 +109,10 @@ size_t score_fast_rowstat_bytes(const tsa_desc& d);
 bool score_exact_supported(const tsa_desc& d);
 size_t exact_logits_stride(int L);
 
+// DEFAULT is the reference's arithmetic (bit-exact scores, hence the
+// reference's k_keep and index sets); FAST only on request.
 inline int scoring_mode(const tsa_desc& d) {
-    if (d.scoring == TSA_SCORING_DEFAULT)
-        return score_fast_supported(d) ? TSA_SCORING_FAST : TSA_SCORING_REFERENCE;
-    return d.scoring;
+    return d.scoring == TSA_SCORING_DEFAULT ? TSA_SCORING_REFERENCE : d.scoring;
 }
 
 // --------------------------------------------------------------- launchers

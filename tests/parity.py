@@ -1,10 +1,16 @@
 """Parity rules between the CUDA path and the CPU oracle.
 
 * index sets: identical, except a head may differ at tokens whose oracle
-  score lies within NEAR_TIE_ULPS ulp of that head's selection threshold
-  (the smallest kept non-forced oracle score);
+  score lies within NEAR_TIE_ULPS (4) ulp of that head's selection threshold
+  (the smallest kept non-forced oracle score) -- with the default (exact)
+  scoring the GPU scores are bit-identical, so the sets are identical;
 * k_keep: identical, except when the oracle's double prefix at the budget
-  boundary lies within BUDGET_REL of tau (then +-1 per boundary crossing);
+  boundary lies within L * 2^-53 of tau (the double accumulation's error
+  bound over L terms; the GPU sums exact 2^-62 fixed-point masses);
+* FAST scoring (opt-in): scores within FAST_SCORE_REL relative, k_keep within
+  FAST_BUDGET_REL * L, index sets at the reference's k_keep identical except
+  tokens within FAST_SCORE_REL of the threshold (the approximation's measured
+  error bound, not an fp32 near tie);
 * outputs: f32 max |d| <= 1e-5 (bench.cpp:27); bf16 rel_l2 <= 1e-2
   (bench.cpp:199-214) on the oracle run with the same index sets, and
   unselected rows bitwise +0.0.
@@ -13,8 +19,7 @@ from __future__ import annotations
 
 import numpy as np
 
-NEAR_TIE_ULPS = 8
-BUDGET_REL = 1e-5
+NEAR_TIE_ULPS = 4
 # FAST (tensor-core) scoring: bf16 products are exact, but f32 accumulation
 # order, ex2.approx and the tile-wise softmax normalisation move scores by up
 # to ~1e-5 relative; near ties are judged at this relative width instead.
@@ -50,10 +55,11 @@ def check_index_sets(gpu_idx, ora_idx, ora_scores, forced, rel_tol=None):
     return diffs
 
 
-def check_budget(k_gpu, k_ora, prefix_prev, prefix_at, tau):
+def check_budget(k_gpu, k_ora, prefix_prev, prefix_at, tau, L=None):
     if k_gpu == k_ora:
         return True
-    near = min(abs(prefix_at - tau), abs(tau - prefix_prev)) <= BUDGET_REL * max(tau, 1e-30)
+    n = L if L is not None else 1 << 20
+    near = min(abs(prefix_at - tau), abs(tau - prefix_prev)) <= n * 2.0 ** -53
     assert near and abs(k_gpu - k_ora) <= 2, (
         f"k_keep {k_gpu} vs oracle {k_ora}; boundary prefix {prefix_prev!r}..{prefix_at!r}, "
         f"tau {tau}")
