@@ -2,7 +2,10 @@
 python tools/ncu_times.py log.csv [regex]"""
 import csv
 import re
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 
 pat = re.compile(sys.argv[2]) if len(sys.argv) > 2 else None
 hdr = None
