@@ -235,6 +235,10 @@ def run_ours(args):
         if shared:
             dist.init_process_group("gloo")
         else:
+            # NCCL's init lines (rank, device, transport) on stderr, beside the JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=device)
     L, Hq, Hk = args.seq_len, args.heads, args.kv_heads
     sigma = args.sigma if args.sigma is not None else workloads.DEFAULT_SIGMA
@@ -281,7 +285,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier(world)
         launches = lib.tsa_kernel_launches() - launches0
-        if graph and obj.shard.world == 1:  # replays bypass the library's counter
+        if graph and getattr(obj, "graph_kernels", None):  # replays bypass the library's counter
             launches = obj.graph_kernels * steps
         total = start.elapsed_time(end)
         stages = {}
@@ -412,6 +416,9 @@ def run_ours(args):
                        "sigma": sigma, "last_q": 64, "kernel": 7, "forced": "final_token",
                        "parallelism": f"head-parallel x{world}",
                        "c2": (layer.c2 if world > 1 else None),
+                       "c2_entry": (getattr(layer, "_c_form", None) if world > 1 else None),
+                       "peer_access": (getattr(getattr(layer, "_peer", None), "peer_access", None)
+                                       if world > 1 else None),
                        **({"c2_fallback": layer.c2_error} if getattr(layer, "c2_error", None)
                           else {}),
                        "l2": "inputs (1.5 GiB) larger than L2; no flush"},

@@ -48,7 +48,7 @@ enum tsa_dtype { TSA_F32 = 0, TSA_BF16 = 1 };
 enum tsa_mode { TSA_MODE_DENSE = 0, TSA_MODE_DYNAMIC = 1, TSA_MODE_FIXED = 2 };
 /* ForcedPolicy, model.hpp:54 */
 enum tsa_forced_policy { TSA_FORCED_FINAL_TOKEN = 0, TSA_FORCED_RECENT_WINDOW = 1 };
-enum tsa_status { TSA_OK = 0, TSA_ERR_INVALID = 1, TSA_ERR_CUDA = 2 };
+enum tsa_status { TSA_OK = 0, TSA_ERR_INVALID = 1, TSA_ERR_CUDA = 2, TSA_ERR_NCCL = 3 };
 /* Scoring arithmetic: REFERENCE reproduces the reference's f32 operation
  * order bit for bit (sequential-order logits, glibc's expf, sequential softmax
  * sums; bf16 d = 128 runs the fused kernels of score_exact.cu); FAST runs
@@ -199,12 +199,19 @@ TSA_API int tsa_attend_indexed_replicas(const tsa_desc* d, const void* q, const 
 /* Peer memory for those exchanges (CUDA IPC): tsa_ipc_alloc returns a zeroed
  * device buffer and its 64-byte handle, which the other ranks map with
  * tsa_ipc_open (over NVLink between GPUs; ranks sharing a device work too).
- * tsa_peer_barrier is a cross-rank barrier on the stream: signals[r] is rank
- * r's int32 [world] slot array (this rank's own and the mapped peers'); the
- * call stores `epoch` into slot [rank] of every array (system-scope release,
- * after a system fence) and waits until this rank's array holds >= epoch in
- * every slot (acquire).  epoch starts at 1 and grows by one per call on the
- * same arrays; a peer that never arrives traps after 60 s. */
+ * tsa_peer_barrier is a cross-rank barrier on the stream over one channel's
+ * signal arrays: signals[r] is rank r's int32 [world + 2] array (this rank's
+ * own and the mapped peers'; zeroed before first use): slots [0, world) take
+ * the arrivals, [world] is the rank's epoch counter, [world + 1] a timeout
+ * flag.  With epoch < 1 the epoch is the device counter + 1 (graph-capturable:
+ * every rank runs the same barrier sequence); epoch >= 1 uses the host's value.
+ * The call stores the epoch into slot [rank] of every array (system-scope
+ * release, after a system fence) and waits until this rank's array holds >=
+ * epoch in every slot (acquire).  A peer that has not arrived within
+ * TSA_PEER_TIMEOUT_S seconds (environment, default 600 -- NCCL's) sets the
+ * timeout flag and the barrier returns instead of trapping; tsa_peer_check
+ * reads the flags of this rank's n_channels consecutive arrays (synchronous)
+ * and fails with TSA_ERR_CUDA if one is set. */
 #define TSA_IPC_HANDLE_BYTES 64
 TSA_API int tsa_ipc_alloc(size_t bytes, void** ptr, void* handle);
 TSA_API int tsa_ipc_open(const void* handle, void** ptr);
@@ -212,6 +219,38 @@ TSA_API int tsa_ipc_close(void* ptr);
 TSA_API int tsa_ipc_free(void* ptr);
 TSA_API int tsa_peer_barrier(int32_t* const* signals, int32_t world, int32_t rank, int32_t epoch,
                              void* stream);
+TSA_API int tsa_peer_check(const int32_t* own_signals, int32_t world, int32_t n_channels,
+                           void* stream);
+
+/* The head-sharded layer in one call (model.cpp:169-183 with the heads of the
+ * layer split over world ranks, one process per GPU).  d holds
+ * the WHOLE layer's geometry with [head_begin, head_end) = this rank's shard
+ * (whole KV groups); q / k / v are this rank's heads ([head_end - head_begin,
+ * L, d] and their KV heads).  ws: tsa_workspace_size(d) bytes.  k_keep
+ * (device int32) is the layer's budget (identical on every rank).  Exactly
+ * one exchange form:
+ *  - peer (tsa_peer, CUDA IPC buffers every rank allocated and mapped): the
+ *    score rows go from the pool pass straight into every rank's [H x L]
+ *    buffer, the output rows from the zero-row pass and the attention
+ *    epilogue into every rank's [H x L x d] buffer (out[rank] holds the
+ *    gathered layer output when the call completes on the stream); device
+ *    barriers on signals[0..2] order the step (graph-capturable; bf16, d 128);
+ *  - nccl_comm (an ncclComm_t over the same ranks, rank = shard index): the
+ *    score rows are all-gathered in place in s_full [H x L] before the budget
+ *    and the outputs in out_full [H x L x d] after the attention
+ *    (ncclAllGather, libnccl.so.2 resolved at run time).
+ * TSA_MODE_DENSE runs the dense kernel on the shard and the same output
+ * exchange. */
+typedef struct tsa_peer {
+    int32_t world, rank;
+    float* scores[TSA_MAX_REPLICAS];            /* every rank's [H x L] f32 buffer, rank order */
+    void* out[TSA_MAX_REPLICAS];                /* every rank's [H x L x d] buffer */
+    int32_t* signals[3][TSA_MAX_REPLICAS];      /* per channel: every rank's int32 [world + 2] */
+} tsa_peer;
+TSA_API int tsa_sparse_attention_layer_sharded(const tsa_desc* d, const void* q, const void* k,
+                                               const void* v, const tsa_peer* peer,
+                                               void* nccl_comm, float* s_full, void* out_full,
+                                               int32_t* k_keep, void* ws, void* stream);
 
 /* out[h, t] = +0.0 for every t with inv[h, t] < 0 (scatter_rows' zero rows). */
 TSA_API int tsa_zero_unselected(const tsa_desc* d, const int32_t* inv, void* out, void* stream);

@@ -15,7 +15,7 @@ TSA_F32, TSA_BF16 = 0, 1
 TSA_MODE_DENSE, TSA_MODE_DYNAMIC, TSA_MODE_FIXED = 0, 1, 2
 TSA_FORCED_FINAL_TOKEN, TSA_FORCED_RECENT_WINDOW = 0, 1
 TSA_SCORING_DEFAULT, TSA_SCORING_REFERENCE, TSA_SCORING_FAST = 0, 1, 2
-TSA_OK, TSA_ERR_INVALID, TSA_ERR_CUDA = 0, 1, 2
+TSA_OK, TSA_ERR_INVALID, TSA_ERR_CUDA, TSA_ERR_NCCL = 0, 1, 2, 3
 
 # Every symbol include/tsa_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -27,7 +27,8 @@ EXPORTS = (
     "tsa_split_heads_rope", "tsa_heads_concat", "tsa_sparse_attention_layer_host",
     "tsa_layer_drift", "tsa_select_sparse_layers", "tsa_gather_zero_replicas",
     "tsa_attend_indexed_replicas", "tsa_score_replicas", "tsa_ipc_alloc", "tsa_ipc_open",
-    "tsa_ipc_close", "tsa_ipc_free", "tsa_peer_barrier", "tsa_expf",
+    "tsa_ipc_close", "tsa_ipc_free", "tsa_peer_barrier", "tsa_expf", "tsa_peer_check",
+    "tsa_sparse_attention_layer_sharded",
 )
 TSA_IPC_HANDLE_BYTES = 64
 TSA_MAX_REPLICAS = 8
@@ -107,6 +108,8 @@ def load() -> C.CDLL:
         "tsa_ipc_close": (C.c_int, [P]),
         "tsa_ipc_free": (C.c_int, [P]),
         "tsa_peer_barrier": (C.c_int, [P, I, I, I, P]),
+        "tsa_peer_check": (C.c_int, [P, I, I, P]),
+        "tsa_sparse_attention_layer_sharded": (C.c_int, [D, P, P, P, P, P, P, P, P, P, P]),
         "tsa_attend_indexed_replicas": (C.c_int, [D, P, P, P, P, P, P, P, P, I, P]),
         "tsa_scatter_rows": (C.c_int, [D, P, P, P, P, P, P]),
         "tsa_check": (C.c_int, [D, P, P]),

@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtsa_b200.so"
-SOURCES = ["capi.cu", "score.cu", "score_fast.cu", "score_exact.cu", "select.cu", "gather_scatter.cu", "attend_simt.cu",
+SOURCES = ["capi.cu", "sharded.cu", "score.cu", "score_fast.cu", "score_exact.cu", "select.cu", "gather_scatter.cu", "attend_simt.cu",
            "attend_sm100.cu", "graph.cu", "producer.cu", "peer.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
     tmp = LIB.with_suffix(".so.tmp")
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
-                    *objs, "-lcudart"], check=True)
+                    *objs, "-lcudart", "-ldl"], check=True)
     os.replace(tmp, LIB)
     return LIB
 

@@ -687,6 +687,15 @@ int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const v
                               rows_per_head, kv_rows_per_head, single_replica(o), st);
 }
 
+// Dense causal attention with the output rows stored to every replica (the
+// head-sharded dense layer's all-gather fused into the epilogue).
+int launch_attend_sm100_rep(const tsa_desc& d, const void* q, const void* k, const void* v,
+                            const OutReplicas& o, cudaStream_t st) {
+    const int L = d.seq_len;
+    return launch_impl<false>(d, q, k, v, nullptr, nullptr, nullptr, nullptr, L,
+                              d.n_heads / d.n_kv_heads, L, L, o, st);
+}
+
 // Fused gather -> causal attention -> scatter of the selected rows (the
 // unselected rows are zeroed separately by launch_zero_unselected).
 int launch_attend_indexed(const tsa_desc& d, const void* q, const void* k, const void* v,

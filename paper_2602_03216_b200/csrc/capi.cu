@@ -176,6 +176,25 @@ int budget_impl(const tsa_desc& d, const float* s, int32_t* k_keep, void* ws, in
 }
 
 }  // namespace
+
+int forced_begin_of(const tsa_desc& d) { return forced_begin(d); }
+int check_descriptor(const tsa_desc* d) { return check_desc(d); }
+int budget_stage(const tsa_desc& d, const float* s, int32_t* k_keep, void* ws, int min_keep,
+                 cudaStream_t st) {
+    return budget_impl(d, s, k_keep, ws, min_keep, st);
+}
+
+int score_stage(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s, void* ws,
+                cudaStream_t st) {
+    const Workspace w = workspace_layout(d);
+    if (scoring_mode(d) == TSA_SCORING_FAST)
+        return launch_score_fast(d, q, k, s, at<float>(ws, w.colraw), at<float>(ws, w.rowstat), st);
+    if (score_exact_supported(d) && lq_of(d) <= 2048)
+        return launch_score_exact(d, q, k, s, at<float>(ws, w.logits), at<int>(ws, w.rowmax),
+                                  at<float>(ws, w.rowsum), at<float>(ws, w.colraw), st);
+    return launch_score_reference(d, q, k, s, at<float>(ws, w.logits), st);
+}
+
 }  // namespace tsa
 
 using namespace tsa;
@@ -216,14 +235,7 @@ int tsa_workspace_size(const tsa_desc* d, size_t* bytes) {
 
 static int score_impl(const tsa_desc* d, const void* q, const void* k, const OutReplicas& s,
                       void* ws, void* stream) {
-    const Workspace w = workspace_layout(*d);
-    if (scoring_mode(*d) == TSA_SCORING_FAST)
-        return launch_score_fast(*d, q, k, s, at<float>(ws, w.colraw), at<float>(ws, w.rowstat),
-                                 S(stream));
-    if (score_exact_supported(*d) && lq_of(*d) <= 2048)
-        return launch_score_exact(*d, q, k, s, at<float>(ws, w.logits), at<int>(ws, w.rowmax),
-                                  at<float>(ws, w.rowsum), at<float>(ws, w.colraw), S(stream));
-    return launch_score_reference(*d, q, k, s, at<float>(ws, w.logits), S(stream));
+    return tsa::score_stage(*d, q, k, s, ws, S(stream));
 }
 
 int tsa_score(const tsa_desc* d, const void* q, const void* k, float* s, void* ws, void* stream) {

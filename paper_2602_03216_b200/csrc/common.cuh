@@ -180,5 +180,16 @@ int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const v
                         int32_t rows_per_head, int32_t kv_rows_per_head, void* o,
                         cudaStream_t st);
 bool attend_sm100_supported(const tsa_desc& d);
+int launch_attend_sm100_rep(const tsa_desc& d, const void* q, const void* k, const void* v,
+                            const OutReplicas& o, cudaStream_t st);
+// capi.cu (shared with sharded.cu)
+int score_stage(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s, void* ws,
+                cudaStream_t st);
+int budget_stage(const tsa_desc& d, const float* s, int32_t* k_keep, void* ws, int min_keep,
+                 cudaStream_t st);
+int forced_begin_of(const tsa_desc& d);
+int check_descriptor(const tsa_desc* d);
+// peer.cu
+int launch_peer_barrier(int32_t* const* signals, int world, int rank, cudaStream_t st);
 
 }  // namespace tsa

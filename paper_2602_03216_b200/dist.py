@@ -82,6 +82,12 @@ class CudaBackend:
         self.local = _lib.make_desc(shard.h_per, shard.kv_per, L, d, dtype_code, **common)
         # the budget reads all H score rows
         self.full = _lib.make_desc(H, Hkv, L, d, dtype_code, **common)
+        # the whole layer with this rank's head range: tsa_sparse_attention_layer_sharded
+        self.sharded = _lib.make_desc(H, Hkv, L, d, dtype_code, **common)
+        self.sharded.head_begin, self.sharded.head_end = shard.h0, shard.h1
+        self.sharded_dense = _lib.make_desc(H, Hkv, L, d, dtype_code,
+                                            **dict(common, mode=int(SparseMode.kDense)))
+        self.sharded_dense.head_begin, self.sharded_dense.head_end = shard.h0, shard.h1
         lib = _lib.load()
         n1 = C.c_size_t()
         _lib.check(lib.tsa_workspace_size(C.byref(self.local), C.byref(n1)))
@@ -167,6 +173,15 @@ class CudaBackend:
         _lib.check(self.lib.tsa_scatter(C.byref(self.local), _ptr(self.oc), _ptr(self.inv),
                                         _ptr(out_local), _stream(self.device)))
 
+    def layer_sharded(self, q, k, v, dense, peer=None, nccl_comm=None, s_full=None,
+                      out_full=None):
+        """The whole sharded step in one C call (tsa_sparse_attention_layer_sharded)."""
+        desc = self.sharded_dense if dense else self.sharded
+        _lib.check(self.lib.tsa_sparse_attention_layer_sharded(
+            C.byref(desc), _ptr(q), _ptr(k), _ptr(v), C.byref(peer) if peer is not None else None,
+            C.c_void_p(nccl_comm) if nccl_comm else None, _ptr(s_full), _ptr(out_full),
+            _ptr(self.k_keep), _ptr(self.ws), _stream(self.device)))
+
     def dense(self, q, k, v, out_local):
         _lib.check(self.lib.tsa_dense_attention(C.byref(self.local), _ptr(q), _ptr(k), _ptr(v),
                                                 _ptr(out_local), _stream(self.device)))
@@ -181,12 +196,26 @@ class _CudaArray:
                                          "data": (int(ptr), False), "version": 3, "strides": None}
 
 
+class TsaPeer(C.Structure):
+    """struct tsa_peer (include/tsa_b200.h)."""
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32),
+                ("scores", C.c_void_p * _lib.TSA_MAX_REPLICAS),
+                ("out", C.c_void_p * _lib.TSA_MAX_REPLICAS),
+                ("signals", (C.c_void_p * _lib.TSA_MAX_REPLICAS) * 3)]
+
+
 class PeerBuffers:
     """Named device buffers every rank allocates with tsa_ipc_alloc and maps
     from every peer with tsa_ipc_open (handles exchanged through the process
-    group), plus per-channel signal slots for tsa_peer_barrier.  ``ptrs[name]``
-    lists the buffer's base address on every rank, in rank order, as seen from
-    this device."""
+    group), plus per-channel signal arrays for tsa_peer_barrier (int32 [world +
+    2] per channel and rank: arrivals, the device epoch counter, the timeout
+    flag).  ``ptrs[name]`` lists the buffer's base address on every rank, in
+    rank order, as seen from this device.
+
+    Setup is collective and failure-tolerant: a rank whose allocation or
+    mapping fails still takes part in every exchange (with a failure marker),
+    frees what it allocated or mapped, and every rank raises together -- the
+    collectives never go out of step."""
 
     CHANNELS = 3
 
@@ -195,33 +224,71 @@ class PeerBuffers:
         if world > _lib.TSA_MAX_REPLICAS:
             raise RuntimeError(f"peer exchange: world {world} > {_lib.TSA_MAX_REPLICAS}")
         self._own, self._opened = [], []
-        sizes = dict(sizes, _signals=self.CHANNELS * world * 4)
+        self.sig_stride = world + 2
+        sizes = dict(sizes, _signals=self.CHANNELS * self.sig_stride * 4)
+        err = None
         mine = {}
         with torch.cuda.device(device):
-            for name, nbytes in sizes.items():
-                ptr, h = C.c_void_p(), (C.c_char * _lib.TSA_IPC_HANDLE_BYTES)()
-                _lib.check(self.lib.tsa_ipc_alloc(nbytes, C.byref(ptr), h))
-                self._own.append(ptr.value)
-                mine[name] = (ptr.value, bytes(h))
+            try:
+                for name, nbytes in sizes.items():
+                    ptr, h = C.c_void_p(), (C.c_char * _lib.TSA_IPC_HANDLE_BYTES)()
+                    _lib.check(self.lib.tsa_ipc_alloc(nbytes, C.byref(ptr), h))
+                    self._own.append(ptr.value)
+                    mine[name] = (ptr.value, bytes(h))
+                if os.environ.get("TSA_TEST_PEER_ALLOC_FAIL_RANK") == str(rank):  # test hook
+                    raise RuntimeError("injected peer allocation failure")
+            except Exception as e:
+                err = f"rank {rank}: {type(e).__name__}: {e}"
             every = [None] * world
+            dev_index = torch.device(device).index if torch.device(device).index is not None \
+                else torch.cuda.current_device()
+            payload = {"err": err, "h": {k: v[1] for k, v in mine.items()} if not err else None,
+                       "device": dev_index}
             if world > 1:
-                dist.all_gather_object(every, {k: v[1] for k, v in mine.items()})
+                dist.all_gather_object(every, payload)
+            else:
+                every = [payload]
+            errs = [x["err"] for x in every if x["err"]]
+            # direct peer access (NVLink / NVSwitch) to every other rank's device:
+            # the kernels store into the peers' buffers
+            self.peer_access = {}
+            for r, x in enumerate(every):
+                other = x["device"]
+                ok = other == dev_index or torch.cuda.can_device_access_peer(dev_index, other)
+                self.peer_access[r] = bool(ok)
+                if not ok and not errs:
+                    errs.append(f"rank {rank}: no peer access from cuda:{dev_index} to cuda:{other}")
             self.ptrs = {}
-            for name in sizes:
-                row = []
-                for r in range(world):
-                    if r == rank:
-                        row.append(mine[name][0])
-                        continue
-                    ptr = C.c_void_p()
-                    h = (C.c_char * _lib.TSA_IPC_HANDLE_BYTES).from_buffer_copy(every[r][name])
-                    _lib.check(self.lib.tsa_ipc_open(h, C.byref(ptr)))
-                    self._opened.append(ptr.value)
-                    row.append(ptr.value)
-                self.ptrs[name] = row
-        self._epoch = [0] * self.CHANNELS
+            if not errs:
+                try:
+                    for name in sizes:
+                        row = []
+                        for r in range(world):
+                            if r == rank:
+                                row.append(mine[name][0])
+                                continue
+                            ptr = C.c_void_p()
+                            h = (C.c_char * _lib.TSA_IPC_HANDLE_BYTES).from_buffer_copy(
+                                every[r]["h"][name])
+                            _lib.check(self.lib.tsa_ipc_open(h, C.byref(ptr)))
+                            self._opened.append(ptr.value)
+                            row.append(ptr.value)
+                        self.ptrs[name] = row
+                except Exception as e:
+                    errs.append(f"rank {rank}: {type(e).__name__}: {e}")
+            if world > 1:  # the mapping outcome of every rank
+                flag = [None] * world
+                dist.all_gather_object(flag, errs[-1] if errs else None)
+                errs = errs or [f for f in flag if f]
+            if errs:
+                self.close_mappings()
+                if world > 1:
+                    dist.barrier()  # every importer closed before any exporter frees
+                self.free_own()
+                raise RuntimeError("peer buffers: " + "; ".join(errs))
+        base = self.ptrs["_signals"]
         self._sig = [(C.c_void_p * _lib.TSA_MAX_REPLICAS)(
-            *[p + c * world * 4 for p in self.ptrs["_signals"]]) for c in range(self.CHANNELS)]
+            *[p + c * self.sig_stride * 4 for p in base]) for c in range(self.CHANNELS)]
 
     def tensor(self, name, shape, dtype):
         """This rank's buffer as a tensor (bf16 through an int16 view)."""
@@ -230,9 +297,24 @@ class PeerBuffers:
         return t.view(dtype) if dtype == torch.bfloat16 else t
 
     def barrier(self, channel: int, stream=None):
-        self._epoch[channel] += 1
-        _lib.check(self.lib.tsa_peer_barrier(self._sig[channel], self.world, self.rank,
-                                             self._epoch[channel], _stream(self.device)))
+        """Device barrier on `channel` (epoch from the device counter: capturable)."""
+        _lib.check(self.lib.tsa_peer_barrier(self._sig[channel], self.world, self.rank, 0,
+                                             _stream(self.device)))
+
+    def check(self):
+        """Raises if a barrier of this rank timed out (synchronous)."""
+        own = C.c_void_p(self.ptrs["_signals"][self.rank])
+        _lib.check(self.lib.tsa_peer_check(own, self.world, self.CHANNELS, _stream(self.device)))
+
+    def peer_struct(self, scores: str, out: str) -> TsaPeer:
+        p = TsaPeer()
+        p.world, p.rank = self.world, self.rank
+        for r in range(self.world):
+            p.scores[r] = self.ptrs[scores][r]
+            p.out[r] = self.ptrs[out][r]
+            for c in range(self.CHANNELS):
+                p.signals[c][r] = self._sig[c][r]
+        return p
 
     def close_mappings(self):
         """Unmap the peers' buffers (local; safe at any time after the last step)."""
@@ -328,6 +410,22 @@ class ShardedSparseAttention:
         if self.c2 != "peer":
             self.out_full = self.out_local if world == 1 or not gather_output else torch.empty(
                 (H, L, d), dtype=dtype, device=device)
+        # the unmarked step as one C call (tsa_sparse_attention_layer_sharded):
+        # the peer form, or the NCCL form on the process group's communicator
+        self._c_form, self._nccl_comm = None, None
+        if isinstance(self.backend, CudaBackend) and gather_output:
+            if self.c2 == "peer":
+                self._c_form = "peer"
+            elif world > 1 and dist.get_backend() == "nccl":
+                try:
+                    t = torch.zeros(1, device=device)
+                    dist.all_reduce(t)  # the communicator exists from here on
+                    pg = dist.distributed_c10d._get_default_group()
+                    self._nccl_comm = int(pg._get_backend(torch.device("cuda", torch.device(
+                        device).index))._comm_ptr())
+                    self._c_form = "nccl" if self._nccl_comm else None
+                except Exception:  # no raw communicator: the staged all-gathers
+                    self._c_form = None
 
     def _setup_peer(self, H, L, d, dtype, device):
         sh = self.shard
@@ -341,6 +439,7 @@ class ShardedSparseAttention:
         out_off = sh.h0 * L * d * eb
         self._replicas = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(
             *[p + out_off for p in self._peer.ptrs["out"]])
+        self._peer_struct = self._peer.peer_struct("s", "out")
         off = sh.h0 * L * 4
         self._s_replicas = (C.c_void_p * _lib.TSA_MAX_REPLICAS)(
             *[p + off for p in self._peer.ptrs["s"]])
@@ -378,11 +477,12 @@ class ShardedSparseAttention:
         """``step`` replayed from a CUDA graph captured on the first call for
         these input buffers: the chain never waits on the host (k_keep stays
         on the device), so the launch sequence is fixed and one graph launch
-        replaces ~8 host launches and their gaps.  Single-process only (the
-        NCCL all-gathers and peer barriers of a sharded step run
-        eagerly)."""
-        if self.shard.world > 1 or self.c2 == "peer":
-            return self.step(q, k, v, dense=dense)
+        replaces ~8 host launches and their gaps.  The peer form of a sharded
+        step is captured too (its barriers take their epochs from device
+        counters, so every replay synchronises the ranks); the NCCL form runs
+        eagerly."""
+        if self.shard.world > 1 and self._c_form != "peer":
+            return self.step(q, k, v, dense=dense)  # NCCL all-gathers run eagerly
         key = (q.data_ptr(), k.data_ptr(), v.data_ptr(), dense)
         graphs = self.__dict__.setdefault("_graphs", {})
         g = graphs.get(key)
@@ -403,14 +503,39 @@ class ShardedSparseAttention:
         self.graph_kernels = g.tsa_kernels
         return self.out_full
 
+    def _step_c(self, q, k, v, dense):
+        b = self.backend
+        if self._c_form == "peer":
+            b.layer_sharded(q, k, v, dense, peer=self._peer_struct)
+        else:
+            b.layer_sharded(q, k, v, dense, nccl_comm=self._nccl_comm, s_full=self.s_full,
+                            out_full=self.out_full)
+        return self.out_full
+
+    def check(self):
+        """Raises if a peer barrier of this rank timed out (synchronous)."""
+        if self._peer is not None:
+            self._peer.check()
+
     def step(self, q, k, v, marks=None, dense: bool = False):
+        dense = dense or self.plan.mode == SparseMode.kDense
+        if marks is None and self._c_form is not None:
+            return self._step_c(q, k, v, dense)
+        # staged: one library call per stage (bench.py records events between them)
         mark = marks or (lambda name: None)
         b = self.backend
-        if dense or self.plan.mode == SparseMode.kDense:
+        if dense:
             mark("start")
+            if self.c2 == "peer":
+                self._peer.barrier(0)
             b.dense(q, k, v, self.out_local)
             mark("attend")
-            self._all_gather(self.out_full, self.out_local)
+            if self.c2 == "peer" and self.shard.world == 1:
+                self.out_full.copy_(self.out_local)  # the peer buffer is the output
+            else:
+                self._all_gather(self.out_full, self.out_local)
+            if self.c2 == "peer":
+                self._peer.barrier(1)
             mark("allgather_out")
             return self.out_full
         mark("start")

@@ -99,16 +99,77 @@ SCRIPT = textwrap.dedent("""
     peer = ShardedSparseAttention(8, 2, L, 128, torch.bfloat16, plan, device=dev, c2="peer")
     assert peer.c2 == "peer", peer.c2
     a = ref.step(q, k, v).clone()
-    for _ in range(2):
+    same = lambda x, y: torch.equal(x.view(torch.int16), y.view(torch.int16))
+    # the peer form: one C call (tsa_sparse_attention_layer_sharded), the staged
+    # stage calls (marks) and the graph-replayed C call (device barrier epochs)
+    for run in ("c", "staged", "graph", "graph", "c"):
         peer.out_full.fill_(float("nan"))
         peer.s_full.fill_(float("nan"))
-        b = peer.step(q, k, v)
+        if run == "c":
+            b = peer.step(q, k, v)
+        elif run == "staged":
+            b = peer.step(q, k, v, marks=lambda name: None)
+        else:
+            b = peer.step_graphed(q, k, v)
         torch.cuda.synchronize()
-        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
-        assert torch.equal(peer.s_full, ref.s_full) and peer.k_keep == ref.k_keep
+        assert same(a, b), run
+        assert torch.equal(peer.s_full, ref.s_full) and peer.k_keep == ref.k_keep, run
+    peer.check()  # no barrier timed out
+    # a dense step in the peer form lands in the peer output buffer (staged and C)
+    dense_ref, _ = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), tsa.SparsePlan())
+    for marks in (None, lambda name: None):
+        peer.out_full.fill_(float("nan"))
+        b = peer.step(q, k, v, dense=True, marks=marks)
+        torch.cuda.synchronize()
+        assert same(dense_ref, b) and peer.k_keep == L
+    # the NCCL form of the C entry on the process group's communicator (world 1)
+    pg = dist.distributed_c10d._get_default_group()
+    comm = int(pg._get_backend(dev)._comm_ptr())
+    s_full = torch.full((8, L), float("nan"), device=dev)
+    out_full = torch.full_like(q, float("nan"))
+    ref.backend.layer_sharded(q, k, v, False, nccl_comm=comm, s_full=s_full, out_full=out_full)
+    torch.cuda.synchronize()
+    assert same(a, out_full) and torch.equal(s_full, ref.s_full)
+    ref.backend.layer_sharded(q, k, v, True, nccl_comm=comm, s_full=s_full, out_full=out_full)
+    torch.cuda.synchronize()
+    assert same(dense_ref, out_full)
     dist.destroy_process_group()
     print("peer c2 ok", ref.k_keep)
 """)
+
+
+TIMEOUT_SCRIPT = textwrap.dedent("""
+    import ctypes as C, os, sys, torch
+    sys.path.insert(0, {root!r})
+    from paper_2602_03216_b200 import _lib
+    lib = _lib.load()
+    world = 2
+    sig = torch.zeros(2 * (world + 2), dtype=torch.int32, device="cuda")
+    arr = (C.c_void_p * 8)(sig.data_ptr(), sig.data_ptr() + (world + 2) * 4)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    # rank 0 of 2 alone at the barrier: the peer never arrives
+    _lib.check(lib.tsa_peer_barrier(arr, world, 0, 0, st))
+    torch.cuda.synchronize()  # returns after TSA_PEER_TIMEOUT_S, no trap
+    try:
+        _lib.check(lib.tsa_peer_check(C.c_void_p(sig.data_ptr()), world, 1, st))
+        print("no timeout reported")
+    except _lib.CudaError as e:
+        assert "did not reach barrier" in str(e), e
+        x = torch.ones(4, device="cuda") * 2  # the context is still usable
+        print("timeout ok", float(x.sum()))
+""")
+
+
+def test_peer_barrier_timeout_sets_a_flag_not_a_trap(cuda, tmp_path):
+    """A peer that never arrives: the barrier returns after TSA_PEER_TIMEOUT_S
+    with the timeout flag set (tsa_peer_check raises) and the CUDA context stays
+    usable -- no __trap / sticky error (the 60 s trap)."""
+    p = tmp_path / "timeout.py"
+    p.write_text(TIMEOUT_SCRIPT.format(root=str(ROOT)))
+    r = subprocess.run([sys.executable, str(p)], capture_output=True, text=True, timeout=120,
+                       env={**os.environ, "TSA_PEER_TIMEOUT_S": "1"})
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "timeout ok" in r.stdout
 
 
 def test_peer_c2_ipc_buffers_world1(cuda, tmp_path):

@@ -19,6 +19,9 @@ def _rank(rank, world, port, out_path, tau, c, c2):
     if c2 == "auto-fail":  # the last rank's peer setup fails: every rank falls back together
         os.environ["TSA_TEST_PEER_FAIL_RANK"] = str(world - 1)
         c2 = "auto"
+    if c2 == "auto-allocfail":  # rank 0's IPC allocation fails BEFORE the handle exchange
+        os.environ["TSA_TEST_PEER_ALLOC_FAIL_RANK"] = "0"
+        c2 = "auto"
     import paper_2602_03216_b200 as tsa
     from paper_2602_03216_b200 import workloads
     from paper_2602_03216_b200.dist import ShardedSparseAttention
@@ -32,15 +35,26 @@ def _rank(rank, world, port, out_path, tau, c, c2):
     sh = lay.shard
     args = (q[sh.h0:sh.h1].contiguous(), k[sh.kv0:sh.kv1].contiguous(),
             v[sh.kv0:sh.kv1].contiguous())
-    for _ in range(3):  # repeated steps: barrier epochs, buffers rewritten in place
+    outs = []
+    # repeated steps (barrier epochs, buffers rewritten in place) through every
+    # entry: the one-call C form, the staged stage calls, the graph replay
+    for run in ("c", "staged", "graph", "graph", "c"):
         if lay.c2 == "peer":
             lay.out_full.fill_(float("nan"))
             lay.s_full.fill_(float("nan"))
             torch.cuda.synchronize()
             dist.barrier()  # no rank refills after a peer's kernels started writing
-        out = lay.step(*args)
+        if run == "c":
+            out = lay.step(*args)
+        elif run == "staged":
+            out = lay.step(*args, marks=lambda name: None)
+        else:
+            out = lay.step_graphed(*args)
         torch.cuda.synchronize()
         dist.barrier()
+        outs.append(out.view(torch.int16).clone())
+    assert all(torch.equal(outs[0], o) for o in outs)
+    lay.check()
     if rank == 0:
         np.savez(out_path, out=out.view(torch.int16).cpu().numpy(), k_keep=lay.k_keep,
                  s=lay.s_full.cpu().numpy(), c2=lay.c2)
@@ -54,7 +68,7 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("c2", ["nccl", "peer", "auto-fail"])
+@pytest.mark.parametrize("c2", ["nccl", "peer", "auto-fail", "auto-allocfail"])
 @pytest.mark.parametrize("world,H,Hkv,tau", [(2, 8, 2, 0.02), (2, 8, 2, 0.0), (4, 16, 4, 0.02)])
 def test_multi_rank_cuda_sharding_matches_single_process(cuda, tmp_path, world, H, Hkv, tau, c2):
     """c2="nccl": the all-gathers (over gloo here); c2="peer": the score and
@@ -74,7 +88,7 @@ def test_multi_rank_cuda_sharding_matches_single_process(cuda, tmp_path, world, 
                                  device=q.device)
     ref = one.step(q, k, v)
     torch.cuda.synchronize()
-    assert str(got["c2"]) == ("nccl" if c2 == "auto-fail" else c2)
+    assert str(got["c2"]) == ("nccl" if c2.startswith("auto-") else c2)
     assert int(got["k_keep"]) == one.k_keep
     assert np.array_equal(got["s"].view(np.uint32), one.s_full.cpu().numpy().view(np.uint32))
     assert np.array_equal(got["out"], ref.view(torch.int16).cpu().numpy())
