@@ -497,9 +497,12 @@ struct HostPipe {
     cudaEvent_t start = nullptr, kvq = nullptr, q[64] = {}, done[64] = {}, vr[64] = {},
                 fin = nullptr;
 };
+// One pipeline (copy streams + events) per calling thread and device: two
+// threads' host-tensor calls never share streams or events (the reference's
+// operators are pure and safe to call concurrently).
 HostPipe* host_pipe(int device) {
-    static HostPipe pipes[16];
-    static bool init[16] = {};
+    thread_local HostPipe pipes[16];
+    thread_local bool init[16] = {};
     if (device < 0 || device >= 16) return nullptr;
     HostPipe& p = pipes[device];
     if (!init[device]) {

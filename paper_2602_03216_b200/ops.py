@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import Callable, List, Optional, Sequence
@@ -218,16 +219,25 @@ def _stream(device: torch.device):
 
 
 _kd_cache = {}
+# Scratch buffers are cached per (device, stream): calls on one stream are
+# ordered, so they may share them; calls on different streams (threads) get
+# their own -- the operators stay safe to call concurrently.
+_cache_lock = threading.Lock()
+
+
+def _stream_key(device: torch.device):
+    return (device.type, device.index, torch.cuda.current_stream(device).cuda_stream)
 
 
 def _workspace(desc: _lib.TsaDesc, device: torch.device) -> torch.Tensor:
     nbytes = C.c_size_t()
     _lib.check(_lib.load().tsa_workspace_size(C.byref(desc), C.byref(nbytes)))
-    key = (device.type, device.index)
-    ws = _ws_cache.get(key)
-    if ws is None or ws.numel() < nbytes.value:
-        ws = torch.zeros(max(nbytes.value, 256), dtype=torch.uint8, device=device)
-        _ws_cache[key] = ws
+    key = _stream_key(device)
+    with _cache_lock:
+        ws = _ws_cache.get(key)
+        if ws is None or ws.numel() < nbytes.value:
+            ws = torch.zeros(max(nbytes.value, 256), dtype=torch.uint8, device=device)
+            _ws_cache[key] = ws
     return ws
 
 
@@ -467,9 +477,11 @@ def sparse_attention_layer(heads: HeadTensors, plan: SparsePlan, layer: int = 0,
         kd = torch.empty(1, dtype=torch.int32, device=dev)
     else:  # selection stays in the workspace; stable addresses keep the graph cache warm
         idx = None
-        kd = _kd_cache.get((dev.type, dev.index))
-        if kd is None:
-            kd = _kd_cache[(dev.type, dev.index)] = torch.empty(1, dtype=torch.int32, device=dev)
+        key = _stream_key(dev)
+        with _cache_lock:
+            kd = _kd_cache.get(key)
+            if kd is None:
+                kd = _kd_cache[key] = torch.empty(1, dtype=torch.int32, device=dev)
     _lib.check(_lib.load().tsa_sparse_attention_layer(
         C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(idx), _ptr(kd), None,
         _ptr(ws), _stream(dev)))
@@ -565,12 +577,14 @@ def sparse_attention_layer_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tenso
     desc = _desc_for(H, Hkv, L, d, _dtype_code(q), mode=int(plan.mode), tau=plan.tau,
                      s_fixed=plan.s_fixed, last_q=plan.last_q, kernel=plan.kernel,
                      forced_policy=int(plan.forced), scoring=scoring)
-    key = (device.index, q.dtype, H, Hkv, L, d)
-    bufs = _staging.get(key)
-    if bufs is None:
-        bufs = _staging[key] = (torch.empty_like(q, device=device), torch.empty_like(k, device=device),
-                                torch.empty_like(v, device=device), torch.empty_like(out, device=device),
-                                torch.empty(1, dtype=torch.int32, device=device))
+    key = _stream_key(device) + (q.dtype, H, Hkv, L, d)
+    with _cache_lock:
+        bufs = _staging.get(key)
+        if bufs is None:
+            bufs = _staging[key] = (
+                torch.empty_like(q, device=device), torch.empty_like(k, device=device),
+                torch.empty_like(v, device=device), torch.empty_like(out, device=device),
+                torch.empty(1, dtype=torch.int32, device=device))
     qd, kd, vd, od, kk = bufs
     ws = _workspace(desc, device)
     _lib.check(_lib.load().tsa_sparse_attention_layer_host(
