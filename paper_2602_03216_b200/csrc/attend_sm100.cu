@@ -562,6 +562,42 @@ int make_f32_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t r
     return 0;
 }
 
+// 2-D map over [rows x 128] bf16 rows, whole-row (256 B) x box_rows boxes, no
+// swizzle: rows land in shared memory back to back (gather_scatter.cu's TMA
+// gather: tile::gather4 loads with box_rows = 1, bulk tensor stores of 64 rows).
+int make_bf16_rows_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return invalid("tsa: cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {HD, rows};
+    cuuint64_t strides[1] = {HD * 2};
+    cuuint32_t box[2] = {HD, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return invalid("tsa: row tensor map encode failed (" + std::to_string((int)r) + ")");
+    return 0;
+}
+
+// 3-D [heads x rows x 128] bf16, whole-row x box_rows x 1 boxes, no swizzle: a
+// store box never crosses into the next head (rows >= `rows` are clipped).
+int make_bf16_rows_map_3d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t heads,
+                          uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return invalid("tsa: cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {HD, rows, heads};
+    cuuint64_t strides[2] = {HD * 2, rows * HD * 2};
+    cuuint32_t box[3] = {HD, box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return invalid("tsa: 3-D row tensor map encode failed (" + std::to_string((int)r) + ")");
+    return 0;
+}
+
 // 3-D map over [heads x rows x 128] bf16 with the same 64 x 128 SW128 boxes,
 // used by the indexed kernel for a head's last, partial V tile: past the
 // head's last row it reads zeros (out of bounds), never the next head's rows

@@ -7,9 +7,18 @@
 //   out[h, t] = oc[h, inv[h, t]] if inv >= 0 else +0.0 -- every output row is
 //   written exactly once (no zero-fill pass).  Bytes: H*L*d*b written +
 //   H*k*d*b read + 4*H*L inv.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace tsa {
+
+int make_bf16_rows_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows);
+int make_bf16_rows_map_3d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t heads,
+                          uint32_t box_rows);
+
 namespace {
 
 // A block moves 64 rows of one head: the 64 indices are staged in shared
@@ -110,6 +119,83 @@ __global__ void __launch_bounds__(256) gather_kernel(const V* __restrict__ q,
     }
 }
 
+// The K/V compress of the fused path (bf16, d = 128) on the TMA: per block of
+// 64 compressed rows one thread issues 16 tile::gather4 loads per tensor (4
+// selected rows of 256 B each) into shared memory and one bulk tensor store of
+// the 64 rows (16 KB) per tensor -- the copy costs a few dozen instructions per
+// 32 KB instead of two thousand 16-B loads and stores.  Rows in [n, ceil128(n))
+// are read out of bounds (zeros).  The dropped output rows of the block's 64
+// positions are zeroed by all threads with streaming stores beside it.
+constexpr int GT_ROWS = 64;
+
+struct __align__(128) GatherSmem {
+    uint8_t k[GT_ROWS * 256];
+    uint8_t v[GT_ROWS * 256];
+    uint64_t full;
+    int32_t rows[GT_ROWS];
+    bool drop[GT_ROWS];
+};
+
+__global__ void __launch_bounds__(256) gather_tma_kernel(
+    const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+    const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc,
+    const int32_t* __restrict__ idx, const int32_t* __restrict__ k_keep_p, int L, int group,
+    int head_begin, int kv_rows, const int32_t* __restrict__ inv, const OutReplicas out) {
+    __shared__ GatherSmem sm;
+    using namespace tsa_dev;
+    const int hg = blockIdx.x % group, rb = blockIdx.x / group;
+    const int h = head_begin + blockIdx.y * group + hg;  // kc / vc / out are indexed by h
+    const int kv = h / group - head_begin / group;
+    const int n = *k_keep_p;
+    const int r0 = rb * GT_ROWS;
+    const int pad_end = min(L, (n + 127) / 128 * 128);
+    // k_keep == L: identity selection, the attention reads K/V in place
+    const bool gather = r0 < pad_end && n != L;
+    if (!gather && out.n == 0) return;
+    const int tid = threadIdx.x;
+    if (tid < GT_ROWS) {
+        const int r = r0 + tid;
+        // rows past k_keep read out of bounds: TMA fills zeros
+        sm.rows[tid] = gather && r < n ? kv * L + idx[(size_t)h * L + r] : kv_rows;
+        if (out.n) sm.drop[tid] = r < L && __ldg(inv + (size_t)h * L + r) < 0;
+    }
+    if (tid == 0 && gather) {
+        mbar_init(&sm.full, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (gather && tid == 0) {
+        const int nr = min(GT_ROWS, pad_end - r0);
+        const int ng = (nr + 3) / 4;
+        mbar_arrive_expect_tx(&sm.full, ng * 4 * 256 * 2);
+        for (int g4 = 0; g4 < ng; ++g4) {
+            const int* rr = sm.rows + 4 * g4;
+            tma_gather4(sm.k + g4 * 1024, &tm_k, &sm.full, 0, rr[0], rr[1], rr[2], rr[3]);
+            tma_gather4(sm.v + g4 * 1024, &tm_v, &sm.full, 0, rr[0], rr[1], rr[2], rr[3]);
+        }
+    }
+    if (out.n) {  // zero rows of the dropped positions, every replica
+#pragma unroll
+        for (int i = 0; i < TSA_MAX_REPLICAS; ++i) {
+            if (i >= out.n) break;
+            uint4* o = static_cast<uint4*>(out.p[i]) + ((size_t)h * L + r0) * 16;
+            for (int e = tid; e < GT_ROWS * 16; e += 256)
+                if (sm.drop[e >> 4]) __stcs(o + e, make_uint4(0u, 0u, 0u, 0u));
+        }
+        if (out.n > 1) __threadfence_system();
+    }
+    if (gather && tid == 0) {
+        mbar_wait(&sm.full, 0);
+        fence_proxy_async_smem();
+        // 64 rows per tensor in one store; the 3-D map clips rows >= L (never the
+        // next head's); rows in (pad_end, r0 + 64) are scratch the attention skips
+        tma_store_3d(&tm_kc, sm.k, 0, r0, h);
+        tma_store_3d(&tm_vc, sm.v, 0, r0, h);
+        bulk_commit();
+        bulk_wait0();
+    }
+}
+
 template <typename V>
 __global__ void __launch_bounds__(256) scatter_kernel(const V* __restrict__ oc,
                                                       const int32_t* __restrict__ inv,
@@ -207,6 +293,23 @@ static int gather_t(const tsa_desc& d, const void* q, const void* k, const void*
     const int group = d.n_heads / d.n_kv_heads;  // shards hold whole KV groups
     dim3 grid((L + 63) / 64 * group, nh / group);
     const int skip = (qc == nullptr && out.n > 0) ? 1 : 0;
+    if (sizeof(V) == 16 && chunks == 16 && d.dtype == TSA_BF16 && qc == nullptr && skip) {
+        // the fused path's K/V compress: TMA row gathers and bulk row stores
+        const int kv_begin = d.head_begin / group, n_kv = nh / group;
+        const uint8_t* kb = static_cast<const uint8_t*>(k) + (size_t)kv_begin * L * 256;
+        const uint8_t* vb = static_cast<const uint8_t*>(v) + (size_t)kv_begin * L * 256;
+        CUtensorMap mk, mv, mkc, mvc;
+        int rc;
+        if ((rc = make_bf16_rows_map(&mk, kb, (uint64_t)n_kv * L, 1)) ||
+            (rc = make_bf16_rows_map(&mv, vb, (uint64_t)n_kv * L, 1)) ||
+            (rc = make_bf16_rows_map_3d(&mkc, kc, L, d.head_end, GT_ROWS)) ||
+            (rc = make_bf16_rows_map_3d(&mvc, vc, L, d.head_end, GT_ROWS)))
+            return rc;
+        gather_tma_kernel<<<grid, 256, 0, st>>>(mk, mv, mkc, mvc, idx, k_keep, L, group,
+                                                 d.head_begin, n_kv * L, inv, out);
+        TSA_LAUNCH_CHECK("gather_tma");
+        return 0;
+    }
     if (sizeof(V) == 16 && chunks == 16)  // d = 128 bf16 rows
         gather_kernel<V, 16><<<grid, 256, 0, st>>>((const V*)q, (const V*)k, (const V*)v, idx,
                                                    k_keep, (V*)qc, (V*)kc, (V*)vc, L, group,
