@@ -147,14 +147,18 @@ def f_attn(k, d, heads):
     return 2.0 * k * (k + 1) * d * heads
 
 
-def kernel_rooflines(stages, H, Hkv, L, k, d=128, b=2, lq=64):
+def kernel_rooflines(stages, H, Hkv, L, k, d=128, b=2, lq=64, exact=True, sm_mhz=None):
     """Per-kernel roofline of one sparse step (SURVEY §8(d) work per unit):
     achieved GB/s or TFLOP/s of each stage's algorithmic work over its event
     time, against the measured HBM copy / sustained bf16 peaks."""
     hbm, _, tf_sust, _ = measured_peaks()
     work = {
-        # K read in two passes per KV group + Q tails + score rows; 2 passes x 2 lq L d H flop
-        "score": ("ridge (HBM ~ tensor; MUFU exp2 bound in practice)",
+        # exact (default) scoring: the p-ordered logits (2 lq L d H flop on the FP32 pipe,
+        # FFMA2) written once as f32 and read by the row and the column pass
+        "score": ("fp32 FFMA2 (exact-order logits) + HBM (row / column passes over the logits)",
+                  Hkv * L * d * b + H * lq * d * b + 3 * 4 * H * lq * L + 4 * H * L,
+                  2.0 * lq * L * d * H) if exact else
+                 ("ridge (HBM ~ tensor; MUFU exp2 bound in practice)",
                   2 * Hkv * L * d * b + H * lq * d * b + 4 * H * L, 4.0 * lq * L * d * H),
         "budget": ("latency", 4 * H * L + 8 * L, None),
         "select": ("latency", 4 * H * L + 8 * H * L, None),
@@ -174,7 +178,14 @@ def kernel_rooflines(stages, H, Hkv, L, k, d=128, b=2, lq=64):
         if nbytes:
             gbs = nbytes / (ms * 1e-3) / 1e9
             row.update({"GB/s": round(gbs, 1), "hbm_frac": round(gbs / hbm, 4)})
-        if flops:
+        if flops and name == "score" and exact:
+            # FP32 pipe: 128 FMA / clk / SM nominal (the FFMA2 issue ceiling measured by
+            # tools/probes/ffma2_probe.cu is ~90), at the sampled SM clock
+            tfs = flops / (ms * 1e-3) / 1e12
+            peak = 2 * 128 * 148 * (sm_mhz or 1965.0) * 1e6 / 1e12
+            row.update({"TFLOP/s": round(tfs, 1), "fp32_peak_TFLOP/s": round(peak, 1),
+                        "fp32_frac": round(tfs / peak, 4)})
+        elif flops:
             tfs = flops / (ms * 1e-3) / 1e12
             row.update({"TFLOP/s": round(tfs, 1), "tensor_frac": round(tfs / tf_sust, 4)})
         out[name] = row
@@ -429,7 +440,9 @@ def run_ours(args):
             "tau_sweep": sweep, "eager_ms": round(eager_ms, 3),
             "stages_ms": {kk: round(vv, 4) for kk, vv in stages.items()},
             "hbm_stages": hbm_rows, "roofline": roofline,
-            "kernel_rooflines": kernel_rooflines(stages, sh.h_per, sh.kv_per, L, k_keep),
+            "kernel_rooflines": kernel_rooflines(stages, sh.h_per, sh.kv_per, L, k_keep,
+                                                 exact=args.scoring != 2,
+                                                 sm_mhz=clocks.get("sm_mhz")),
             "scoring": {0: "REFERENCE (default): the reference's f32 operation order, bit-exact "
                            "scores (exact-order FFMA2 logits, glibc expf port, sequential "
                            "sums)", 1: "REFERENCE (exact f32 order)",

@@ -555,10 +555,10 @@ select_kernel(const float* __restrict__ s, int L, const int32_t* __restrict__ k_
 // Same algorithm as select_kernel, with each CTA's slice of the head's scores
 // staged once into shared memory as radix keys (forced tokens as the
 // kForcedKey sentinel): the three histogram levels and the two compaction
-// passes then read shared memory instead of re-reading L2 five times, and 512
-// threads per CTA let two clusters share an SM.  Used when a slice fits
+// passes then read shared memory instead of re-reading L2 five times, and 384
+// threads per CTA let two clusters share an SM without register spills.  Used when a slice fits
 // (ceil(L / CL) <= kSliceMax).
-constexpr int BS = 512;
+constexpr int BS = 384;  // 2 CTAs per SM at <= 85 registers: no spills (512 spilled 56 B)
 constexpr int kSliceMax = 16384;
 constexpr uint32_t kForcedKey = 0xFFFFFFFFu;
 
