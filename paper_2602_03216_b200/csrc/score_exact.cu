@@ -26,11 +26,11 @@
 //     on an ordered-int encoding).  34.4 G FMA at 128K / Llama-3-8B: the
 //     FP32 pipe is the roofline.
 //   score_exact_rowsum (XB): the sequential row sums, one CTA per ~n_rows/#SM
-//     rows (<= 16): X tiles arrive by TMA, 8 helper warps (thread = key)
-//     compute e into a transposed shared tile, one warp (lane = row) runs the
-//     f32 chain in key order -- L dependent FADDs per row, the floor of this
-//     kernel (0.27 ms at 128K).
-//   score_exact_colsum (XC): thread = key, e recomputed, P = e / sum_r
+//     rows (<= 16): X tiles arrive by TMA, 16 helper warps (thread = key x half
+//     the rows) compute e -- once: it is written back over X -- into a
+//     transposed shared tile, one warp (lane = row) runs the f32 chain in key
+//     order (L dependent FADDs per row: 0.32 ms at 128K).
+//   score_exact_colsum (XC): thread = key, P = e / sum_r (Markstein division)
 //     accumulated over r in order -> raw column sums.
 //   pool: the shared edge-clamped pool kernel (score.cu).
 #include <cuda.h>
@@ -318,8 +318,9 @@ struct __align__(128) XbSmem {
 };
 
 __global__ void __launch_bounds__(XB_THREADS, 1)
-score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int n_rows,
-                   int rows_per_cta, const int* __restrict__ rowmax, float* __restrict__ rowsum) {
+score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__ X, int L, int Lp,
+                   int lq, int n_rows, int rows_per_cta, const int* __restrict__ rowmax,
+                   float* __restrict__ rowsum) {
     extern __shared__ uint8_t smem_raw[];
     XbSmem& sm = smem_view<XbSmem, 128>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -377,11 +378,15 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int 
             float xv[RH];
 #pragma unroll
             for (int i = 0; i < RH; ++i) xv[i] = xs[i * XB_KEYS];
+            // e overwrites X in HBM (the column pass reads it: the exponentials run once)
+            float* xg = X + (size_t)(row0 + rbase) * Lp + key;
 #pragma unroll
             for (int i = 0; i < RH; ++i) {
                 // masked entries add +0 to the chain: exactly the reference's skip
                 const float e = expf_glibc(__fsub_rn(xv[i], mrow[i]), sm.tab);
-                es[i] = key < arow[i] ? e : 0.0f;
+                const bool ok = key < arow[i];
+                es[i] = ok ? e : 0.0f;
+                if (ok) __stcs(xg + (size_t)i * Lp, e);
             }
             __syncwarp();
             if (lane == 0) {
@@ -447,21 +452,21 @@ struct __align__(128) XcHead {
 };
 __host__ __device__ constexpr int xc_rs_bytes(int lq) { return (lq * 16 + 127) / 128 * 128; }
 
-// c[j] = sum over r (ascending) of expf(X[r, j] - m_r) / sum_r.  e is
-// recomputed from X (cheaper than writing it back and reading it again); X
-// chunks [64 rows x 128 keys] arrive by TMA, so many loads are in flight
-// without registers.
+// c[j] = sum over r (ascending) of e[r, j] / sum_r, reading the e rows the
+// row-sum pass wrote over X; chunks [64 rows x 128 keys] arrive by TMA, so
+// many loads are in flight without registers.
 __global__ void __launch_bounds__(XC_KEYS)
 score_exact_colsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int head_begin,
                    const int* __restrict__ rowmax, const float* __restrict__ rowsum,
                    float* __restrict__ colraw) {
     extern __shared__ uint8_t smem_raw[];
     XcHead& sm = smem_view<XcHead, 128>(smem_raw);
-    float4* rs = reinterpret_cast<float4*>(&sm + 1);  // per row: m, sum, RN(1/sum)
+    float4* rs = reinterpret_cast<float4*>(&sm + 1);  // per row: -, sum, RN(1/sum)
     float* xbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(rs) + xc_rs_bytes(lq));
     const int tid = threadIdx.x;
     const int hl = blockIdx.y;
     const int k0 = blockIdx.x * XC_KEYS;
+    (void)rowmax;
     const int n_chunks = (lq + XC_ROWS - 1) / XC_ROWS;
     const int n_st = min(n_chunks, XC_STAGES);
     const int row_base = hl * lq;
@@ -473,10 +478,9 @@ score_exact_colsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int 
             tma_load_2d(xbuf + c * XC_ROWS * XC_KEYS, &tm_x, &sm.full[c], k0, row_base + c * XC_ROWS);
         }
     }
-    exp2f_table_to_smem(sm.tab);
     for (int r = tid; r < lq; r += XC_KEYS) {
         const float sum = rowsum[row_base + r];
-        rs[r] = make_float4(dec_max(rowmax[row_base + r]), sum, __frcp_rn(sum), 0.0f);
+        rs[r] = make_float4(0.0f, sum, __frcp_rn(sum), 0.0f);
     }
     __syncthreads();
     const int j = k0 + tid;
@@ -493,14 +497,12 @@ score_exact_colsum(const __grid_constant__ CUtensorMap tm_x, int L, int lq, int 
 #pragma unroll 16
             for (int i = 0; i < XC_ROWS; ++i) {
                 const float4 w = rs[r0 + i];
-                const float e = expf_glibc(__fsub_rn(xs[i * XC_KEYS], w.x), sm.tab);
-                c = __fadd_rn(c, div_rn(e, w.y, w.z));
+                c = __fadd_rn(c, div_rn(xs[i * XC_KEYS], w.y, w.z));
             }
         } else {
             for (int i = max(0, r_first - r0); i < rn; ++i) {
                 const float4 w = rs[r0 + i];
-                const float e = expf_glibc(__fsub_rn(xs[i * XC_KEYS], w.x), sm.tab);
-                c = __fadd_rn(c, div_rn(e, w.y, w.z));
+                c = __fadd_rn(c, div_rn(xs[i * XC_KEYS], w.y, w.z));
             }
         }
         __syncthreads();  // the stage is refilled below
@@ -578,7 +580,7 @@ int launch_score_exact(const tsa_desc& d, const void* q, const void* k, const Ou
         const int smem = (int)sizeof(XbSmem) + 128;
         if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(score_exact_rowsum), smem))) return rc;
         score_exact_rowsum<<<(n_rows + rpc - 1) / rpc, XB_THREADS, smem, st>>>(
-            mx, L, lq, n_rows, rpc, rowmax, rowsum);
+            mx, X, L, Lp, lq, n_rows, rpc, rowmax, rowsum);
         TSA_LAUNCH_CHECK("score_exact_rowsum");
     }
     {
