@@ -488,6 +488,60 @@ EXTRA = {
 }
 
 
+def proj_compare(st, x0, tsa, iters=5):
+    """One cfg4 layer's producer and consumer: the fused tcgen05 projections the
+    stack runs against the unfused chain with cuBLAS GEMMs (rms_norm -> x W_qkv
+    -> split/RoPE; concat -> x += cat W_o), CUDA events, after warm-up."""
+    w = st.layers[0]
+    L, D = x0.shape
+    H, Hkv, d = st.H, st.Hkv, st.d
+    x = x0.clone()
+    xn = torch.empty_like(x0)
+    qkv = torch.empty((L, w.wqkv_t.shape[0]), dtype=x0.dtype, device=x0.device)
+    o = st.heads.q  # any [H, L, d] rows
+    cat = torch.empty((L, H * d), dtype=x0.dtype, device=x0.device)
+    stream = torch.cuda.current_stream(x0.device)
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record(stream)
+        for _ in range(iters):
+            fn()
+        e.record(stream)
+        torch.cuda.synchronize()
+        return round(s.elapsed_time(e) / iters, 3)
+
+    def prod_fused():
+        tsa.row_inv_rms(x, st.eps, out=st.inv_rms)
+        tsa.qkv_proj(x, w.wqkv_t, st.inv_rms, st.table, H, Hkv, d, out=st.heads)
+
+    def prod_cublas():
+        tsa.rms_norm(x, w.attn_norm, st.eps, out=xn)
+        torch.matmul(xn, w.wqkv, out=qkv)
+        tsa.split_heads_rope(qkv, st.table, H, Hkv, d, out=st.heads)
+
+    def cons_fused():
+        tsa.out_proj_residual(o, w.wo_t, x)
+
+    def cons_cublas():
+        tsa.heads_concat(o, out=cat)
+        x.addmm_(cat, w.wo)
+
+    r = {"producer_fused_ms": timed(prod_fused), "producer_cublas_chain_ms": timed(prod_cublas),
+         "consumer_fused_ms": timed(cons_fused), "consumer_cublas_chain_ms": timed(cons_cublas)}
+    fq = 2.0 * L * D * w.wqkv_t.shape[0]
+    fo = 2.0 * L * H * d * D
+    r["qkv_TFLOP_per_s"] = round(fq / (r["producer_fused_ms"] * 1e-3) / 1e12, 1)
+    r["out_TFLOP_per_s"] = round(fo / (r["consumer_fused_ms"] * 1e-3) / 1e12, 1)
+    r["speedup"] = round((r["producer_cublas_chain_ms"] + r["consumer_cublas_chain_ms"]) /
+                         (r["producer_fused_ms"] + r["consumer_fused_ms"]), 3)
+    del x, xn, qkv, cat
+    return r
+
+
 def run_cfg4(args, tsa, rank, world, device):
     """BASELINE configs[3]: the full 32-layer prefill attention stack at L = 64K
     (Llama-3-8B heads, d_model 4096, random-init layers, paper_2602_03216_b200/
@@ -565,7 +619,10 @@ def run_cfg4(args, tsa, rank, world, device):
         "k_keep_per_layer": kk,
         "k_over_L_mean": round(sum(kk) / (len(kk) * L), 4),
         "tokens_per_s": round(L / (out["ms"] * 1e-3), 1),
-        "gemm": "cuBLAS (torch.matmul / addmm): x W_qkv and cat W_o",
+        "gemm": "hand-written tcgen05 (proj_gemm.cu, 2-CTA 256x256 tiles): rms_norm scale + "
+                "RoPE + head split fused into the QKV GEMM, the residual add into the W_o GEMM "
+                "(reading o [H, L, d] directly, no concat)",
+        "projections_one_layer": proj_compare(st, x0, tsa),
     })
     del st, x, x0
     return out

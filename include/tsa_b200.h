@@ -337,6 +337,46 @@ TSA_API int tsa_split_heads_rope(const tsa_desc* d, const void* qkv, const float
 /* Head concat before W_o (model.cpp:196-200): heads [H][L][d] -> cat [L][H d]. */
 TSA_API int tsa_heads_concat(const tsa_desc* d, const void* heads, void* cat, void* stream);
 
+/* ---- The projections on the tensor cores, with the work around them fused ----
+ * Hand-written tcgen05 GEMMs (bf16 in, f32 accumulation in TMEM): one
+ * persistent kernel per projection, 128 x 256 tiles.  These replace the
+ * caller's BLAS calls of project_qkv (model.cpp:139-158) and the W_O
+ * projection (model.cpp:196-201) and absorb the passes around them. */
+
+/* c [M][N] = a [M][K] * b_t [N][K]^T (bf16, N % 256 == 0, K % 64 == 0). */
+TSA_API int tsa_gemm_bf16(const void* a, const void* b_t, void* c, int32_t M, int32_t N, int32_t K,
+                          void* stream);
+
+/* Weight layout for the projections, done once per weight: w_t [cols][rows]
+ * bf16 = (diag(gain) w)^T for w [rows][cols] (dtype TSA_F32 / TSA_BF16).  For
+ * W_qkv pass the attention-norm gain (rms_norm's gain folds into the weight);
+ * for W_o pass gain = NULL. */
+TSA_API int tsa_prepare_weight(const void* w, int32_t dtype, const float* gain, int32_t rows,
+                               int32_t cols, void* w_t, void* stream);
+
+/* inv[r] = 1 / sqrt(sum_j x[r, j]^2 / cols + eps) for bf16 x [rows][cols]
+ * (rms_norm's row statistic, model.cpp:81-94; cols % 8 == 0). */
+TSA_API int tsa_row_inv_rms(const void* x, int64_t rows, int32_t cols, float eps, float* inv,
+                            void* stream);
+
+/* project_qkv (model.cpp:128-158) with rms_norm (model.cpp:81-94) folded in,
+ * one GEMM: q [H][L][d], k / v [Hkv][L][d] = split_heads(rope(
+ * (inv_rms[t] * x[t]) W')) for x [L][d_model] bf16 and w_t from
+ * tsa_prepare_weight(W_qkv, gain) ([(H + 2 Hkv) d][d_model]); inv_rms from
+ * tsa_row_inv_rms (NULL: no norm); table from tsa_rope_table.  RoPE rotates in
+ * f32 (x0 c - x1 s, x0 s + x1 c) before the single bf16 rounding.  bf16,
+ * d_head 128, d_model % 64 == 0, (H + 2 Hkv) d % 256 == 0. */
+TSA_API int tsa_qkv_proj(const tsa_desc* d, const void* x, int32_t d_model, const void* w_t,
+                         const float* inv_rms, const float* table, void* q, void* k, void* v,
+                         void* stream);
+
+/* The W_O projection and residual (model.cpp:196-201): x [L][d_model] +=
+ * concat_h(o_h) W_o, reading o [H][L][d] directly (no concat buffer); wo_t =
+ * tsa_prepare_weight(W_o, NULL) ([d_model][H d]).  bf16, d_head 128,
+ * d_model % 256 == 0.  The sum is rounded to bf16 once. */
+TSA_API int tsa_out_proj_residual(const tsa_desc* d, const void* o, const void* wo_t,
+                                  int32_t d_model, void* x, void* stream);
+
 /* ---- Drift calibration (drift.hpp, drift.cpp:14-65) ----
  * compute_drift for one layer boundary: *r_out (device double) = mean over
  * the rows t of |next[t] - prev[t]|_2 / (|prev[t]|_2 + epsilon), with the

@@ -28,7 +28,8 @@ EXPORTS = (
     "tsa_layer_drift", "tsa_select_sparse_layers", "tsa_gather_zero_replicas",
     "tsa_attend_indexed_replicas", "tsa_score_replicas", "tsa_ipc_alloc", "tsa_ipc_open",
     "tsa_ipc_close", "tsa_ipc_free", "tsa_peer_barrier", "tsa_expf", "tsa_peer_check",
-    "tsa_sparse_attention_layer_sharded",
+    "tsa_sparse_attention_layer_sharded", "tsa_gemm_bf16", "tsa_prepare_weight",
+    "tsa_row_inv_rms", "tsa_qkv_proj", "tsa_out_proj_residual",
 )
 TSA_IPC_HANDLE_BYTES = 64
 TSA_MAX_REPLICAS = 8
@@ -85,6 +86,11 @@ def load() -> C.CDLL:
         "tsa_rope_table": (C.c_int, [I, I, C.c_float, P, P]),
         "tsa_split_heads_rope": (C.c_int, [D, P, P, P, P, P, P]),
         "tsa_heads_concat": (C.c_int, [D, P, P, P]),
+        "tsa_gemm_bf16": (C.c_int, [P, P, P, I, I, I, P]),
+        "tsa_prepare_weight": (C.c_int, [P, I, P, I, I, P, P]),
+        "tsa_row_inv_rms": (C.c_int, [P, C.c_int64, I, C.c_float, P, P]),
+        "tsa_qkv_proj": (C.c_int, [D, P, I, P, P, P, P, P, P, P]),
+        "tsa_out_proj_residual": (C.c_int, [D, P, P, I, P, P]),
         "tsa_layer_drift": (C.c_int, [P, P, C.c_int64, I, I, C.c_double, P, P, P]),
         "tsa_select_sparse_layers": (C.c_int, [P, I, C.c_double, P, P, P]),
         "tsa_sparse_attention_layer_host": (C.c_int, [D, P, P, P, P, P, P, P, P, P, P, P, P, I, P]),

@@ -528,6 +528,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return encode_fn(); }
+
 // 2-D map over a [rows x 128] bf16 matrix, 64-column x box_rows boxes, 128-B swizzle.
 int make_bf16_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
     auto fn = encode_fn();

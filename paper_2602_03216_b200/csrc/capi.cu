@@ -689,6 +689,41 @@ int tsa_heads_concat(const tsa_desc* d, const void* heads, void* cat, void* stre
     return launch_heads_concat(*d, heads, cat, S(stream));
 }
 
+// ---- the projections on the tensor cores (proj_gemm.cu) ----
+int tsa_gemm_bf16(const void* a, const void* b_t, void* c, int32_t M, int32_t N, int32_t K,
+                  void* stream) {
+    if (!a || !b_t || !c) return invalid("gemm_bf16: null pointer");
+    return launch_gemm_bf16(a, b_t, c, M, N, K, S(stream));
+}
+
+int tsa_prepare_weight(const void* w, int32_t dtype, const float* gain, int32_t rows, int32_t cols,
+                       void* w_t, void* stream) {
+    if (!w || !w_t) return invalid("prepare_weight: null pointer");
+    if (rows < 1 || cols < 1) return invalid("prepare_weight: bad shape");
+    if (dtype != TSA_F32 && dtype != TSA_BF16) return invalid("prepare_weight: unknown dtype");
+    return launch_prepare_weight(w, dtype, gain, rows, cols, w_t, S(stream));
+}
+
+int tsa_row_inv_rms(const void* x, int64_t rows, int32_t cols, float eps, float* inv, void* stream) {
+    if (!x || !inv) return invalid("row_inv_rms: null pointer");
+    if (rows < 0 || cols < 1) return invalid("row_inv_rms: bad shape");
+    return launch_row_inv_rms(x, rows, cols, eps, inv, S(stream));
+}
+
+int tsa_qkv_proj(const tsa_desc* d, const void* x, int32_t d_model, const void* w_t,
+                 const float* inv_rms, const float* table, void* q, void* k, void* v, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!x || !w_t || !table || !q || !k || !v) return invalid("qkv_proj: null pointer");
+    return launch_qkv_proj(*d, x, d_model, w_t, inv_rms, table, q, k, v, S(stream));
+}
+
+int tsa_out_proj_residual(const tsa_desc* d, const void* o, const void* wo_t, int32_t d_model,
+                          void* x, void* stream) {
+    if (int rc = check_desc(d)) return rc;
+    if (!o || !wo_t || !x) return invalid("out_proj_residual: null pointer");
+    return launch_out_proj_residual(*d, o, wo_t, d_model, x, S(stream));
+}
+
 // ---- drift calibration (drift.cpp:14-65) ----
 int tsa_layer_drift(const void* prev, const void* next, int64_t rows, int32_t cols, int32_t dtype,
                     double epsilon, double* r_out, void* ws, void* stream) {

@@ -169,6 +169,16 @@ int launch_rope_table(int seq_len, int d_head, float theta, float* table, cudaSt
 int launch_split_heads_rope(const tsa_desc& d, const void* qkv, const float* table, void* q,
                             void* k, void* v, cudaStream_t st);
 int launch_heads_concat(const tsa_desc& d, const void* heads, void* cat, cudaStream_t st);
+// proj_gemm.cu: the projections on the tensor cores with fused epilogues
+int launch_gemm_bf16(const void* a, const void* b_t, void* c, int M, int N, int K, cudaStream_t st);
+int launch_qkv_proj(const tsa_desc& d, const void* x, int d_model, const void* w_t,
+                    const float* inv_rms, const float* table, void* q, void* k, void* v,
+                    cudaStream_t st);
+int launch_out_proj_residual(const tsa_desc& d, const void* o, const void* wo_t, int d_model,
+                             void* x, cudaStream_t st);
+int launch_row_inv_rms(const void* x, int64_t rows, int cols, float eps, float* inv, cudaStream_t st);
+int launch_prepare_weight(const void* w, int dtype, const float* gain, int rows, int cols, void* w_t,
+                          cudaStream_t st);
 int launch_layer_drift(const void* prev, const void* next, int64_t rows, int cols, int dtype,
                        double eps, double* out, double* ratio_ws, cudaStream_t st);
 // attend_simt.cu / attend_sm100.cu

@@ -46,7 +46,8 @@ __all__ = [
     "fixed_budget", "select_tokens", "validate", "dense_causal_attention",
     "token_sparse_attention", "sparse_attention_layer", "InvalidArgument", "NativeLibraryError",
     "rms_norm", "rope_table", "split_heads_rope", "heads_concat", "sparse_attention_layer_host",
-    "layer_drift", "select_sparse_layers",
+    "layer_drift", "select_sparse_layers", "gemm_bf16", "prepare_weight", "row_inv_rms",
+    "qkv_proj", "out_proj_residual",
 ]
 
 
@@ -555,6 +556,95 @@ def heads_concat(heads: torch.Tensor, out: Optional[torch.Tensor] = None) -> tor
     _lib.check(_lib.load().tsa_heads_concat(C.byref(desc), _ptr(heads), _ptr(out),
                                             _stream(heads.device)))
     return out
+
+
+# ---- the projections on the tensor cores (proj_gemm.cu)
+def gemm_bf16(a: torch.Tensor, b_t: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """c [M, N] = a [M, K] b_t[N, K]^T on the hand-written tcgen05 GEMM (bf16,
+    f32 accumulation; N % 256 == 0, K % 64 == 0)."""
+    _require_cuda(a, b_t)
+    if a.dtype != torch.bfloat16 or b_t.dtype != torch.bfloat16:
+        raise InvalidArgument("gemm_bf16: a and b_t must be bf16")
+    M, K = a.shape
+    N = b_t.shape[0]
+    if b_t.shape[1] != K:
+        raise InvalidArgument(f"gemm_bf16: inner dimensions differ ({K} vs {b_t.shape[1]})")
+    a, b_t = a.contiguous(), b_t.contiguous()
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.bfloat16, device=a.device)
+    _lib.check(_lib.load().tsa_gemm_bf16(_ptr(a), _ptr(b_t), _ptr(out), M, N, K,
+                                         _stream(a.device)))
+    return out
+
+
+def prepare_weight(w: torch.Tensor, gain: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The projections' weight layout, once per weight: (diag(gain) w)^T as bf16
+    [cols, rows] for w [rows, cols] (f32 or bf16).  W_qkv takes the attention
+    norm's gain (rms_norm folds into the weight), W_o none."""
+    _require_cuda(w)
+    rows, cols = w.shape
+    w = w.contiguous()
+    g = None
+    if gain is not None:
+        if gain.numel() != rows:
+            raise InvalidArgument(f"prepare_weight: gain size {gain.numel()} != {rows} rows")
+        g = gain.to(torch.float32).contiguous()
+    out = torch.empty((cols, rows), dtype=torch.bfloat16, device=w.device)
+    _lib.check(_lib.load().tsa_prepare_weight(_ptr(w), _dtype_code(w), _ptr(g) if g is not None
+                                              else None, rows, cols, _ptr(out), _stream(w.device)))
+    return out
+
+
+def row_inv_rms(x: torch.Tensor, eps: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """rms_norm's row statistic (model.cpp:81-94): 1 / sqrt(mean_j x^2 + eps), f32 [rows]."""
+    _require_cuda(x)
+    if x.dtype != torch.bfloat16 or x.dim() != 2:
+        raise InvalidArgument("row_inv_rms: x must be bf16 [rows, cols]")
+    x = x.contiguous()
+    if out is None:
+        out = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+    _lib.check(_lib.load().tsa_row_inv_rms(_ptr(x), x.shape[0], x.shape[1], eps, _ptr(out),
+                                           _stream(x.device)))
+    return out
+
+
+def qkv_proj(x: torch.Tensor, w_t: torch.Tensor, inv_rms: Optional[torch.Tensor],
+             table: torch.Tensor, n_heads: int, n_kv_heads: int, d_head: int,
+             out: Optional[HeadTensors] = None) -> HeadTensors:
+    """project_qkv with rms_norm folded in (model.cpp:81-94, 128-158), one tcgen05
+    GEMM: q / k / v heads of rope((inv_rms * x) W') with w_t = prepare_weight(W_qkv,
+    gain) and the RoPE table of rope_table."""
+    _require_cuda(x, w_t, table)
+    L, D = x.shape
+    if w_t.shape != ((n_heads + 2 * n_kv_heads) * d_head, D):
+        raise InvalidArgument("qkv_proj: w_t must be [(H + 2 Hkv) d, d_model]")
+    if out is None:
+        out = HeadTensors(torch.empty((n_heads, L, d_head), dtype=x.dtype, device=x.device),
+                          torch.empty((n_kv_heads, L, d_head), dtype=x.dtype, device=x.device),
+                          torch.empty((n_kv_heads, L, d_head), dtype=x.dtype, device=x.device))
+    desc = _desc_for(n_heads, n_kv_heads, L, d_head, _dtype_code(x))
+    x = x.contiguous()
+    _lib.check(_lib.load().tsa_qkv_proj(C.byref(desc), _ptr(x), D, _ptr(w_t),
+                                        _ptr(inv_rms) if inv_rms is not None else None,
+                                        _ptr(table), _ptr(out.q), _ptr(out.k), _ptr(out.v),
+                                        _stream(x.device)))
+    return out
+
+
+def out_proj_residual(o: torch.Tensor, wo_t: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+    """x += concat_h(o_h) W_o in place (model.cpp:196-201), A read from o [H, L, d]
+    directly; wo_t = prepare_weight(W_o)."""
+    _require_cuda(o, wo_t, x)
+    H, L, d = o.shape
+    D = x.shape[1]
+    if x.shape[0] != L or wo_t.shape != (D, H * d):
+        raise InvalidArgument("out_proj_residual: shapes do not match")
+    if not (o.is_contiguous() and x.is_contiguous()):
+        raise InvalidArgument("out_proj_residual: o and x must be contiguous")
+    desc = _desc_for(H, H, L, d, _dtype_code(o))
+    _lib.check(_lib.load().tsa_out_proj_residual(C.byref(desc), _ptr(o), _ptr(wo_t), D, _ptr(x),
+                                                 _stream(o.device)))
+    return x
 
 
 _staging: dict = {}

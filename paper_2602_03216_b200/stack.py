@@ -3,12 +3,17 @@
 Each layer is the attention branch of the reference's ``layer_forward``
 (model.cpp:169-201) on the residual stream x [L, d_model]:
 
-    xn  = rms_norm(x, attn_norm, eps)                 tsa_rms_norm       (model.cpp:81-94)
-    qkv = xn [W_q | W_k | W_v]                        cuBLAS GEMM        (model.cpp:139-158)
-    q, k, v = split_heads + RoPE at 0..L-1            tsa_split_heads_rope
+    q, k, v = split_heads(rope(rms_norm(x, attn_norm, eps) [W_q | W_k | W_v]))
+                                  tsa_row_inv_rms + tsa_qkv_proj: one tcgen05 GEMM
+                                  (model.cpp:81-94, 128-158); rms_norm's 1/rms
+                                  scales the accumulator, its gain is folded
+                                  into the weight, RoPE and the head split are
+                                  the epilogue
     o   = sparse attention layer (score -> budget -> select -> gather -> attend)
-                                                      the path (this package)
-    x  += concat_h(o_h) W_o                           tsa_heads_concat + cuBLAS GEMM
+                                  the path (this package)
+    x  += concat_h(o_h) W_o       tsa_out_proj_residual: one tcgen05 GEMM reading
+                                  o [H, L, d] directly, the residual add in the
+                                  epilogue (model.cpp:196-201)
 
 The FFN half of layer_forward (SwiGLU) is outside the attention stack.  Only
 one B200 is in this build, so the stack runs single-process (``world`` = 1);
@@ -41,9 +46,19 @@ from .ops import SparsePlan
 @dataclass
 class StackLayer:
     attn_norm: torch.Tensor   # [D] f32 (ones)
-    wqkv: torch.Tensor        # [D, (H + 2 Hkv) d]: W_q | W_k | W_v
-    wo: torch.Tensor          # [H d, D]
+    wqkv_t: torch.Tensor      # [(H + 2 Hkv) d, D] = (diag(attn_norm) [W_q | W_k | W_v])^T
+    wo_t: torch.Tensor        # [D, H d] = W_o^T
     qk_gain: float
+
+    @property
+    def wqkv(self) -> torch.Tensor:
+        """[D, (H + 2 Hkv) d] W_q | W_k | W_v (a view; exact while attn_norm is ones)."""
+        return self.wqkv_t.t()
+
+    @property
+    def wo(self) -> torch.Tensor:
+        """[H d, D] W_o (a view)."""
+        return self.wo_t.t()
 
 
 def _xavier(rows: int, cols: int, gen: torch.Generator, device, gain: float = 1.0) -> torch.Tensor:
@@ -92,23 +107,22 @@ class PrefillAttentionStack:
             wk = _xavier(d_model, Wkv, g, device, qk_gain[i])
             wv = _xavier(d_model, Wkv, g, device)
             wo = _xavier(Wq, d_model, g, device)
+            norm = torch.ones(d_model, dtype=torch.float32, device=device)
+            wqkv = torch.cat([wq, wk, wv], dim=1).to(dtype)
             self.layers.append(StackLayer(
-                attn_norm=torch.ones(d_model, dtype=torch.float32, device=device),
-                wqkv=torch.cat([wq, wk, wv], dim=1).to(dtype).contiguous(),
-                wo=wo.to(dtype).contiguous(), qk_gain=qk_gain[i]))
-            del wq, wk, wv, wo
+                attn_norm=norm, wqkv_t=ops.prepare_weight(wqkv, norm),
+                wo_t=ops.prepare_weight(wo.to(dtype)), qk_gain=qk_gain[i]))
+            del wq, wk, wv, wo, wqkv
         self.scoring = scoring
         self.attn = ShardedSparseAttention(n_heads, n_kv_heads, seq_len, d_head, dtype, plan,
                                            device=device, scoring=scoring)
         # persistent buffers: the whole forward is a fixed launch sequence
         self.table = ops.rope_table(seq_len, d_head, rope_theta, device)
-        self.xn = torch.empty((seq_len, d_model), dtype=dtype, device=device)
-        self.qkv = torch.empty((seq_len, Wq + 2 * Wkv), dtype=dtype, device=device)
+        self.inv_rms = torch.empty(seq_len, dtype=torch.float32, device=device)
         self.heads = ops.HeadTensors(
             torch.empty((n_heads, seq_len, d_head), dtype=dtype, device=device),
             torch.empty((n_kv_heads, seq_len, d_head), dtype=dtype, device=device),
             torch.empty((n_kv_heads, seq_len, d_head), dtype=dtype, device=device))
-        self.cat = torch.empty((seq_len, Wq), dtype=dtype, device=device)
         self.k_keep = torch.zeros(n_layers, dtype=torch.int32, device=device)
 
     def set_plan(self, plan: SparsePlan) -> None:
@@ -121,9 +135,9 @@ class PrefillAttentionStack:
         """One attention branch in place on the residual stream x [L, D]."""
         mark = marks or (lambda name: None)
         w = self.layers[i]
-        ops.rms_norm(x, w.attn_norm, self.eps, out=self.xn)
-        torch.matmul(self.xn, w.wqkv, out=self.qkv)
-        ops.split_heads_rope(self.qkv, self.table, self.H, self.Hkv, self.d, out=self.heads)
+        ops.row_inv_rms(x, self.eps, out=self.inv_rms)
+        ops.qkv_proj(x, w.wqkv_t, self.inv_rms, self.table, self.H, self.Hkv, self.d,
+                     out=self.heads)
         mark("producer")
         o = self.attn.step(self.heads.q, self.heads.k, self.heads.v, dense=dense)
         if dense:
@@ -131,8 +145,7 @@ class PrefillAttentionStack:
         else:
             self.k_keep[i].copy_(self.attn.backend.k_keep[0])
         mark("attention")
-        ops.heads_concat(o, out=self.cat)
-        x.addmm_(self.cat, w.wo)
+        ops.out_proj_residual(o, w.wo_t, x)
         mark("consumer")
         return x
 

@@ -47,3 +47,21 @@ def test_attention_mma_operands_stay_uniform(attend_sass, kind):
     # the only broadcasts are the gather4 issue loop's (indexed: 10 row indices)
     assert s.count("R2UR.BROADCAST") <= (12 if kind == "indexed" else 0)
     assert s.count("R2UR ") <= 16
+
+
+def test_projection_gemm_sass_is_2cta_tcgen05():
+    """proj_gemm.cu: every instantiation issues cta_group::2 MMAs
+    (UTCHMMA.2CTA) fed by pair TMA loads (UTMALDG.*.2CTA), reads the
+    accumulator with LDTM, and does not spill."""
+    if not LIB.exists() or not Path(CUOBJDUMP).exists():
+        pytest.skip("library not built or cuobjdump absent")
+    txt = subprocess.run([CUOBJDUMP, "-sass", str(LIB)], capture_output=True, text=True,
+                         check=True).stdout
+    parts = [p for p in re.split(r"\n\s*Function : ", txt)
+             if "proj_gemm_kernel" in p.split("\n", 1)[0]]
+    assert len(parts) == 3, len(parts)   # STORE, QKV, OUT (3-D A map)
+    for p in parts:
+        assert p.count("UTCHMMA.2CTA") >= 4
+        assert re.search(r"UTMALDG\.[23]D\.2CTA", p)
+        assert "LDTM" in p
+        assert "LDL" not in p and "STL" not in p
