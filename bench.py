@@ -656,7 +656,40 @@ def run_cfg1(args, tsa, rank, world, device):
     o_gpu, st = tsa.sparse_attention_layer(heads, plan)
     res = {"workload": "cfg1: one attention layer, Llama-3-8B heads (32 Q / 8 KV, d=128), "
                        "L=4096, fp32 uniform inputs, tau=0.5", "gpu_ms": round(gpu_ms, 3),
-           "k_keep": st.k_keep, "dtype": "f32 (REFERENCE-order scoring, register-tiled f32 attention on the CUDA cores)"}
+           "k_keep": st.k_keep,
+           "dtype": "f32 (REFERENCE-order scoring; attention on the tensor cores as 3xTF32, "
+                    "attend_tf32.cu)"}
+    # the attention alone on the compressed rows (dense causal over k per head),
+    # against the tensor pipe: 3 TF32 MMAs per product, TF32 dense = half the bf16 rate
+    kk = st.k_keep
+    idx = st.selection.indices.long()
+    grp = H // HKV
+    qc = torch.gather(q, 1, idx[:, :, None].expand(-1, -1, D)).contiguous()
+    kvi = idx[:, :, None].expand(-1, -1, D)
+    kc = torch.gather(k.repeat_interleave(grp, 0), 1, kvi).contiguous()
+    vc = torch.gather(v.repeat_interleave(grp, 0), 1, kvi).contiguous()
+    hc = tsa.HeadTensors(qc, kc, vc)
+    oc = torch.empty_like(qc)
+    for _ in range(3):
+        tsa.sparse_attention_layer(hc, tsa.SparsePlan(), out=oc, stat=False)
+    torch.cuda.synchronize()
+    s.record(stream)
+    for _ in range(n):
+        tsa.sparse_attention_layer(hc, tsa.SparsePlan(), out=oc, stat=False)
+    e.record(stream)
+    torch.cuda.synchronize()
+    att_ms = s.elapsed_time(e) / n
+    _, _, bf16_sust, peak_src = measured_peaks()
+    tf32_peak = bf16_sust / 2
+    achieved = 3 * f_attn(kk, D, H) / (att_ms * 1e-3) / 1e12
+    res["attention"] = {
+        "kernel": "attend_tf32_kernel (3xTF32 tcgen05, S double-buffered in TMEM)",
+        "ms": round(att_ms, 4), "f32_equiv_TFLOP_per_s": round(f_attn(kk, D, H) / (att_ms * 1e-3) / 1e12, 1),
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(tf32_peak, 1),
+                     "unit": "TFLOP/s (TF32 MMA work: 3 per f32 product)",
+                     "frac": round(achieved / tf32_peak, 4),
+                     "peak_kind": f"half the {peak_src} sustained bf16 rate (dense TF32 = 1/2 bf16)"}}
+    del qc, kc, vc, oc, hc
     if not args.no_cpu_baseline:
         ora = Oracle("port")
         T = n_threads_default()

@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtsa_b200.so"
 SOURCES = ["capi.cu", "sharded.cu", "score.cu", "score_fast.cu", "score_exact.cu", "select.cu", "gather_scatter.cu", "attend_simt.cu",
-           "attend_sm100.cu", "graph.cu", "producer.cu", "proj_gemm.cu", "peer.cu"]
+           "attend_sm100.cu", "attend_tf32.cu", "graph.cu", "producer.cu", "proj_gemm.cu", "peer.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

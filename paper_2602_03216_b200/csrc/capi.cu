@@ -156,6 +156,8 @@ int attend_dispatch(const tsa_desc& d, const void* q, const void* k, const void*
                     cudaStream_t st) {
     if (attend_sm100_supported(d))
         return launch_attend_sm100(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
+    if (attend_tf32_supported(d))
+        return launch_attend_tf32(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
     return launch_attend_simt(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
 }
 

@@ -190,6 +190,11 @@ int launch_attend_sm100(const tsa_desc& d, const void* q, const void* k, const v
                         int32_t rows_per_head, int32_t kv_rows_per_head, void* o,
                         cudaStream_t st);
 bool attend_sm100_supported(const tsa_desc& d);
+// attend_tf32.cu: f32, d = 128 on the tensor cores (3xTF32)
+bool attend_tf32_supported(const tsa_desc& d);
+int launch_attend_tf32(const tsa_desc& d, const void* q, const void* k, const void* v,
+                       const int32_t* n_dev, int32_t n_const, int32_t kv_group,
+                       int32_t rows_per_head, int32_t kv_rows_per_head, void* o, cudaStream_t st);
 int launch_attend_sm100_rep(const tsa_desc& d, const void* q, const void* k, const void* v,
                             const OutReplicas& o, cudaStream_t st);
 // capi.cu (shared with sharded.cu)

@@ -65,3 +65,19 @@ def test_projection_gemm_sass_is_2cta_tcgen05():
         assert re.search(r"UTMALDG\.[23]D\.2CTA", p)
         assert "LDTM" in p
         assert "LDL" not in p and "STL" not in p
+
+
+def test_tf32_attention_sass_is_tcgen05():
+    """attend_tf32.cu: the f32 attention runs on the tensor cores (UTCHMMA,
+    TMA 3-D loads, LDTM / STTM for S, P and O) without spills."""
+    if not LIB.exists() or not Path(CUOBJDUMP).exists():
+        pytest.skip("library not built or cuobjdump absent")
+    txt = subprocess.run([CUOBJDUMP, "-sass", str(LIB)], capture_output=True, text=True,
+                         check=True).stdout
+    parts = [p for p in re.split(r"\n\s*Function : ", txt)
+             if "attend_tf32_kernel" in p.split("\n", 1)[0]]
+    assert len(parts) == 1
+    p = parts[0]
+    assert p.count("UTCHMMA") >= 24 and "UTMALDG.3D" in p
+    assert "LDTM" in p and "STTM" in p
+    assert "LDL" not in p and "STL" not in p
