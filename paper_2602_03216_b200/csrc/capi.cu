@@ -497,7 +497,7 @@ namespace {
 struct HostPipe {
     cudaStream_t in = nullptr, out = nullptr;
     cudaEvent_t start = nullptr, kvq = nullptr, q[64] = {}, done[64] = {}, vr[64] = {},
-                fin = nullptr;
+                kr[64] = {}, fin = nullptr;
 };
 // One pipeline (copy streams + events) per calling thread and device: two
 // threads' host-tensor calls never share streams or events (the reference's
@@ -518,7 +518,8 @@ HostPipe* host_pipe(int device) {
         for (int g = 0; g < 64; ++g)
             if (cudaEventCreateWithFlags(&p.q[g], f) != cudaSuccess ||
                 cudaEventCreateWithFlags(&p.done[g], f) != cudaSuccess ||
-                cudaEventCreateWithFlags(&p.vr[g], f) != cudaSuccess)
+                cudaEventCreateWithFlags(&p.vr[g], f) != cudaSuccess ||
+                cudaEventCreateWithFlags(&p.kr[g], f) != cudaSuccess)
                 return nullptr;
         init[device] = true;
     }
@@ -571,12 +572,20 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
     TSA_HCK(cudaEventRecord(p->start, st));  // the device buffers are free after prior work
     TSA_HCK(cudaStreamWaitEvent(p->in, p->start, 0));
     TSA_HCK(cudaStreamWaitEvent(p->out, p->start, 0));
-    // scoring inputs first: all of K and the Q tail rows of every head
-    TSA_HCK(cudaMemcpyAsync(k, k_host, Hkv * head_bytes, cudaMemcpyHostToDevice, p->in));
+    // scoring inputs first: the Q tail rows of every head, then K one KV head at a
+    // time -- the scoring of a KV group starts as soon as its K rows have arrived,
+    // so all but the last group's scoring hides under the K copy
     const size_t tail_off = (L - lq) * D * eb;
     TSA_HCK(cudaMemcpy2DAsync(qd + tail_off, head_bytes, qh + tail_off, head_bytes, lq * D * eb, H,
                               cudaMemcpyHostToDevice, p->in));
-    TSA_HCK(cudaEventRecord(p->kvq, p->in));
+    const int score_groups = Hkv <= 64 ? Hkv : 1;
+    for (int i = 0; i < score_groups; ++i) {
+        const size_t kv0 = (size_t)i * (Hkv / score_groups), nkv = Hkv / score_groups;
+        TSA_HCK(cudaMemcpyAsync(static_cast<uint8_t*>(k) + kv0 * head_bytes,
+                                static_cast<const uint8_t*>(k_host) + kv0 * head_bytes,
+                                nkv * head_bytes, cudaMemcpyHostToDevice, p->in));
+        TSA_HCK(cudaEventRecord(p->kr[i], p->in));
+    }
     // Compute chunks: whole head groups, except the first and the last group,
     // which run head by head -- the first attention then waits for one head's
     // Q rows (not a group's) and the last copy back is one head's rows (not a
@@ -610,8 +619,7 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
                                       p->in));
         TSA_HCK(cudaEventRecord(p->q[c], p->in));
     }
-    // score -> budget -> select on the compute stream
-    TSA_HCK(cudaStreamWaitEvent(st, p->kvq, 0));
+    // score (KV group by KV group, as K arrives) -> budget -> select on the compute stream
     const Workspace w = workspace_layout(*d);
     float* s = at<float>(ws, w.scores);
     int32_t* idx = idx_out ? idx_out : at<int32_t>(ws, w.idx);
@@ -619,7 +627,13 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
     const int fb = forced_begin(*d);
     const int nf = d->seq_len - fb;
     int rc;
-    if ((rc = tsa_score(d, q, k, s, ws, stream))) return rc;
+    for (int i = 0; i < score_groups; ++i) {
+        tsa_desc ds = *d;
+        ds.head_begin = i * (H / score_groups);
+        ds.head_end = (i + 1) * (H / score_groups);
+        TSA_HCK(cudaStreamWaitEvent(st, p->kr[i], 0));
+        if ((rc = tsa_score(&ds, q, k, s, ws, stream))) return rc;
+    }
     if ((rc = budget_impl(*d, s, k_keep_out, ws, std::max(1, nf), st))) return rc;
     if ((rc = launch_select(*d, s, k_keep_out, nullptr, nf, fb, idx, inv, st))) return rc;
     // per chunk: compress K/V of its group (+ zero the group's dropped rows) once,

@@ -380,6 +380,7 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
             for (int i = 0; i < RH; ++i) xv[i] = xs[i * XB_KEYS];
             // e overwrites X in HBM (the column pass reads it: the exponentials run once)
             float* xg = X + (size_t)(row0 + rbase) * Lp + key;
+            if (rbase < R)  // (warp-uniform) a half with no live rows skips its exponentials
 #pragma unroll
             for (int i = 0; i < RH; ++i) {
                 // masked entries add +0 to the chain: exactly the reference's skip
