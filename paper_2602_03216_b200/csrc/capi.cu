@@ -572,13 +572,15 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
     TSA_HCK(cudaEventRecord(p->start, st));  // the device buffers are free after prior work
     TSA_HCK(cudaStreamWaitEvent(p->in, p->start, 0));
     TSA_HCK(cudaStreamWaitEvent(p->out, p->start, 0));
-    // scoring inputs first: the Q tail rows of every head, then K one KV head at a
-    // time -- the scoring of a KV group starts as soon as its K rows have arrived,
-    // so all but the last group's scoring hides under the K copy
+    // scoring inputs first: the Q tail rows of every head, then K two KV heads at
+    // a time -- their scoring starts as soon as their K rows have arrived, so all
+    // but the last pair's scoring hides under the K copy
     const size_t tail_off = (L - lq) * D * eb;
     TSA_HCK(cudaMemcpy2DAsync(qd + tail_off, head_bytes, qh + tail_off, head_bytes, lq * D * eb, H,
                               cudaMemcpyHostToDevice, p->in));
-    const int score_groups = Hkv <= 64 ? Hkv : 1;
+    // two KV heads per scoring launch: each launch's row-sum chain costs its full
+    // L-long latency, so one launch per KV head would fall behind the copy
+    const int score_groups = Hkv > 64 ? 1 : (Hkv % 2 == 0 ? Hkv / 2 : Hkv);
     for (int i = 0; i < score_groups; ++i) {
         const size_t kv0 = (size_t)i * (Hkv / score_groups), nkv = Hkv / score_groups;
         TSA_HCK(cudaMemcpyAsync(static_cast<uint8_t*>(k) + kv0 * head_bytes,
@@ -586,16 +588,18 @@ int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host, const
                                 nkv * head_bytes, cudaMemcpyHostToDevice, p->in));
         TSA_HCK(cudaEventRecord(p->kr[i], p->in));
     }
-    // Compute chunks: whole head groups, except the first and the last group,
-    // which run head by head -- the first attention then waits for one head's
-    // Q rows (not a group's) and the last copy back is one head's rows (not a
-    // group's): the two ends of the pipeline that the PCIe copies expose.
+    // Compute chunks: one query head each (a group's K/V are compressed once, before
+    // its first head) -- an attention waits for one head's Q rows, not a group's,
+    // so the copies stay ahead of the compute after the first group (whole groups
+    // left the compute idle at every group boundary), and the last copy back is
+    // one head's rows.  More than 64 heads: whole groups, the ends head by head.
     struct Chunk { int h0, h1, gi; };
     Chunk chunks[64];
     int nc = 0;
+    const bool per_head = H <= 64;
     const bool split_ends = G >= 2 && hpg > 1 && (G - 2) + 2 * hpg <= 64;
     for (int gi = 0; gi < G; ++gi) {
-        if (split_ends && (gi == 0 || gi == G - 1))
+        if (per_head || (split_ends && (gi == 0 || gi == G - 1)))
             for (int h = gi * hpg; h < (gi + 1) * hpg; ++h) chunks[nc++] = {h, h + 1, gi};
         else
             chunks[nc++] = {gi * hpg, (gi + 1) * hpg, gi};

@@ -652,12 +652,19 @@ _staging: dict = {}
 
 def sparse_attention_layer_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                                 out: torch.Tensor, plan: SparsePlan, device=None,
-                                n_groups: int = 0, scoring: int = 0) -> torch.Tensor:
+                                n_groups: int = 0, scoring: int = 0,
+                                overlap: bool = True) -> torch.Tensor:
     """The sparse layer on HOST tensors (the reference's calling convention):
     q [H, L, d], k / v [Hkv, L, d] and out [H, L, d] in (pinned) host memory.
     Transfers are pipelined with the compute (tsa_sparse_attention_layer_host);
     returns the device k_keep (int32[1]); ``out`` is complete once the current
-    stream of ``device`` has drained."""
+    stream of ``device`` has drained.
+
+    overlap (default): consecutive calls alternate between two device staging
+    sets, each on its own stream, so a call's K copy and scoring overlap the
+    previous call's attention (the copies of one call only wait for the call
+    before the last, which used the same buffers).  The returned k_keep stays
+    valid until the call after next."""
     device = torch.device(device or "cuda")
     for t in (q, k, v, out):
         if t.is_cuda:
@@ -667,19 +674,30 @@ def sparse_attention_layer_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tenso
     desc = _desc_for(H, Hkv, L, d, _dtype_code(q), mode=int(plan.mode), tau=plan.tau,
                      s_fixed=plan.s_fixed, last_q=plan.last_q, kernel=plan.kernel,
                      forced_policy=int(plan.forced), scoring=scoring)
-    key = _stream_key(device) + (q.dtype, H, Hkv, L, d)
+    key = _stream_key(device) + (q.dtype, H, Hkv, L, d, bool(overlap))
     with _cache_lock:
-        bufs = _staging.get(key)
-        if bufs is None:
-            bufs = _staging[key] = (
-                torch.empty_like(q, device=device), torch.empty_like(k, device=device),
-                torch.empty_like(v, device=device), torch.empty_like(out, device=device),
-                torch.empty(1, dtype=torch.int32, device=device))
+        ent = _staging.get(key)
+        if ent is None:
+            sets = []
+            for _ in range(2 if overlap else 1):
+                side = torch.cuda.Stream(device) if overlap else None
+                sets.append((side, (
+                    torch.empty_like(q, device=device), torch.empty_like(k, device=device),
+                    torch.empty_like(v, device=device), torch.empty_like(out, device=device),
+                    torch.empty(1, dtype=torch.int32, device=device))))
+            ent = _staging[key] = [0, sets]
+        i = ent[0]
+        ent[0] = (i + 1) % len(ent[1])
+        side, bufs = ent[1][i]
     qd, kd, vd, od, kk = bufs
-    ws = _workspace(desc, device)
-    _lib.check(_lib.load().tsa_sparse_attention_layer_host(
-        C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(qd), _ptr(kd), _ptr(vd),
-        _ptr(od), None, _ptr(kk), None, _ptr(ws), n_groups, _stream(device)))
+    cur = torch.cuda.current_stream(device)
+    with torch.cuda.stream(side if side is not None else cur):
+        ws = _workspace(desc, device)  # per stream: each staging set has its own
+        _lib.check(_lib.load().tsa_sparse_attention_layer_host(
+            C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(qd), _ptr(kd), _ptr(vd),
+            _ptr(od), None, _ptr(kk), None, _ptr(ws), n_groups, _stream(device)))
+    if side is not None:
+        cur.wait_stream(side)  # `out` complete once the caller's stream drains
     return kk
 
 

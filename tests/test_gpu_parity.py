@@ -540,6 +540,31 @@ def test_host_api_equals_device_layer_bitwise(cuda, dtype, L):
                            ref.cpu().view(torch.int16 if dtype == torch.bfloat16 else torch.int32))
 
 
+def test_host_api_back_to_back_calls_overlap_correctly(cuda):
+    """Consecutive host-API calls without a sync alternate staging sets on two
+    streams (a call's copies and scoring overlap the previous call's attention):
+    three calls on different inputs into different outputs, one sync, each
+    output and budget equal to its own device-resident layer."""
+    from paper_2602_03216_b200 import workloads
+    plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=0.02)
+    cases = []
+    for seed in (31, 32, 33):
+        q, k, v = workloads.heavy_tailed_heads(8, 2, 2500, 128, seed=seed)
+        ref, st = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), plan)
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        hout = torch.full(q.shape, 7.0, dtype=q.dtype).pin_memory()
+        cases.append((hq, hk, hv, hout, ref.cpu(), st.k_keep))
+    torch.cuda.synchronize()
+    kks = []
+    for hq, hk, hv, hout, _, _ in cases:
+        # (the clone is ordered on the caller's stream after the call's work)
+        kks.append(tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan).clone())
+    torch.cuda.synchronize()
+    for (hq, hk, hv, hout, ref, k_ref), kk in zip(cases, kks):
+        assert int(kk.item()) == k_ref
+        assert torch.equal(hout.view(torch.int16), ref.view(torch.int16))
+
+
 def _full_size_check(port, q, k, v, tau, rows=256, head_stride=16, plan=None):
     """Default (exact) scoring at full size: scores bit-identical to the oracle,
     k_keep equal to the reference's, every index set identical, sampled
