@@ -339,8 +339,8 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
             mbar_init(&sm.x_empty[s], XB_HELP);
         }
         for (int s = 0; s < XB_STAGES; ++s) {
-            mbar_init(&sm.e_full[s], XB_HELP);
-            mbar_init(&sm.e_empty[s], 1);
+            mbar_init(&sm.e_full[s], XB_HELP * 32);
+            mbar_init(&sm.e_empty[s], 32);
         }
         fence_barrier_init();
     }
@@ -389,11 +389,10 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
                 es[i] = ok ? e : 0.0f;
                 if (ok) __stcs(xg + (size_t)i * Lp, e);
             }
+            // every helper thread publishes its own e writes (release) to the chain warp
+            mbar_arrive(&sm.e_full[st]);
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&sm.x_empty[xt]);
-                mbar_arrive(&sm.e_full[st]);
-            }
+            if (lane == 0) mbar_arrive(&sm.x_empty[xt]);
         }
     } else {
         // the sequential f32 row sums, lane = row (tensor_ops.cpp:59-65)
@@ -419,8 +418,7 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
 #pragma unroll
                 for (int i = 0; i < 32; ++i) cur[i] = nxt[i];
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.e_empty[st]);
+            mbar_arrive(&sm.e_empty[st]);  // each lane's reads of the stage are done
         }
         if (lane < R && row0 + lane < n_rows) rowsum[row0 + lane] = s;
     }

@@ -1,6 +1,9 @@
 """Small end-to-end runs of every production path, for compute-sanitizer:
 FAST bf16 layer (fused gather/attend), tau = 0 in-place, fixed mode, f32
-reference-order layer, host-tensor pipeline, dense, producer kernels."""
+reference-order layer, host-tensor pipeline (back-to-back, overlapping), dense, the
+3xTF32 f32 attention, the exact budget total (chunk-monoid walk), the fused tcgen05
+projections (2-CTA GEMM) and the row statistic / weight layout kernels."""
+import math
 import sys
 
 import torch
@@ -20,8 +23,22 @@ for L in (1000, 1537):
         hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
         hout = torch.empty(q.shape, dtype=q.dtype).pin_memory()
         tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan, n_groups=2)
+        tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan)  # back to back, overlapping
     hf = tsa.HeadTensors(q.float(), k.float(), v.float())
     tsa.sparse_attention_layer(hf, tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0],
                                                   tau=0.3))
+    # exact total on adversarial values (ties, crossings) through aggregate_scores
+    x = torch.linspace(-20, 5, 40000, device="cuda").exp()[None]
+    tsa.aggregate_scores(tsa.HeadScores(x))
+# projections: QKV with norm / RoPE / split, W_o with residual, plain GEMM (ragged M)
+L, D, H, Hkv = 300, 512, 4, 2
+x = torch.randn((L, D), device="cuda").to(torch.bfloat16)
+w = (torch.randn((D, (H + 2 * Hkv) * 128), device="cuda") / math.sqrt(D)).to(torch.bfloat16)
+wo = (torch.randn((H * 128, D), device="cuda") / 16).to(torch.bfloat16)
+table = tsa.rope_table(L, 128, 10000.0, "cuda")
+heads = tsa.qkv_proj(x, tsa.prepare_weight(w, torch.ones(D, device="cuda")),
+                     tsa.row_inv_rms(x, 1e-5), table, H, Hkv, 128)
+tsa.out_proj_residual(heads.q.contiguous(), tsa.prepare_weight(wo), x)
+tsa.gemm_bf16(x, tsa.prepare_weight(w))
 torch.cuda.synchronize()
 print("sanitize_small done")
