@@ -147,3 +147,31 @@ def test_out_proj_matches_concat_addmm(cuda):
     tsa.out_proj_residual(o, tsa.prepare_weight(wo), x)
     x2.addmm_(tsa.heads_concat(o), wo)
     close(x, x2)
+
+
+def test_projections_at_cfg4_size_sampled_rows(cuda):
+    """cfg4's per-layer shapes (L = 65536, d_model 4096, 32 / 8 heads): the fused
+    QKV projection and the W_o projection + residual, sampled rows against fp32
+    (the kernels run every tile; the check reads 512 rows spread over L, so
+    every M tile position class and all N tiles are covered)."""
+    L, D, H, Hkv, d = 65536, 4096, 32, 8, 128
+    x = rnd(L, D, seed=20)
+    gain = torch.rand(D, device="cuda") + 0.5
+    w = (torch.randn(D, (H + 2 * Hkv) * d, device="cuda") / math.sqrt(D)).to(torch.bfloat16)
+    table = tsa.rope_table(L, d, 500000.0, "cuda")
+    heads = tsa.qkv_proj(x, tsa.prepare_weight(w, gain), tsa.row_inv_rms(x, 1e-5), table, H,
+                         Hkv, d)
+    rows = torch.linspace(0, L - 1, 512, device="cuda").long()
+    xf = x[rows].float()
+    xn = xf / torch.sqrt(xf.pow(2).mean(1, keepdim=True) + 1e-5) * gain
+    p = (xn @ w.float()).view(-1, H + 2 * Hkv, d)
+    p[:, :H + Hkv] = rope_ref(p[:, :H + Hkv], table[rows])
+    close(heads.q[:, rows], p[:, :H].permute(1, 0, 2))
+    close(heads.k[:, rows], p[:, H:H + Hkv].permute(1, 0, 2))
+    close(heads.v[:, rows], p[:, H + Hkv:].permute(1, 0, 2))
+    wo = (torch.randn(H * d, D, device="cuda") / math.sqrt(H * d)).to(torch.bfloat16)
+    o = heads.q
+    x0 = x[rows].float()
+    tsa.out_proj_residual(o, tsa.prepare_weight(wo), x)
+    ref = x0 + o[:, rows].permute(1, 0, 2).reshape(-1, H * d).float() @ wo.float()
+    close(x[rows], ref)
