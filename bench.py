@@ -536,6 +536,11 @@ def proj_compare(st, x0, tsa, iters=5):
     fo = 2.0 * L * H * d * D
     r["qkv_TFLOP_per_s"] = round(fq / (r["producer_fused_ms"] * 1e-3) / 1e12, 1)
     r["out_TFLOP_per_s"] = round(fo / (r["consumer_fused_ms"] * 1e-3) / 1e12, 1)
+    _, burst, _, src = measured_peaks()  # each GEMM timed alone: the burst peak
+    r["roofline"] = {"bound": "tensor", "peak": burst, "unit": "TFLOP/s", "peak_kind": f"{src} burst bf16",
+                     "qkv_frac": round(r["qkv_TFLOP_per_s"] / burst, 4),
+                     "out_frac": round(r["out_TFLOP_per_s"] / burst, 4),
+                     "note": "producer includes the 1/rms pass; consumer the residual read/write"}
     r["speedup"] = round((r["producer_cublas_chain_ms"] + r["consumer_cublas_chain_ms"]) /
                          (r["producer_fused_ms"] + r["consumer_fused_ms"]), 3)
     del x, xn, qkv, cat
