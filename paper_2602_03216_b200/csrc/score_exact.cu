@@ -40,6 +40,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "chain_sum.cuh"
 #include "expf_glibc.cuh"
 #include "sm100.cuh"
 
@@ -307,6 +308,10 @@ constexpr int XB_XST = 8;                         // X tiles in flight (HBM late
 constexpr int XB_HELP = 16;                       // helper warps: thread = (key, half of the rows)
 constexpr int XB_THREADS = 32 * (XB_HELP + 1);    // + the summing warp
 constexpr int XB_EP = XB_MAXR + 1;                // e tile row pitch (conflict-free transpose)
+// Rows per row-sum CTA at or below which the chains run apart (row_chain_sum):
+// A/B, 4 heads of one KV group at 128K 0.740 -> 0.675 ms; at 4 rows per CTA
+// the split is slower (0.955 -> 1.115 ms).
+constexpr int kSplitRowsPerCta = 2;
 
 struct __align__(128) XbSmem {
     float x[XB_XST][XB_MAXR * XB_KEYS];           // X tile (TMA), rows x keys
@@ -317,6 +322,10 @@ struct __align__(128) XbSmem {
     uint64_t x_full[XB_XST], x_empty[XB_XST], e_full[XB_STAGES], e_empty[XB_STAGES];
 };
 
+// kChain = false: the exponentials only (e written over X); the row sums then
+// come from row_chain_sum below (few rows: each CTA's L-long chain would be the
+// whole kernel's floor).
+template <bool kChain>
 __global__ void __launch_bounds__(XB_THREADS, 1)
 score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__ X, int L, int Lp,
                    int lq, int n_rows, int rows_per_cta, const int* __restrict__ rowmax,
@@ -371,7 +380,7 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
             if (tid == 0 && t + XB_XST - 1 < n_tiles) issue(t + XB_XST - 1);
             const int xt = t % XB_XST, st = t % XB_STAGES;
             mbar_wait(&sm.x_full[xt], (t / XB_XST) & 1);
-            if (t >= XB_STAGES) mbar_wait(&sm.e_empty[st], ((t / XB_STAGES) - 1) & 1);
+            if (kChain && t >= XB_STAGES) mbar_wait(&sm.e_empty[st], ((t / XB_STAGES) - 1) & 1);
             const float* xs = sm.x[xt] + rbase * XB_KEYS + j;
             float* es = sm.e[st] + j * XB_EP + rbase;
             const int key = t * XB_KEYS + j;
@@ -386,15 +395,15 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
                 // masked entries add +0 to the chain: exactly the reference's skip
                 const float e = expf_glibc(__fsub_rn(xv[i], mrow[i]), sm.tab);
                 const bool ok = key < arow[i];
-                es[i] = ok ? e : 0.0f;
+                if (kChain) es[i] = ok ? e : 0.0f;
                 if (ok) __stcs(xg + (size_t)i * Lp, e);
             }
             // every helper thread publishes its own e writes (release) to the chain warp
-            mbar_arrive(&sm.e_full[st]);
+            if (kChain) mbar_arrive(&sm.e_full[st]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.x_empty[xt]);
         }
-    } else {
+    } else if (kChain) {
         // the sequential f32 row sums, lane = row (tensor_ops.cpp:59-65)
         const int row = lane & (XB_MAXR - 1);
         float s = 0.0f;
@@ -422,6 +431,18 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
         }
         if (lane < R && row0 + lane < n_rows) rowsum[row0 + lane] = s;
     }
+}
+
+// The row sums of few rows: one CTA per row, the exact sequential f32 sum of
+// its e values (the first L - lq + r + 1 keys; the masked tail adds nothing)
+// without the L-long chain (chain_sum.cuh).
+constexpr int XR_THREADS = 512;
+__global__ void __launch_bounds__(XR_THREADS) row_chain_sum(const float* __restrict__ X, int L, int Lp,
+                                                            int lq, float* __restrict__ rowsum) {
+    const int row = blockIdx.x;
+    const int n = min(L, L - lq + row % lq + 1);
+    const float s = exact_chain_sum<XR_THREADS>(X + (size_t)row * Lp, n);
+    if (threadIdx.x == 0) rowsum[row] = s;
 }
 
 __global__ void fill_int(int* __restrict__ p, int v, int n) {
@@ -576,11 +597,19 @@ int launch_score_exact(const tsa_desc& d, const void* q, const void* k, const Ou
         TSA_LAUNCH_CHECK("score_exact_logits");
     }
     {
+        // few rows (a head shard of a multi-GPU layer): exponentials, then the
+        // chain-free row sums; otherwise the chains overlap the exponentials
+        const bool split = rpc <= kSplitRowsPerCta;
         const int smem = (int)sizeof(XbSmem) + 128;
-        if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(score_exact_rowsum), smem))) return rc;
-        score_exact_rowsum<<<(n_rows + rpc - 1) / rpc, XB_THREADS, smem, st>>>(
-            mx, X, L, Lp, lq, n_rows, rpc, rowmax, rowsum);
+        auto kern = split ? score_exact_rowsum<false> : score_exact_rowsum<true>;
+        if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem))) return rc;
+        kern<<<(n_rows + rpc - 1) / rpc, XB_THREADS, smem, st>>>(mx, X, L, Lp, lq, n_rows, rpc,
+                                                                rowmax, rowsum);
         TSA_LAUNCH_CHECK("score_exact_rowsum");
+        if (split) {
+            row_chain_sum<<<n_rows, XR_THREADS, 0, st>>>(X, L, Lp, lq, rowsum);
+            TSA_LAUNCH_CHECK("row_chain_sum");
+        }
     }
     {
         CUtensorMap mxc;
