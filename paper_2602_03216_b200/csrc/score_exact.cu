@@ -308,10 +308,9 @@ constexpr int XB_XST = 8;                         // X tiles in flight (HBM late
 constexpr int XB_HELP = 16;                       // helper warps: thread = (key, half of the rows)
 constexpr int XB_THREADS = 32 * (XB_HELP + 1);    // + the summing warp
 constexpr int XB_EP = XB_MAXR + 1;                // e tile row pitch (conflict-free transpose)
-// Rows per row-sum CTA at or below which the chains run apart (row_chain_sum):
-// A/B, 4 heads of one KV group at 128K 0.740 -> 0.675 ms; at 4 rows per CTA
-// the split is slower (0.955 -> 1.115 ms).
-constexpr int kSplitRowsPerCta = 2;
+// Rows per row-sum CTA (chain mode) at or below which the chains run apart
+// (row_chain_sum) and the exponentials split over key ranges.
+constexpr int kSplitRowsPerCta = 4;
 
 struct __align__(128) XbSmem {
     float x[XB_XST][XB_MAXR * XB_KEYS];           // X tile (TMA), rows x keys
@@ -328,8 +327,8 @@ struct __align__(128) XbSmem {
 template <bool kChain>
 __global__ void __launch_bounds__(XB_THREADS, 1)
 score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__ X, int L, int Lp,
-                   int lq, int n_rows, int rows_per_cta, const int* __restrict__ rowmax,
-                   float* __restrict__ rowsum) {
+                   int lq, int n_rows, int rows_per_cta, int tiles_per_split,
+                   const int* __restrict__ rowmax, float* __restrict__ rowsum) {
     extern __shared__ uint8_t smem_raw[];
     XbSmem& sm = smem_view<XbSmem, 128>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -354,12 +353,15 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
         fence_barrier_init();
     }
     __syncthreads();
-    const int n_tiles = (L + XB_KEYS - 1) / XB_KEYS;
-    auto issue = [&](int t) {
+    // this CTA's key tiles: all of them with the chain; a range of them (blockIdx.y)
+    // for the exponentials alone
+    const int tb = blockIdx.y * tiles_per_split;
+    const int n_tiles = min((L + XB_KEYS - 1) / XB_KEYS - tb, tiles_per_split);
+    auto issue = [&](int t) {  // t: local tile index
         const int st = t % XB_XST;
         if (t >= XB_XST) mbar_wait(&sm.x_empty[st], ((t / XB_XST) - 1) & 1);
         mbar_arrive_expect_tx(&sm.x_full[st], R * XB_KEYS * 4);
-        tma_load_2d(sm.x[st], &tm_x, &sm.x_full[st], t * XB_KEYS, row0);
+        tma_load_2d(sm.x[st], &tm_x, &sm.x_full[st], (tb + t) * XB_KEYS, row0);
     };
     if (warp < XB_HELP) {
         if (tid == 0)
@@ -383,7 +385,7 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
             if (kChain && t >= XB_STAGES) mbar_wait(&sm.e_empty[st], ((t / XB_STAGES) - 1) & 1);
             const float* xs = sm.x[xt] + rbase * XB_KEYS + j;
             float* es = sm.e[st] + j * XB_EP + rbase;
-            const int key = t * XB_KEYS + j;
+            const int key = (tb + t) * XB_KEYS + j;
             float xv[RH];
 #pragma unroll
             for (int i = 0; i < RH; ++i) xv[i] = xs[i * XB_KEYS];
@@ -597,14 +599,23 @@ int launch_score_exact(const tsa_desc& d, const void* q, const void* k, const Ou
         TSA_LAUNCH_CHECK("score_exact_logits");
     }
     {
-        // few rows (a head shard of a multi-GPU layer): exponentials, then the
-        // chain-free row sums; otherwise the chains overlap the exponentials
+        // few rows (a head shard of a multi-GPU layer): the exponentials of full
+        // 16-row CTAs split over key ranges, then the chain-free row sums;
+        // otherwise each CTA's chains overlap its exponentials
         const bool split = rpc <= kSplitRowsPerCta;
         const int smem = (int)sizeof(XbSmem) + 128;
+        const int n_tiles = (L + XB_KEYS - 1) / XB_KEYS;
+        const int rows = split ? std::min(XB_MAXR, n_rows) : rpc;
+        const int row_ctas = (n_rows + rows - 1) / rows;
+        const int splits = split ? std::max(1, std::min(n_tiles, nsm / row_ctas)) : 1;  // one wave
+        const int tps = (n_tiles + splits - 1) / splits;
+        if (split && (rc = make_f32_map_2d(&mx, X, (uint64_t)Lp, (uint64_t)n_rows, (uint64_t)Lp * 4,
+                                           XB_KEYS, (uint32_t)rows)))
+            return rc;
         auto kern = split ? score_exact_rowsum<false> : score_exact_rowsum<true>;
         if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem))) return rc;
-        kern<<<(n_rows + rpc - 1) / rpc, XB_THREADS, smem, st>>>(mx, X, L, Lp, lq, n_rows, rpc,
-                                                                rowmax, rowsum);
+        kern<<<dim3(row_ctas, (n_tiles + tps - 1) / tps), XB_THREADS, smem, st>>>(
+            mx, X, L, Lp, lq, n_rows, rows, tps, rowmax, rowsum);
         TSA_LAUNCH_CHECK("score_exact_rowsum");
         if (split) {
             row_chain_sum<<<n_rows, XR_THREADS, 0, st>>>(X, L, Lp, lq, rowsum);
