@@ -4,6 +4,8 @@
 // rows are too few to hide their L-long chains).  See exact_chain_sum below.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include <cstdint>
 
 namespace tsa_dev {
@@ -260,6 +262,146 @@ __device__ float exact_chain_sum(const float* __restrict__ x, int n) {
             if (lead < 32 && pos < nch) add_chunk(pos++);
         }
         if (lane == 0) s_res = S;
+    }
+    __syncthreads();
+    return s_res;
+}
+
+
+// The same sum over a thread-block cluster of CLN CTAs whose slices of x
+// ([r S, (r+1) S), S = ceil(n / CLN), in rank order) are staged in each CTA's
+// shared memory (xs = this CTA's slice, ns its length, at most 64 chunks of
+// 256): every CTA folds its own chunks, the chunk sums, their prefix and the
+// folds meet in rank 0's shared memory through DSMEM, and rank 0's warp 0 walks
+// them.  The result is returned in rank 0 (other ranks: undefined).
+template <int NT, int CLN>
+__device__ float cluster_exact_chain_sum(const float* xs, int ns, const float* __restrict__ x,
+                                         int n) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    static_assert(NT % 32 == 0, "whole warps");
+    constexpr int NW = NT / 32, CH = 256, PER = CH / 32;
+    constexpr int kMaxChunks = kChainChunks;
+    __shared__ uint4 cm[kMaxChunks];
+    __shared__ double csum[kMaxChunks];
+    __shared__ float stage[CH];
+    __shared__ float s_res;
+    const int rank = (int)cluster.block_rank();
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int S = (n + CLN - 1) / CLN;
+    const int cpr = (S + CH - 1) / CH;  // chunks per rank (the last rank may have fewer)
+    const int base = rank * cpr, nloc = (ns + CH - 1) / CH;
+    const int last_len = n - (CLN - 1) * S;
+    const int nch = (CLN - 1) * cpr + (last_len > 0 ? (last_len + CH - 1) / CH : 0);
+    uint4* cm0 = cluster.map_shared_rank(cm, 0);
+    double* csum0 = cluster.map_shared_rank(csum, 0);
+    auto load8 = [&](int lc, float (&v)[PER]) {  // this lane's 8 elements of local chunk lc
+        const int i0 = lc * CH + lane * PER;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) v[j] = i0 + j < ns ? xs[i0 + j] : 0.0f;
+    };
+    cluster.sync();  // every CTA runs before any remote write
+    // phase 1: chunk sums (double) into rank 0
+    for (int lc = warp; lc < nloc; lc += NW) {
+        float v[PER];
+        load8(lc, v);
+        double ds = 0.0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) ds += (double)v[j];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ds += __shfl_xor_sync(0xffffffffu, ds, o);
+        if (lane == 0) csum0[base + lc] = ds;
+    }
+    cluster.sync();
+    if (rank == 0) {  // exclusive prefix over the chunks, two per thread (nch <= 2 NT)
+        const int c0 = 2 * t;
+        const double a0 = c0 < nch ? csum[c0] : 0.0, a1 = c0 + 1 < nch ? csum[c0 + 1] : 0.0;
+        double tot;
+        const double ex = chain_block_excl_scan<NT>(a0 + a1, &tot);
+        __syncthreads();
+        if (c0 < nch) csum[c0] = ex;
+        if (c0 + 1 < nch) csum[c0 + 1] = ex + a0;
+    }
+    cluster.sync();
+    // phase 2: each chunk folded under the binade its start probably has
+    for (int lc = warp; lc < nloc; lc += NW) {
+        const float pf = (float)csum0[base + lc];
+        const int E = pf > 0.0f ? (int)((__float_as_uint(pf) >> 23) & 0xFF) - 127 : -1000;
+        bool valid = E >= -100 && E <= 100;
+        ChainFold f{0u, 0u, 0u, 1u};
+        if (valid) {
+            const float scale = __uint_as_float((uint32_t)(127 + 23 - E) << 23);  // 2^(23 - E)
+            float v[PER];
+            load8(lc, v);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const float y = __fmul_rn(v[j], scale);  // exact: power-of-two scaling
+                if (!(y < 16777216.0f)) valid = false;   // >= 2^24 u: crosses a binade
+                else chain_fold_elem(f, y);
+            }
+            if (f.inc0 > (1u << 25) || f.inc1 > (1u << 25)) valid = false;
+        }
+        valid = __all_sync(0xffffffffu, valid);
+        f = chain_warp_compose(f, lane);
+        if (lane == 31)
+            cm0[base + lc] = make_uint4(f.inc0, f.inc1, (uint32_t)(E + 128) | (f.q0 << 16) | (f.q1 << 17),
+                                        (valid && f.inc0 <= (1u << 25) && f.inc1 <= (1u << 25)) ? 1u : 0u);
+    }
+    cluster.sync();
+    // phase 3: rank 0's warp 0 walks the chunks with the exact running sum
+    if (rank == 0 && warp == 0) {
+        float S_ = 0.0f;
+        auto range = [&](int c, int& cb, int& ce) {
+            const int r = c / cpr, lc = c % cpr;
+            cb = r * S + lc * CH;
+            ce = min(min(n, (r + 1) * S), cb + CH);
+        };
+        auto add_chunk = [&](int c) {  // one chunk, lane-uniform
+            int cb, ce;
+            range(c, cb, ce);
+            const uint4 w = cm[c];
+            const uint32_t bits = __float_as_uint(S_);
+            const int Es = (int)((bits >> 23) & 0xFF) - 127;
+            if (w.w && (bits >> 23) != 0 && Es == (int)(w.z & 0xFFFFu) - 128) {
+                const uint32_t a = (bits & 0x7FFFFFu) | 0x800000u;
+                const uint32_t inc = (a & 1u) ? w.y : w.x;
+                if (a + inc <= (1u << 24)) {
+                    S_ = __fmul_rn((float)(a + inc), __uint_as_float((uint32_t)(127 + Es - 23) << 23));
+                    return;
+                }
+            }
+            const int m = ce - cb;  // element by element, staged (coalesced)
+            for (int i = lane; i < m; i += 32) stage[i] = __ldg(x + cb + i);
+            __syncwarp();
+#pragma unroll 8
+            for (int i = 0; i < m; ++i) S_ = __fadd_rn(S_, stage[i]);
+            __syncwarp();
+        };
+        int pos = 0;
+        while (pos < nch) {
+            const int c = pos + lane;
+            const bool live = c < nch;
+            const uint4 w = live ? cm[c] : make_uint4(0u, 0u, 0u, 0u);
+            const uint32_t bits = __float_as_uint(S_);
+            const int Es = (int)((bits >> 23) & 0xFF) - 127;
+            const bool normal = (bits >> 23) != 0;
+            const bool folded = live && w.w && normal && Es == (int)(w.z & 0xFFFFu) - 128;
+            ChainFold f = live ? ChainFold{w.x, w.y, (w.z >> 16) & 1u, (w.z >> 17) & 1u}
+                               : ChainFold{0u, 0u, 0u, 1u};
+            f = chain_warp_compose(f, lane);
+            const uint32_t a = (bits & 0x7FFFFFu) | 0x800000u;
+            const uint32_t inc = (a & 1u) ? f.inc1 : f.inc0;
+            const bool good = folded && a + inc <= (1u << 24);
+            const uint32_t ball = __ballot_sync(0xffffffffu, good);
+            const int lead = ball == 0xffffffffu ? 32 : __ffs(~ball) - 1;
+            if (lead > 0) {
+                const uint32_t tot = __shfl_sync(0xffffffffu, inc, lead - 1);
+                S_ = __fmul_rn((float)(a + tot), __uint_as_float((uint32_t)(127 + Es - 23) << 23));
+            }
+            pos += lead;
+            if (lead < 32 && pos < nch) add_chunk(pos++);
+        }
+        if (lane == 0) s_res = S_;
     }
     __syncthreads();
     return s_res;

@@ -144,13 +144,18 @@ budget_kernel(const float* __restrict__ headsum, int L, double tau, int min_keep
     float total = 1.0f;
     if (mode != BUDGET_FROM_SL) {
         if (exact_total) {
-            // the sequential f32 chain (token_coverage.cpp:58-61), bit for bit, in rank 0
-            if (rank == 0) {
+            // the sequential f32 chain (token_coverage.cpp:58-61), bit for bit:
+            // staged slices -> the chunk folds spread over the cluster, walked in rank 0
+            if (kStaged) {
+                for (int t = t_begin + tid; t < t_end; t += BB) staged[t - t_begin] = headsum[t];
+                __syncthreads();
+                const float acc = tsa_dev::cluster_exact_chain_sum<BB, CL>(staged, t_end - t_begin,
+                                                                          headsum, L);
+                if (rank == 0 && tid == 0) s_total = acc;
+            } else if (rank == 0) {
                 const float acc = tsa_dev::exact_chain_sum<BB>(headsum, L);
                 if (tid == 0) s_total = acc;
             }
-            if (kStaged)
-                for (int t = t_begin + tid; t < t_end; t += BB) staged[t - t_begin] = headsum[t];
             // (rank 0 publishes locally; the others read it through DSMEM after the
             // barrier -- no remote write may precede the first cluster barrier,
             // when a peer CTA may not have started yet)
