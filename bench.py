@@ -1041,7 +1041,11 @@ def run_reference(args):
                        "seq_len": L, "tau": args.tau, "sigma": sigma, "k_keep": k_keep},
             "cpu_baseline": res, "cpu_baseline_single_thread": single,
             "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            # the full 128K layer takes hours on the host: each step times a bounded
+            # sample of it and `value` is the extrapolation (cpu_baseline.sample)
+            "extrapolated": True,
+            "measured_wall_s_per_step": round(sum(res.get("sample_s", {}).values()), 2)}
     print(json.dumps(line), flush=True)
 
 
