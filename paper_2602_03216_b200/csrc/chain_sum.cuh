@@ -407,4 +407,82 @@ __device__ float cluster_exact_chain_sum(const float* xs, int ns, const float* _
     return s_res;
 }
 
+
+// One warp's exact sequential f32 sum of x[0..n) (all lanes get it), streaming:
+// per round each lane takes a chunk of 32 consecutive elements, a warp scan of
+// the chunk sums (double) predicts each chunk's binade, each lane folds its
+// chunk, and the exact running sum walks the round's chunks (leading run at
+// once; the chunk after it element by element).  For rows of a few thousand
+// elements (the REFERENCE-order softmax, tensor_ops.cpp:59-65).
+__device__ __forceinline__ float warp_exact_chain_sum(const float* __restrict__ x, int n) {
+    const int lane = threadIdx.x & 31;
+    float S = 0.0f;
+    double approx = 0.0;
+    for (int base = 0; base < n; base += 32 * 32) {
+        const int c0 = base + lane * 32;
+        const int cnt = max(0, min(32, n - c0));
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = i < cnt ? x[c0 + i] : 0.0f;
+        double ds = 0.0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) ds += (double)v[i];
+        double incl = ds;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const float pf = (float)(approx + incl - ds);
+        approx += __shfl_sync(0xffffffffu, incl, 31);
+        const int E = pf > 0.0f ? (int)((__float_as_uint(pf) >> 23) & 0xFF) - 127 : -1000;
+        bool valid = cnt > 0 && E >= -100 && E <= 100;
+        ChainFold f{0u, 0u, 0u, 1u};
+        if (valid) {
+            const float scale = __uint_as_float((uint32_t)(127 + 23 - E) << 23);  // 2^(23 - E)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (i < cnt) {
+                    const float y = __fmul_rn(v[i], scale);
+                    if (!(y < 16777216.0f)) valid = false;
+                    else chain_fold_elem(f, y);
+                }
+            }
+            if (f.inc0 > (1u << 25) || f.inc1 > (1u << 25)) valid = false;
+        }
+        int pos = 0;
+        while (pos < 32) {
+            const int cnt_pos = __shfl_sync(0xffffffffu, cnt, pos);
+            if (cnt_pos == 0) break;  // past n
+            const uint32_t bits = __float_as_uint(S);
+            const int Es = (int)((bits >> 23) & 0xFF) - 127;
+            const bool live = lane >= pos && cnt > 0;
+            const bool folded = live && valid && (bits >> 23) != 0 && Es == E;
+            ChainFold g = (lane >= pos) ? f : ChainFold{0u, 0u, 0u, 1u};
+            g = chain_warp_compose(g, lane);
+            const uint32_t a = (bits & 0x7FFFFFu) | 0x800000u;
+            const uint32_t inc = (a & 1u) ? g.inc1 : g.inc0;
+            const bool good = lane < pos || (folded && a + inc <= (1u << 24));
+            const uint32_t ball = __ballot_sync(0xffffffffu, good);
+            const int lead = ball == 0xffffffffu ? 32 : __ffs(~ball) - 1;
+            if (lead > pos) {
+                const uint32_t tot = __shfl_sync(0xffffffffu, inc, lead - 1);
+                S = __fmul_rn((float)(a + tot), __uint_as_float((uint32_t)(127 + Es - 23) << 23));
+            }
+            pos = lead;
+            if (pos < 32) {  // this chunk element by element (its values from lane pos)
+                const int m = __shfl_sync(0xffffffffu, cnt, pos);
+                float w[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) w[i] = __shfl_sync(0xffffffffu, v[i], pos);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i < m) S = __fadd_rn(S, w[i]);
+                ++pos;
+            }
+        }
+    }
+    return S;
+}
+
 }  // namespace tsa_dev

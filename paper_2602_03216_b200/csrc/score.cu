@@ -14,6 +14,7 @@
 //   score_softmax_ref -> in place: P[h, r, j]
 //   score_colsum_ref  -> s[h, t] (column sums + pooling, halo of kernel/2)
 #include "common.cuh"
+#include "chain_sum.cuh"
 #include "expf_glibc.cuh"
 
 namespace tsa {
@@ -86,8 +87,9 @@ __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q,
     }
 }
 
-// One warp per (head, row): max, e = expf(x - max) (glibc's), sequential
-// f32 sum in j order, then divide.  Masked entries (j >= allowed) untouched.
+// One warp per (head, row): max, e = expf(x - max) (glibc's), the sequential
+// f32 sum in j order (chain_sum.cuh: exact, without the L-long chain), then
+// divide.  Masked entries (j >= allowed) untouched.
 __global__ void __launch_bounds__(256) score_softmax_ref(float* __restrict__ logits, int L, int lq,
                                                          int head_begin, int n_rows) {
     __shared__ uint64_t tab[32];
@@ -104,21 +106,10 @@ __global__ void __launch_bounds__(256) score_softmax_ref(float* __restrict__ log
     for (int j = lane; j < allowed; j += 32) mx = fmaxf(mx, row[j]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float sum = 0.0f;  // meaningful in lane 0 only
-    for (int j0 = 0; j0 < allowed; j0 += 32) {
-        const int j = j0 + lane;
-        float e = 0.0f;
-        if (j < allowed) {
-            e = tsa_dev::expf_glibc(__fsub_rn(row[j], mx), tab);
-            row[j] = e;
-        }
-        const int cnt = min(32, allowed - j0);
-        for (int i = 0; i < cnt; ++i) {
-            const float ei = __shfl_sync(0xffffffffu, e, i);
-            sum = __fadd_rn(sum, ei);
-        }
-    }
-    sum = __shfl_sync(0xffffffffu, sum, 0);
+    for (int j = lane; j < allowed; j += 32) row[j] = tsa_dev::expf_glibc(__fsub_rn(row[j], mx), tab);
+    __syncwarp();
+    // the sequential f32 sum in j order, bit for bit, without the L-long chain
+    const float sum = tsa_dev::warp_exact_chain_sum(row, allowed);
     for (int j = lane; j < allowed; j += 32) row[j] = __fdiv_rn(row[j], sum);
 }
 
