@@ -95,19 +95,6 @@ __device__ __forceinline__ void issue_pv_quarter(uint32_t t_o, uint32_t t_p, uin
     }
 }
 
-// O += P[:, 64h .. 64h+63] V[64h .. 64h+63, :] (half h of the 128-key tile).
-__device__ __forceinline__ void issue_pv_half(uint32_t t_o, uint32_t t_p, uint32_t v_base,
-                                              uint32_t idesc, bool accumulate, int half,
-                                              uint32_t leader) {
-    const uint32_t vlo = sdesc_lo(v_base, HALF_BYTES);
-#pragma unroll
-    for (int k2 = 0; k2 < BN / 32; ++k2) {
-        const int kk = half * (BN / 32) + k2;
-        mma_bf16_ts_p(t_o, t_p + kk * 8, sdesc_from_lo(vlo + ((kk * 2048) >> 4)), idesc,
-                      (accumulate || kk > 0) ? 1u : 0u, leader);
-    }
-}
-
 // P = 2^(x*scale - m) for one 128-key S row held in registers: packed f32x2
 // scale (FFMA2), the exponential split between MUFU.EX2 and a polynomial on
 // the FMA pipe (pairs set in kPolyMask, per 32-key chunk; the diagonal tile,

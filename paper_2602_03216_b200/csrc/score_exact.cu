@@ -91,10 +91,6 @@ __device__ __forceinline__ T& smem_view(uint8_t* raw) {
 __device__ __forceinline__ uint32_t word(const uint4& v, int i) {
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
-__device__ __forceinline__ float comp(const float4& v, int i) {
-    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-}
-
 struct RowGeom {
     int hl;  // head relative to the shard's first head
     int r;   // tail row
