@@ -30,8 +30,10 @@ __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q,
                                                         float* __restrict__ logits, int H, int group,
                                                         int L, int d, int lq, int head_begin,
                                                         float inv_sqrt_d) {
-    __shared__ float qs[LG_PCH][LG_ROWS];
-    __shared__ float ks[LG_PCH][LG_KEYS];
+    // +1 pitch: the staging stores walk p fastest (coalesced global reads), which
+    // without it would hit one bank 32 times per warp
+    __shared__ float qs[LG_PCH][LG_ROWS + 1];
+    __shared__ float ks[LG_PCH][LG_KEYS + 1];
     const int h = head_begin + blockIdx.y;
     const int r_base = blockIdx.z * LG_ROWS;
     const int j0 = blockIdx.x * LG_KEYS;
