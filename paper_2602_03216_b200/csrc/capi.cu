@@ -194,7 +194,8 @@ int score_stage(const tsa_desc& d, const void* q, const void* k, const OutReplic
     if (score_exact_supported(d) && lq_of(d) <= 2048)
         return launch_score_exact(d, q, k, s, at<float>(ws, w.logits), at<int>(ws, w.rowmax),
                                   at<float>(ws, w.rowsum), at<float>(ws, w.colraw), st);
-    return launch_score_reference(d, q, k, s, at<float>(ws, w.logits), st);
+    return launch_score_reference(d, q, k, s, at<float>(ws, w.logits), at<int>(ws, w.rowmax),
+                                  at<float>(ws, w.rowsum), at<float>(ws, w.colraw), st);
 }
 
 }  // namespace tsa

@@ -120,7 +120,21 @@ inline int scoring_mode(const tsa_desc& d) {
 // s: the [H x L] score rows, or several replicas of them (multi-GPU, each
 // rank's buffer); rows of the descriptor's heads are written to every one.
 int launch_score_reference(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s,
-                           float* logits, cudaStream_t st);
+                           float* logits, int* rowmax, float* rowsum, float* colraw,
+                           cudaStream_t st);
+// score_exact.cu: the exact row sums, column sums and pool over logits X
+// [local head x lq rows, row stride exact_logits_stride(L)] with their
+// encoded row maxima (the second half of the exact scorer; REFERENCE-order
+// logits of other shapes feed it too)
+int launch_score_exact_rows(const tsa_desc& d, float* X, int* rowmax, float* rowsum, float* colraw,
+                            const OutReplicas& s, cudaStream_t st);
+int launch_fill_int(int* p, int v, int n, cudaStream_t st);
+// ordered int encoding of a float (atomicMax of floats as ints)
+__device__ __forceinline__ int enc_max(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float dec_max(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
 int launch_score_fast(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s,
                       float* logits, float* rowstat, cudaStream_t st);
 int launch_expf(const float* x, float* y, int64_t n, cudaStream_t st);

@@ -13,6 +13,8 @@
 //   score_logits_ref  -> logits[h, r, j] (only the causally allowed prefix)
 //   score_softmax_ref -> in place: P[h, r, j]
 //   score_colsum_ref  -> s[h, t] (column sums + pooling, halo of kernel/2)
+#include <climits>
+
 #include "common.cuh"
 #include "chain_sum.cuh"
 #include "expf_glibc.cuh"
@@ -26,10 +28,14 @@ constexpr int LG_PCH = 32;    // d-chunk staged in smem
 
 // Block: 256 threads = 16 row-groups (4 rows) x 16 key-groups (8 keys).
 template <typename T>
+// Lp > 0: the exact scorer's layout -- rows (local head, r) at stride Lp, and
+// each row's maximum (atomicMax of the ordered encoding into rowmax) for the
+// exact row / column passes; Lp == 0: rows (head, r) at stride L.
 __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q, const T* __restrict__ k,
                                                         float* __restrict__ logits, int H, int group,
                                                         int L, int d, int lq, int head_begin,
-                                                        float inv_sqrt_d) {
+                                                        float inv_sqrt_d, int Lp,
+                                                        int* __restrict__ rowmax) {
     // +1 pitch: the staging stores walk p fastest (coalesced global reads), which
     // without it would hit one bank 32 times per warp
     __shared__ float qs[LG_PCH][LG_ROWS + 1];
@@ -78,13 +84,23 @@ __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q,
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int r = r_base + tr * 4 + a;
-        if (r >= lq) continue;
         const int allowed = L - lq + r + 1;
-        float* out = logits + ((size_t)h * lq + r) * L;
+        const size_t lrow = (size_t)(h - head_begin) * lq + r;
+        float* out = Lp ? logits + lrow * Lp : logits + ((size_t)h * lq + r) * L;
+        float m = -INFINITY;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
             const int j = j0 + tk * 8 + b;
-            if (j < allowed) out[j] = __fmul_rn(acc[a][b], inv_sqrt_d);
+            const float x = __fmul_rn(acc[a][b], inv_sqrt_d);
+            if (r < lq && j < allowed) {
+                out[j] = x;
+                m = fmaxf(m, x);
+            }
+        }
+        if (rowmax) {  // the 16 key groups of this row sit in one half-warp
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (tk == 0 && r < lq && m != -INFINITY) atomicMax(rowmax + lrow, enc_max(m));
         }
     }
 }
@@ -204,22 +220,31 @@ int launch_colsum_pool(const tsa_desc& d, const float* probs, const OutReplicas&
 }
 
 int launch_score_reference(const tsa_desc& d, const void* q, const void* k, const OutReplicas& s,
-                           float* logits, cudaStream_t st) {
+                           float* logits, int* rowmax, float* rowsum, float* colraw,
+                           cudaStream_t st) {
     const int L = d.seq_len, lq = lq_of(d), D = d.d_head;
     const int nh = d.head_end - d.head_begin;
     const int group = d.n_heads / d.n_kv_heads;
     const float inv_sqrt_d = 1.0f / sqrtf((float)D);
+    // the exact scorer's row / column passes take these logits too (its layout
+    // and row maxima); lq > 2048 keeps the per-row warp softmax
+    const bool exact_rows = lq <= 2048;
+    const int Lp = exact_rows ? (int)exact_logits_stride(L) : 0;
+    int* rm = exact_rows ? rowmax : nullptr;
+    const int n_rows = nh * lq;
+    if (rm)
+        if (int rc = launch_fill_int(rm, INT_MIN, n_rows, st)) return rc;
     dim3 grid((L + LG_KEYS - 1) / LG_KEYS, nh, (lq + LG_ROWS - 1) / LG_ROWS);
     if (d.dtype == TSA_BF16)
         score_logits_ref<__nv_bfloat16><<<grid, 256, 0, st>>>(
             (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, logits, d.n_heads, group, L, D, lq,
-            d.head_begin, inv_sqrt_d);
+            d.head_begin, inv_sqrt_d, Lp, rm);
     else
         score_logits_ref<float><<<grid, 256, 0, st>>>((const float*)q, (const float*)k, logits,
                                                       d.n_heads, group, L, D, lq, d.head_begin,
-                                                      inv_sqrt_d);
+                                                      inv_sqrt_d, Lp, rm);
     TSA_LAUNCH_CHECK("score_logits_ref");
-    const int n_rows = nh * lq;
+    if (exact_rows) return launch_score_exact_rows(d, logits, rm, rowsum, colraw, s, st);
     score_softmax_ref<<<(n_rows + 7) / 8, 256, 0, st>>>(logits, L, lq, d.head_begin, n_rows);
     TSA_LAUNCH_CHECK("score_softmax_ref");
     return launch_colsum_pool(d, logits, s, st);

@@ -70,11 +70,6 @@ struct __align__(1024) XaSmem {
     uint64_t empty[XA_STAGES];
 };
 
-__device__ __forceinline__ int enc_max(float f) {
-    const int i = __float_as_int(f);
-    return i >= 0 ? i : i ^ 0x7fffffff;
-}
-__device__ __forceinline__ float dec_max(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
 
 // bf16 halves of a word as f32, by byte permutes (ALU pipe: a shift or mask
 // may be emitted as IMAD, which would take FMA-pipe slots from the FFMA2s)
@@ -572,16 +567,11 @@ int launch_score_exact(const tsa_desc& d, const void* q, const void* k, const Ou
     const size_t eb = 2;
     const uint8_t* qb = static_cast<const uint8_t*>(q) + (size_t)kv_begin * g * L * 128 * eb;
     const uint8_t* kb = static_cast<const uint8_t*>(k) + (size_t)kv_begin * L * 128 * eb;
-    CUtensorMap mk, mx;
+    CUtensorMap mk;
     int rc;
     if ((rc = make_bf16_map_2d(&mk, kb, (uint64_t)n_kv * L, XA_KEYS))) return rc;
     const int n_rows = nh * lq;
     const int nsm = num_sms();
-    // rows per row-sum CTA: spread the rows over every SM (<= 16: one chain lane each)
-    const int rpc = std::min(XB_MAXR, std::max(1, (n_rows + nsm - 1) / nsm));
-    if ((rc = make_f32_map_2d(&mx, X, (uint64_t)Lp, (uint64_t)n_rows, (uint64_t)Lp * 4, XB_KEYS,
-                              (uint32_t)rpc)))
-        return rc;
     fill_int<<<(n_rows + 255) / 256, 256, 0, st>>>(rowmax, INT_MIN, n_rows);  // below every encoding
     TSA_LAUNCH_CHECK("score_exact_fill");
     {
@@ -594,6 +584,29 @@ int launch_score_exact(const tsa_desc& d, const void* q, const void* k, const Ou
             n_ktiles, n_units, inv_sqrt_d, X, rowmax);
         TSA_LAUNCH_CHECK("score_exact_logits");
     }
+    return launch_score_exact_rows(d, X, rowmax, rowsum, colraw, s, st);
+}
+
+int launch_fill_int(int* p, int v, int n, cudaStream_t st) {
+    fill_int<<<(n + 255) / 256, 256, 0, st>>>(p, v, n);
+    TSA_LAUNCH_CHECK("fill_int");
+    return 0;
+}
+
+int launch_score_exact_rows(const tsa_desc& d, float* X, int* rowmax, float* rowsum, float* colraw,
+                            const OutReplicas& s, cudaStream_t st) {
+    const int L = d.seq_len, lq = lq_of(d);
+    const int Lp = (int)exact_logits_stride(L);
+    const int nh = d.head_end - d.head_begin;
+    const int n_rows = nh * lq;
+    const int nsm = num_sms();
+    // rows per row-sum CTA: spread the rows over every SM (<= 16: one chain lane each)
+    const int rpc = std::min(XB_MAXR, std::max(1, (n_rows + nsm - 1) / nsm));
+    CUtensorMap mx;
+    int rc;
+    if ((rc = make_f32_map_2d(&mx, X, (uint64_t)Lp, (uint64_t)n_rows, (uint64_t)Lp * 4, XB_KEYS,
+                              (uint32_t)rpc)))
+        return rc;
     {
         // few rows (a head shard of a multi-GPU layer): the exponentials of full
         // 16-row CTAs split over key ranges, then the chain-free row sums;
