@@ -110,16 +110,26 @@ __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// 16 KiB raw chunk -> hi in place, lo into `lo`; 128 threads, 8 x 16 B each.
+// 16 KiB raw chunk -> hi in place, lo into `lo`; 128 threads, 8 x 16 B each
+// (shared-window addresses: LDS / STS, not generic loads).
 __device__ __forceinline__ void split_chunk(uint8_t* hi, uint8_t* lo, uint32_t t) {
+    const uint32_t h0 = smem_u32(hi), l0 = smem_u32(lo);
+    float4 x[CHUNK_BYTES / 16 / 128];
+#pragma unroll
+    for (int i = 0; i < CHUNK_BYTES / 16 / 128; ++i)
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(x[i].x), "=f"(x[i].y), "=f"(x[i].z), "=f"(x[i].w)
+                     : "r"(h0 + (i * 128 + t) * 16));
 #pragma unroll
     for (int i = 0; i < CHUNK_BYTES / 16 / 128; ++i) {
         const uint32_t off = (i * 128 + t) * 16;
-        float4 x = *reinterpret_cast<const float4*>(hi + off);
-        float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-        *reinterpret_cast<float4*>(hi + off) = h;
-        *reinterpret_cast<float4*>(lo + off) =
-            make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        const float4 h = make_float4(tf32_hi(x[i].x), tf32_hi(x[i].y), tf32_hi(x[i].z), tf32_hi(x[i].w));
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(h0 + off), "f"(h.x), "f"(h.y),
+                     "f"(h.z), "f"(h.w)
+                     : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(l0 + off), "f"(x[i].x - h.x),
+                     "f"(x[i].y - h.y), "f"(x[i].z - h.z), "f"(x[i].w - h.w)
+                     : "memory");
     }
 }
 
