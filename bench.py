@@ -796,23 +796,48 @@ def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau, layer=None):
     (sparse_attention_layer_host -> the C-ABI tsa_sparse_attention_layer_host),
     copies pipelined with the compute.  N GPUs: each rank copies its shard's
     q/k/v from pinned host memory, runs the head-sharded step (global budget,
-    exchanges) and copies its heads' output rows back."""
+    exchanges) and copies its heads' output rows back; two staging sets and a
+    copy stream overlap one step's copies with the neighbouring steps' compute."""
     hq, hk, hv = (t.cpu().pin_memory() for t in (ql, kl, vl))
     hout = torch.empty(ql.shape, dtype=ql.dtype).pin_memory()
     plan = tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0], tau=tau)
     stream = torch.cuda.current_stream(device)
     sharded = world > 1 and layer is not None
     if sharded:
-        dq, dk, dv = (torch.empty_like(t) for t in (ql, kl, vl))
+        # two staging sets and a copy stream: step i's inputs land while step
+        # i-1 computes, and its output rows (copied on the device out of the
+        # layer's exchange buffer first) go back while step i+1 computes
         h0, h1 = layer.shard.h0, layer.shard.h1
+        sets = [tuple(torch.empty_like(t) for t in (ql, kl, vl)) for _ in range(2)]
+        ostage = [torch.empty_like(ql) for _ in range(2)]
+        cstream = torch.cuda.Stream(device)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_sent = [torch.cuda.Event() for _ in range(2)]
+        for ev in ev_out + ev_sent:
+            ev.record(stream)
+        it = [0]
 
     def step():
         if sharded:
-            dq.copy_(hq, non_blocking=True)
-            dk.copy_(hk, non_blocking=True)
-            dv.copy_(hv, non_blocking=True)
+            b = it[0] % 2
+            it[0] += 1
+            dq, dk, dv = sets[b]
+            with torch.cuda.stream(cstream):
+                cstream.wait_event(ev_out[b])  # set b's previous step has consumed it
+                dq.copy_(hq, non_blocking=True)
+                dk.copy_(hk, non_blocking=True)
+                dv.copy_(hv, non_blocking=True)
+                ev_in[b].record(cstream)
+            stream.wait_event(ev_in[b])
+            stream.wait_event(ev_sent[b])  # ostage[b] copied out by its previous step
             out = layer.step(dq, dk, dv)
-            hout.copy_(out[h0:h1], non_blocking=True)
+            ostage[b].copy_(out[h0:h1], non_blocking=True)
+            ev_out[b].record(stream)
+            with torch.cuda.stream(cstream):
+                cstream.wait_event(ev_out[b])
+                hout.copy_(ostage[b], non_blocking=True)
+                ev_sent[b].record(cstream)
         else:
             tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan, device=device)
 
@@ -824,6 +849,8 @@ def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau, layer=None):
     s.record(stream)
     for _ in range(args.steps):
         step()
+    if sharded:
+        stream.wait_stream(cstream)  # the last output rows are home
     e.record(stream)
     torch.cuda.synchronize()
     ms = max_over_ranks(s.elapsed_time(e) / args.steps, world, device)
@@ -843,7 +870,9 @@ def run_e2e(args, tsa, ql, kl, vl, rank, world, device, tau, layer=None):
             "h2d_bytes_per_step": (nb(ql) + nb(kl) + nb(vl)) * world,
             "d2h_bytes_per_step": nb(ql) * world,
             "api": ("ShardedSparseAttention.step on each rank's shard copied from pinned host "
-                    "memory, its heads' output rows copied back" if sharded else
+                    "memory, its heads' output rows copied back; two staging sets on a copy "
+                    "stream overlap a step's copies with the neighbouring steps' compute"
+                    if sharded else
                     "sparse_attention_layer_host (tsa_sparse_attention_layer_host), steps back "
                     "to back: the Q tails, then K two KV heads at a time with their scoring, "
                     "then V and Q head by head with the attention; D2H of each finished head "
