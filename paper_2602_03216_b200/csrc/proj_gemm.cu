@@ -364,11 +364,15 @@ __global__ void prepare_weight_kernel(const T* __restrict__ w, const float* __re
     }
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 }  // namespace
 
 int launch_gemm_bf16(const void* a, const void* b_t, void* c, int M, int N, int K, cudaStream_t st) {
     if (M < 1 || N % GN || K % GK || N < GN || K < GK)
         return invalid("gemm_bf16: needs M >= 1, N a multiple of 256, K a multiple of 64");
+    if (!aligned16(a) || !aligned16(b_t) || !aligned16(c))
+        return invalid("gemm_bf16: a, b_t and c must be 16-byte aligned");
     CUtensorMap ma, mb;
     int rc;
     if ((rc = make_kmajor_map(&ma, a, K, M, CM))) return rc;
@@ -387,6 +391,9 @@ int launch_qkv_proj(const tsa_desc& d, const void* x, int d_model, const void* w
         return invalid("qkv_proj: needs bf16 and d_head 128");
     if (N % GN) return invalid("qkv_proj: (H + 2 Hkv) d must be a multiple of 256");
     if (d_model % GK || d_model < GK) return invalid("qkv_proj: d_model must be a multiple of 64");
+    if (!aligned16(x) || !aligned16(w_t) || !aligned16(table) || !aligned16(q) || !aligned16(k) ||
+        !aligned16(v))
+        return invalid("qkv_proj: x, w_t, table, q, k, v must be 16-byte aligned");
     CUtensorMap ma, mb;
     int rc;
     if ((rc = make_kmajor_map(&ma, x, d_model, L, CM))) return rc;
@@ -408,6 +415,8 @@ int launch_out_proj_residual(const tsa_desc& d, const void* o, const void* wo_t,
     if (d.dtype != TSA_BF16 || d.d_head != kHeadDim)
         return invalid("out_proj_residual: needs bf16 and d_head 128");
     if (d_model % GN || d_model < GN) return invalid("out_proj_residual: d_model must be a multiple of 256");
+    if (!aligned16(o) || !aligned16(wo_t) || !aligned16(x))
+        return invalid("out_proj_residual: o, wo_t and x must be 16-byte aligned");
     CUtensorMap ma, mb;
     int rc;
     if ((rc = make_bf16_map_3d(&ma, o, L, d.n_heads))) return rc;  // 64 x 128 x 1 SW128 boxes

@@ -618,6 +618,10 @@ def qkv_proj(x: torch.Tensor, w_t: torch.Tensor, inv_rms: Optional[torch.Tensor]
     L, D = x.shape
     if w_t.shape != ((n_heads + 2 * n_kv_heads) * d_head, D):
         raise InvalidArgument("qkv_proj: w_t must be [(H + 2 Hkv) d, d_model]")
+    if x.dtype != torch.bfloat16 or w_t.dtype != torch.bfloat16:
+        raise InvalidArgument("qkv_proj: x and w_t must be bf16")
+    if inv_rms is not None and (inv_rms.dtype != torch.float32 or inv_rms.numel() < L):
+        raise InvalidArgument("qkv_proj: inv_rms must be f32 [L]")
     if out is None:
         out = HeadTensors(torch.empty((n_heads, L, d_head), dtype=x.dtype, device=x.device),
                           torch.empty((n_kv_heads, L, d_head), dtype=x.dtype, device=x.device),
@@ -639,6 +643,8 @@ def out_proj_residual(o: torch.Tensor, wo_t: torch.Tensor, x: torch.Tensor) -> t
     D = x.shape[1]
     if x.shape[0] != L or wo_t.shape != (D, H * d):
         raise InvalidArgument("out_proj_residual: shapes do not match")
+    if o.dtype != torch.bfloat16 or wo_t.dtype != torch.bfloat16 or x.dtype != torch.bfloat16:
+        raise InvalidArgument("out_proj_residual: o, wo_t and x must be bf16")
     if not (o.is_contiguous() and x.is_contiguous()):
         raise InvalidArgument("out_proj_residual: o and x must be contiguous")
     desc = _desc_for(H, H, L, d, _dtype_code(o))

@@ -175,3 +175,18 @@ def test_projections_at_cfg4_size_sampled_rows(cuda):
     tsa.out_proj_residual(o, tsa.prepare_weight(wo), x)
     ref = x0 + o[:, rows].permute(1, 0, 2).reshape(-1, H * d).float() @ wo.float()
     close(x[rows], ref)
+
+
+def test_projection_argument_errors(cuda):
+    """Misaligned buffers and wrong dtypes fail loudly (no fault, no silent garbage)."""
+    a = rnd(129, 64)
+    b = rnd(256, 64)
+    c = torch.empty(129 * 256 + 1, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(tsa.InvalidArgument):  # c offset by one element: not 16-B aligned
+        tsa.gemm_bf16(a, b, out=c[1:].view(129, 256))
+    x = rnd(64, 256)
+    table = tsa.rope_table(64, 128, 10000.0, "cuda")
+    with pytest.raises(tsa.InvalidArgument):  # f32 weights
+        tsa.qkv_proj(x, torch.zeros((512, 256), device="cuda"), None, table, 2, 1, 128)
+    with pytest.raises(tsa.InvalidArgument):
+        tsa.out_proj_residual(rnd(2, 64, 128), torch.zeros((256, 256), device="cuda"), x)
