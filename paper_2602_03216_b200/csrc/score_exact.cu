@@ -450,12 +450,19 @@ constexpr int XC_STAGES = 2;
 
 // e / sum, correctly rounded, from y = RN(1/sum): q = RN(e y), r = e - q sum
 // (exact, FMA), RN(q + r y) = RN(e / sum) (Markstein) -- valid while the
-// quotient is normal (e >= 2^-100 > 2^-126 * sum for sum <= 2^26).
+// quotient is normal (e >= 2^-100 > 2^-126 * sum for sum <= 2^26).  Below
+// that: e = 0 gives 0, and a tiny e is divided in double and rounded once more
+// to f32 -- exact, as double rounding is innocuous for a quotient computed with
+// at least 2 * 24 + 2 bits (sharp maps have many such e: __fdiv_rn's slow path
+// made the column pass 4x slower on cfg4's layers).
 __device__ __forceinline__ float div_rn(float e, float sum, float y) {
-    const float q = __fmul_rn(e, y);
-    const float r = __fmaf_rn(-q, sum, e);
-    const float q1 = __fmaf_rn(r, y, q);
-    return e >= 0x1p-100f ? q1 : __fdiv_rn(e, sum);
+    if (e >= 0x1p-100f) {
+        const float q = __fmul_rn(e, y);
+        const float r = __fmaf_rn(-q, sum, e);
+        return __fmaf_rn(r, y, q);
+    }
+    if (e == 0.0f) return 0.0f;
+    return __double2float_rn(__ddiv_rn((double)e, (double)sum));
 }
 
 // shared memory: [XcHead][rs: lq x float4][n_st x X chunk (32 KB)]

@@ -60,13 +60,16 @@ SHAPES = [  # H, Hkv, L, last_q, generator
     (2, 1, 130, 7, "tail"),
     (6, 3, 2049, 64, "tail"),     # L % 64 == 1
     (32, 8, 16384, 64, "tail"),
+    (8, 2, 4096, 64, "sharp"),    # logits over hundreds: tiny / zero e, the slow quotients
 ]
 
 
 @pytest.mark.parametrize("H,Hkv,L,lq,gen", SHAPES)
 def test_exact_scores_bitwise_vs_oracle(cuda, port, H, Hkv, L, lq, gen):
-    if gen == "tail":
+    if gen in ("tail", "sharp"):
         q, k, v = workloads.heavy_tailed_heads(H, Hkv, L, 128, seed=L + H, last_q=lq)
+        if gen == "sharp":  # cfg4-like sharp maps (a per-layer q/k gain)
+            q = (q.float() * 6.0).to(torch.bfloat16)
     else:
         qn, kn, vn = gqa_heads(RefRng(L + 7 * H), H, Hkv, L, 128)
         q, k = (torch.from_numpy(a).cuda().to(torch.bfloat16) for a in (qn, kn))
