@@ -130,6 +130,29 @@ class PrefillAttentionStack:
         self.plan = plan
         self.attn = ShardedSparseAttention(self.H, self.Hkv, self.L, self.d, self.dtype, plan,
                                            device=self.device, scoring=self.scoring)
+        self._graphs = {}
+
+    def forward_graphed(self, x: torch.Tensor, dense: bool = False) -> torch.Tensor:
+        """``forward`` replayed from one CUDA graph per (x buffer, plan): the whole
+        stack is a fixed launch sequence (every k_keep stays on the device), so
+        the ~15 host launches per layer and their gaps collapse into one graph
+        launch.  The first call for a buffer runs eagerly (its result is the
+        forward's) and captures the graph for the next ones."""
+        key = (x.data_ptr(), bool(dense), tuple(self.plan.sparse_layers or ()), self.plan.mode,
+               self.plan.tau, self.plan.s_fixed)
+        graphs = self.__dict__.setdefault("_graphs", {})
+        g = graphs.get(key)
+        if g is None:
+            self.forward(x, dense=dense)  # eager: the result, and every cache warm
+            saved = x.clone()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.forward(x, dense=dense)
+            x.copy_(saved)  # capture records the launches without running them
+            graphs[key] = g
+            return x
+        g.replay()
+        return x
 
     def layer(self, i: int, x: torch.Tensor, dense: bool = False, marks=None) -> torch.Tensor:
         """One attention branch in place on the residual stream x [L, D]."""

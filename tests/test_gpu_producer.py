@@ -227,3 +227,21 @@ def test_report_harness_rows(cuda):
         for r in rows:
             assert float(r["ms"]) > 0 and float(r["est_speedup"]) >= 1.0
             assert 1 <= float(r["avg_k_keep"]) <= 2048
+
+
+def test_stack_graphed_forward_equals_eager(cuda):
+    """forward_graphed (one CUDA graph for the whole stack) == forward, bitwise, on
+    the capturing call and on replays, with the per-layer budgets kept."""
+    from paper_2602_03216_b200.stack import structured_hidden
+    L = 2048
+    st = _stack(L, n_layers=3)
+    x0 = structured_hidden(L, 512, seed=6)
+    ref = st.forward(x0.clone())
+    kk_ref = st.k_keep.clone()
+    x = torch.empty_like(x0)
+    for _ in range(3):
+        x.copy_(x0)
+        st.forward_graphed(x)
+        torch.cuda.synchronize()
+        assert torch.equal(x.view(torch.int16), ref.view(torch.int16))
+        assert torch.equal(st.k_keep, kk_ref)

@@ -27,3 +27,12 @@ st.forward(x)
 ev[1].record()
 torch.cuda.synchronize()
 print("forward ms", round(ev[0].elapsed_time(ev[1]), 1), "k_keep", st.k_keep.cpu().tolist())
+x.copy_(x0)
+st.forward_graphed(x)  # eager + capture
+torch.cuda.synchronize()
+x.copy_(x0)
+ev[0].record()
+st.forward_graphed(x)
+ev[1].record()
+torch.cuda.synchronize()
+print("graphed forward ms", round(ev[0].elapsed_time(ev[1]), 1))
