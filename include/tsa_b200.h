@@ -295,15 +295,17 @@ TSA_API int tsa_sparse_attention_layer(const tsa_desc* d, const void* q, const v
 /* The layer on HOST tensors (the reference's calling convention: its operators
  * take host matrices): q/k/v/out_host [H|Hkv][L][d] in host memory (pinned for
  * asynchronous copies), q/k/v/out device staging buffers of the same shapes.
- * The transfers are pipelined with the compute: K, V and the Q tail rows are
- * copied first (scoring needs them), the remaining Q rows follow in n_groups
- * head groups (0 = one per KV head) while the compute stream scores, selects
- * and compresses; the attention runs per head group as its Q rows arrive and
- * each group's output rows are copied back while the next group computes.  The
- * first and the last group run head by head, so the attention starts after one
- * head's rows arrive and the final copy back is one head's rows.
- * Completion on `stream` covers every copy.  f32 / d != 128 / dense mode: one
- * copy in, the layer, one copy out. */
+ * The transfers are pipelined with the compute: the Q tail rows first, then K
+ * two KV heads at a time, each pair scored as soon as it has arrived (scoring
+ * needs all of K before the budget, so all but the last pair's scoring hides
+ * under the copy); then, per group of n_groups (0 = one per KV head), the
+ * group's V heads and its Q rows head by head: the group's K/V are compressed
+ * once, each head's attention starts when its Q rows have arrived and its
+ * output rows are copied back while the next head computes (more than 64 query
+ * heads: whole groups, the first and last head by head).  Completion on
+ * `stream` covers every copy; a caller may overlap consecutive calls by
+ * alternating two buffer sets (q..out, ws) on two streams.  f32 / d != 128 /
+ * dense mode: one copy in, the layer, one copy out. */
 TSA_API int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_host,
                                             const void* k_host, const void* v_host,
                                             void* out_host, void* q, void* k, void* v, void* out,
