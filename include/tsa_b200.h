@@ -314,9 +314,11 @@ TSA_API int tsa_sparse_attention_layer_host(const tsa_desc* d, const void* q_hos
                                             void* stream);
 
 /* ---- Attention-branch producer / consumer (layer_forward, model.cpp:169-201) ----
- * The kernels cfg4's 32-layer prefill stack runs around the path; the
- * projections themselves (x W_q|k|v, cat W_o) are plain GEMMs for the caller's
- * BLAS (cuBLAS).  Row-major, dtype TSA_F32 or TSA_BF16 (compute in f32). */
+ * The unfused stages around the path: rms_norm, RoPE + head split, head
+ * concat (a caller's BLAS does the projections between them); the fused
+ * tcgen05 projections that replace the whole chain follow below
+ * (tsa_qkv_proj, tsa_out_proj_residual).  Row-major, dtype TSA_F32 or
+ * TSA_BF16 (compute in f32). */
 
 /* rms_norm (model.cpp:81-94): out[r] = (x[r] * inv_r) * gain, inv_r =
  * 1 / sqrt(sum_j x[r, j]^2 / cols + eps), the sum taken sequentially in f32 as

@@ -17,8 +17,9 @@
 //                                       the token mean summed t ascending (the
 //                                       reference's order: bit-exact for f32)
 //
-// The projections themselves (x W_q, x W_k, x W_v, cat W_o) are plain GEMMs and
-// go to cuBLAS through the host; everything here is HBM-bound byte movement.
+// These are the unfused stages (a caller's BLAS does the projections between
+// them); the cfg4 stack runs the fused tcgen05 projections of proj_gemm.cu
+// instead.  Everything here is HBM-bound byte movement.
 #include <cmath>
 
 #include "common.cuh"
