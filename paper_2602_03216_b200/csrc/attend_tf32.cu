@@ -31,6 +31,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -63,9 +65,9 @@ struct __align__(1024) Tf32Smem {
 };
 
 // kind::tf32: D f32, A / B TF32, M 128, N 128.
-__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t b_mn_major) {
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t b_mn_major, uint32_t m = 128) {
     return (1u << 4) | (2u << 7) | (2u << 10) | (b_mn_major << 16) | ((128u >> 3) << 17) |
-           ((128u >> 4) << 24);
+           ((m >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32_ss_p(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
@@ -112,16 +114,17 @@ __device__ __forceinline__ float tf32_hi(float x) {
 
 // 16 KiB raw chunk -> hi in place, lo into `lo`; 128 threads, 8 x 16 B each
 // (shared-window addresses: LDS / STS, not generic loads).
+template <int BYTES = CHUNK_BYTES>
 __device__ __forceinline__ void split_chunk(uint8_t* hi, uint8_t* lo, uint32_t t) {
     const uint32_t h0 = smem_u32(hi), l0 = smem_u32(lo);
-    float4 x[CHUNK_BYTES / 16 / 128];
+    float4 x[BYTES / 16 / 128];
 #pragma unroll
-    for (int i = 0; i < CHUNK_BYTES / 16 / 128; ++i)
+    for (int i = 0; i < BYTES / 16 / 128; ++i)
         asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
                      : "=f"(x[i].x), "=f"(x[i].y), "=f"(x[i].z), "=f"(x[i].w)
                      : "r"(h0 + (i * 128 + t) * 16));
 #pragma unroll
-    for (int i = 0; i < CHUNK_BYTES / 16 / 128; ++i) {
+    for (int i = 0; i < BYTES / 16 / 128; ++i) {
         const uint32_t off = (i * 128 + t) * 16;
         const float4 h = make_float4(tf32_hi(x[i].x), tf32_hi(x[i].y), tf32_hi(x[i].z), tf32_hi(x[i].w));
         asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(h0 + off), "f"(h.x), "f"(h.y),
@@ -141,11 +144,13 @@ attend_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     extern __shared__ uint8_t smem_raw[];
     Tf32Smem& sm = *reinterpret_cast<Tf32Smem*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int h = head_begin + blockIdx.y;
+    // grid (heads, tile slots): the launch order walks every head's heaviest
+    // tile before any head's next one (longest-first over the whole layer)
+    const int h = head_begin + blockIdx.x;
     const int n = n_dev ? *n_dev : n_const;
     const int n_tiles = (n + TBM - 1) / TBM;
-    if ((int)blockIdx.x >= n_tiles) return;
-    const int t = n_tiles - 1 - (int)blockIdx.x;  // heaviest tiles first
+    if ((int)blockIdx.y >= n_tiles) return;
+    const int t = n_tiles - 1 - (int)blockIdx.y;  // heaviest tiles first
     const int nkv = t + 1;
     const int kvh = h / kv_group;
     const uint32_t warp = warp_id_uniform();
@@ -273,17 +278,20 @@ attend_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             mbar_wait(&sm.s_full[j & 1], (j >> 1) & 1);
             tc_fence_after();
             const bool diag = j == t;
-            // pass 1: row max of the scaled, masked logits
+            // pass 1: row max of the scaled, masked logits (the four 32-column
+            // loads in flight together, one wait)
             float mx = -INFINITY;
-#pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tmem_ld32(t_s + lane_off + c * 32, r);
+            {
+                uint32_t sr[128];
+                tmem_ld32_at<0>(t_s + lane_off, sr);
+                tmem_ld32_at<32>(t_s + lane_off + 32, sr);
+                tmem_ld32_at<64>(t_s + lane_off + 64, sr);
+                tmem_ld32_at<96>(t_s + lane_off + 96, sr);
                 tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int key = j * TBM + c * 32 + e;
-                    const float x = __fmul_rn(__uint_as_float(r[e]), scale);
+                for (int e = 0; e < 128; ++e) {
+                    const int key = j * TBM + e;
+                    const float x = __fmul_rn(__uint_as_float(sr[e]), scale);
                     if (!diag || key <= row) mx = fmaxf(mx, x);
                 }
             }
@@ -307,24 +315,30 @@ attend_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             }
             l *= corr;
             m = m_new;
-            // pass 2: p, the row sum, P_hi over S and P_lo beside it
+            // pass 2: p, the row sum, P_hi over S and P_lo beside it (64 columns
+            // loaded per wait)
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32], rl[32];
-                tmem_ld32(t_s + lane_off + c * 32, r);
+            for (int hc = 0; hc < 2; ++hc) {
+                uint32_t sr[64];
+                tmem_ld32_at<0>(t_s + lane_off + hc * 64, sr);
+                tmem_ld32_at<32>(t_s + lane_off + hc * 64 + 32, sr);
                 tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int key = j * TBM + c * 32 + e;
-                    const float x = __fmul_rn(__uint_as_float(r[e]), scale);
-                    const float p = (!diag || key <= row) ? ex2_approx(__fmul_rn(x - m, kLog2e)) : 0.0f;
-                    l += p;
-                    const float ph = tf32_hi(p);
-                    r[e] = __float_as_uint(ph);
-                    rl[e] = __float_as_uint(p - ph);
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t rh[32], rl[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int key = j * TBM + hc * 64 + c * 32 + e;
+                        const float x = __fmul_rn(__uint_as_float(sr[c * 32 + e]), scale);
+                        const float p = (!diag || key <= row) ? ex2_approx(__fmul_rn(x - m, kLog2e)) : 0.0f;
+                        l += p;
+                        const float ph = tf32_hi(p);
+                        rh[e] = __float_as_uint(ph);
+                        rl[e] = __float_as_uint(p - ph);
+                    }
+                    tmem_st32(t_s + lane_off + hc * 64 + c * 32, rh);
+                    tmem_st32(t_lo + lane_off + hc * 64 + c * 32, rl);
                 }
-                tmem_st32(t_s + lane_off + c * 32, r);
-                tmem_st32(t_lo + lane_off + c * 32, rl);
             }
             tmem_wait_st();
             tc_fence_before();
@@ -353,6 +367,285 @@ attend_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------- CTA pairs
+// The same attention on 2-CTA clusters (cta_group::2): the pair's two CTAs
+// hold query tiles 2p and 2p+1 of a head (128 rows each, M = 256 per MMA) and
+// share every K / V chunk -- each CTA stages and splits only its half (64 keys
+// of a K chunk, 64 dims of a V chunk) and the tensor cores exchange the B
+// halves.  Per SM this halves the B-operand shared-memory reads, the split
+// work and the TMA bytes: the single-CTA kernel's S MMA reads A and B at
+// 128 B/clk, the whole shared-memory bandwidth, so it cannot keep the tensor
+// pipe busy (ncu: 45 %).  The pair walks KV tiles 0..2p+1; tile 2p+1 is fully
+// masked for the lower tile (its MMA work is the price of sharing).
+// The leader (cluster rank 0) issues the MMAs; the split and softmax threads
+// of both CTAs arrive on the leader's barriers; the MMA commits multicast to
+// both CTAs.
+constexpr int HALF_BYTES = CHUNK_BYTES / 2;  // [64 x 32] f32 = 8 KiB
+constexpr int NSTG2 = 6;
+
+struct __align__(1024) Tf32PairSmem {
+    uint8_t q_hi[4][CHUNK_BYTES];
+    uint8_t q_lo[4][CHUNK_BYTES];
+    uint8_t hi[NSTG2][HALF_BYTES];
+    uint8_t lo[NSTG2][HALF_BYTES];
+    uint64_t q_full, q_ready;
+    uint64_t raw_full[NSTG2], conv_full[NSTG2], empty[NSTG2];
+    uint64_t s_full[2], p_full, pv_done;
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void mma_tf32_ss_pair_p(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                   uint32_t idesc, uint32_t accumulate,
+                                                   uint32_t issue) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.ne.b32 q, %5, 0;\n"
+        "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(issue)
+        : "memory");
+}
+__device__ __forceinline__ void mma_tf32_ts_pair_p(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                   uint32_t idesc, uint32_t accumulate,
+                                                   uint32_t issue) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.ne.b32 q, %5, 0;\n"
+        "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(issue)
+        : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTf32Threads, 1)
+attend_tf32_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ n_dev,
+                        int n_const, int kv_group, int rows_per_head, int head_begin, float scale,
+                        float* __restrict__ o) {
+    extern __shared__ uint8_t smem_raw[];
+    Tf32PairSmem& sm = *reinterpret_cast<Tf32PairSmem*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // grid (2 x heads, pair slots), clusters along x: longest-first over the layer
+    const int h = head_begin + ((int)blockIdx.x >> 1);
+    const int n = n_dev ? *n_dev : n_const;
+    const int n_tiles = (n + TBM - 1) / TBM;
+    const int n_pairs = (n_tiles + 1) / 2;
+    const int cid = (int)blockIdx.y;
+    if (cid >= n_pairs) return;  // uniform over the pair
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int p = n_pairs - 1 - cid;  // heaviest pairs first
+    const int t = 2 * p + (int)rank;  // this CTA's query tile
+    const int nkv = min(2 * p + 2, n_tiles);
+    const int kvh = h / kv_group;
+    const uint32_t warp = warp_id_uniform();
+    const uint32_t lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.q_full, 1);
+        mbar_init(&sm.q_ready, 256);
+        for (int s = 0; s < NSTG2; ++s) {
+            mbar_init(&sm.raw_full[s], 1);
+            mbar_init(&sm.conv_full[s], 256);
+            mbar_init(&sm.empty[s], 1);
+        }
+        mbar_init(&sm.s_full[0], 1);
+        mbar_init(&sm.s_full[1], 1);
+        mbar_init(&sm.p_full, 256);
+        mbar_init(&sm.pv_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_pair(&sm.tmem_base, 512);
+    tc_fence_before();
+    cluster_sync_all();  // barriers initialised in both CTAs before any remote arrival
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+    const uint32_t t_lo = tmem + 256, t_o = tmem + 384;
+    const int n_items = nkv * 8;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA (both CTAs)
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&sm.q_full, 4 * CHUNK_BYTES);
+            for (int c = 0; c < 4; ++c) tma_load_3d(sm.q_hi[c], &tm_q, &sm.q_full, 32 * c, t * TBM, h);
+            int it = 0;
+            auto load = [&](int j, bool is_v) {
+                for (int c = 0; c < 4; ++c, ++it) {
+                    const int s = it % NSTG2;
+                    if (it >= NSTG2) mbar_wait(&sm.empty[s], ((it / NSTG2) - 1) & 1);
+                    mbar_arrive_expect_tx(&sm.raw_full[s], HALF_BYTES);
+                    if (!is_v) {  // keys [64 rank, +64) of tile j, dims [32 c, +32)
+                        tma_load_3d(sm.hi[s], &tm_k, &sm.raw_full[s], 32 * c, j * TBM + 64 * (int)rank, kvh);
+                    } else {  // keys [32 c, +32) of tile j, dims [64 rank, +64): two N atoms
+                        for (int a = 0; a < 2; ++a)
+                            tma_load_3d(sm.hi[s] + a * 4096, &tm_v, &sm.raw_full[s],
+                                        64 * (int)rank + 32 * a, j * TBM + 32 * c, kvh);
+                    }
+                }
+            };
+            load(0, false);
+            for (int j = 0; j < nkv; ++j) {
+                if (j + 1 < nkv) load(j + 1, false);
+                load(j, true);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA (leader)
+        if (leader) {
+            const uint32_t issue = elect_one() ? 1u : 0u;
+            constexpr uint32_t id_s = idesc_tf32(0, 256), id_pv = idesc_tf32(1, 256);
+            mbar_wait_cluster(&sm.q_ready, 0);
+            tc_fence_after();
+            int it = 0;
+            auto issue_s = [&](int j) {
+                const uint32_t t_s = tmem + 128 * (j & 1);
+                for (int c = 0; c < 4; ++c, ++it) {
+                    const int s = it % NSTG2;
+                    mbar_wait_cluster(&sm.conv_full[s], (it / NSTG2) & 1);
+                    tc_fence_after();
+                    const uint32_t qh = smem_u32(sm.q_hi[c]), ql = smem_u32(sm.q_lo[c]);
+                    const uint32_t kh = smem_u32(sm.hi[s]), kl = smem_u32(sm.lo[s]);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t off = kk * 32;
+                        mma_tf32_ss_pair_p(t_s, kdesc(qh + off), kdesc(kh + off), id_s, (c | kk) ? 1u : 0u, issue);
+                        mma_tf32_ss_pair_p(t_s, kdesc(qh + off), kdesc(kl + off), id_s, 1u, issue);
+                        mma_tf32_ss_pair_p(t_s, kdesc(ql + off), kdesc(kh + off), id_s, 1u, issue);
+                    }
+                    mma_commit_pair_p(&sm.empty[s], issue);
+                }
+                mma_commit_pair_p(&sm.s_full[j & 1], issue);
+            };
+            issue_s(0);
+            for (int j = 0; j < nkv; ++j) {
+                if (j + 1 < nkv) issue_s(j + 1);
+                mbar_wait_cluster(&sm.p_full, j & 1);
+                tc_fence_after();
+                const uint32_t t_p = tmem + 128 * (j & 1);
+                for (int c = 0; c < 4; ++c, ++it) {
+                    const int s = it % NSTG2;
+                    mbar_wait_cluster(&sm.conv_full[s], (it / NSTG2) & 1);
+                    tc_fence_after();
+                    const uint32_t vh = smem_u32(sm.hi[s]), vl = smem_u32(sm.lo[s]);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t col = c * 32 + kk * 8, off = kk * 1024;
+                        mma_tf32_ts_pair_p(t_o, t_p + col, ndesc(vh + off), id_pv, (j | c | kk) ? 1u : 0u, issue);
+                        mma_tf32_ts_pair_p(t_o, t_p + col, ndesc(vl + off), id_pv, 1u, issue);
+                        mma_tf32_ts_pair_p(t_o, t_lo + col, ndesc(vh + off), id_pv, 1u, issue);
+                    }
+                    mma_commit_pair_p(&sm.empty[s], issue);
+                }
+                mma_commit_pair_p(&sm.pv_done, issue);
+            }
+        }
+    } else if (warp < 6) {
+        // ---------------------------------------------------------------- split (both CTAs)
+        const uint32_t tid = threadIdx.x - 64;
+        mbar_wait(&sm.q_full, 0);
+        for (int c = 0; c < 4; ++c) split_chunk(sm.q_hi[c], sm.q_lo[c], tid);
+        fence_proxy_async_smem();
+        mbar_arrive_leader_release(&sm.q_ready);
+        for (int it = 0; it < n_items; ++it) {
+            const int s = it % NSTG2;
+            mbar_wait(&sm.raw_full[s], (it / NSTG2) & 1);
+            split_chunk<HALF_BYTES>(sm.hi[s], sm.lo[s], tid);
+            fence_proxy_async_smem();
+            mbar_arrive_leader_release(&sm.conv_full[s]);
+        }
+    } else {
+        // ---------------------------------------------------------------- softmax (both CTAs)
+        const uint32_t quarter = warp & 3;
+        const int row = t * TBM + (int)(quarter * 32 + lane);
+        const uint32_t lane_off = (quarter * 32) << 16;
+        float m = -INFINITY, l = 0.0f;
+        for (int j = 0; j < nkv; ++j) {
+            const uint32_t t_s = tmem + 128 * (j & 1);
+            mbar_wait(&sm.s_full[j & 1], (j >> 1) & 1);
+            tc_fence_after();
+            const bool masked = j >= t;  // the diagonal tile, or (lower tile) the one past it
+            float mx = -INFINITY;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                tmem_ld32(t_s + lane_off + c * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int key = j * TBM + c * 32 + e;
+                    const float x = __fmul_rn(__uint_as_float(r[e]), scale);
+                    if (!masked || key <= row) mx = fmaxf(mx, x);
+                }
+            }
+            if (j > 0) {
+                mbar_wait(&sm.pv_done, (j - 1) & 1);
+                tc_fence_after();
+            }
+            const float m_new = fmaxf(m, mx);
+            const float corr = (m == -INFINITY) ? 0.0f : ex2_approx(__fmul_rn(m - m_new, kLog2e));
+            if (j > 0 && __any_sync(0xffffffffu, corr != 1.0f)) {
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(t_o + lane_off + c * 32, r);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * corr);
+                    tmem_st32(t_o + lane_off + c * 32, r);
+                }
+            }
+            l *= corr;
+            m = m_new;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32], rl[32];
+                tmem_ld32(t_s + lane_off + c * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int key = j * TBM + c * 32 + e;
+                    const float x = __fmul_rn(__uint_as_float(r[e]), scale);
+                    const float pe = (!masked || key <= row) ? ex2_approx(__fmul_rn(x - m, kLog2e)) : 0.0f;
+                    l += pe;
+                    const float ph = tf32_hi(pe);
+                    r[e] = __float_as_uint(ph);
+                    rl[e] = __float_as_uint(pe - ph);
+                }
+                tmem_st32(t_s + lane_off + c * 32, r);
+                tmem_st32(t_lo + lane_off + c * 32, rl);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive_leader_release(&sm.p_full);
+        }
+        mbar_wait(&sm.pv_done, (nkv - 1) & 1);
+        tc_fence_after();
+        const float inv_l = 1.0f / l;
+        float* dst = o + ((size_t)h * rows_per_head + row) * TD;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld32(t_o + lane_off + c * 32, r);
+            tmem_wait_ld();
+            if (row < n) {
+#pragma unroll
+                for (int e = 0; e < 32; e += 4)
+                    *reinterpret_cast<float4*>(dst + c * 32 + e) =
+                        make_float4(__uint_as_float(r[e]) * inv_l, __uint_as_float(r[e + 1]) * inv_l,
+                                    __uint_as_float(r[e + 2]) * inv_l, __uint_as_float(r[e + 3]) * inv_l);
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // the leader's MMAs into this CTA's TMEM / smem are complete
+    if (warp == 1) tmem_dealloc_pair(tmem, 512);
+}
+
 // 3-D [heads x rows x 128] f32, boxes of 32 x box_rows x 1 (128-B rows),
 // swizzled for the operand's major-ness: rows past a head's end read zeros.
 int make_f32_heads_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t heads,
@@ -373,6 +666,15 @@ int make_f32_heads_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t
 
 }  // namespace
 
+// The single-CTA kernel by default; TSA_TF32_PAIRS=1 selects the 2-CTA one
+// (measured slower at cfg1: 237 vs 183 us under ncu, profiles/r2/ab_notes.txt;
+// kept as the measured alternative and as a second implementation the tests
+// compare against).
+static bool tf32_pairs() {
+    const char* e = getenv("TSA_TF32_PAIRS");
+    return e && e[0] == '1';
+}
+
 bool attend_tf32_supported(const tsa_desc& d) { return d.dtype == TSA_F32 && d.d_head == TD; }
 
 int launch_attend_tf32(const tsa_desc& d, const void* q, const void* k, const void* v,
@@ -384,15 +686,28 @@ int launch_attend_tf32(const tsa_desc& d, const void* q, const void* k, const vo
     CUtensorMap mq, mk, mv;
     int rc;
     constexpr CUtensorMapSwizzle kK = CU_TENSOR_MAP_SWIZZLE_128B, kMN = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+    const bool pair = tf32_pairs();
     if ((rc = make_f32_heads_map(&mq, q, rows_per_head, d.n_heads, 128, kK))) return rc;
-    if ((rc = make_f32_heads_map(&mk, k, kv_rows_per_head, n_kv_buf, 128, kK))) return rc;
+    if ((rc = make_f32_heads_map(&mk, k, kv_rows_per_head, n_kv_buf, pair ? 64 : 128, kK))) return rc;
     if ((rc = make_f32_heads_map(&mv, v, kv_rows_per_head, n_kv_buf, 32, kMN))) return rc;
+    const float scale = 1.0f / sqrtf((float)TD);
+    if (pair) {
+        const int smem = (int)sizeof(Tf32PairSmem) + 1024;
+        if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(attend_tf32_pair_kernel), smem)))
+            return rc;
+        const int max_pairs = ((rows_per_head + TBM - 1) / TBM + 1) / 2;
+        dim3 grid(2 * nh, max_pairs);
+        attend_tf32_pair_kernel<<<grid, kTf32Threads, smem, st>>>(
+            mq, mk, mv, n_dev, n_const, kv_group, rows_per_head, d.head_begin, scale,
+            static_cast<float*>(o));
+        TSA_LAUNCH_CHECK("attend_tf32_pair");
+        return 0;
+    }
     const int smem = (int)sizeof(Tf32Smem) + 1024;
     if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(attend_tf32_kernel), smem))) return rc;
-    dim3 grid((rows_per_head + TBM - 1) / TBM, nh);
+    dim3 grid(nh, (rows_per_head + TBM - 1) / TBM);
     attend_tf32_kernel<<<grid, kTf32Threads, smem, st>>>(mq, mk, mv, n_dev, n_const, kv_group,
-                                                        rows_per_head, d.head_begin,
-                                                        1.0f / sqrtf((float)TD),
+                                                        rows_per_head, d.head_begin, scale,
                                                         static_cast<float*>(o));
     TSA_LAUNCH_CHECK("attend_tf32");
     return 0;

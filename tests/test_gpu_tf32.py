@@ -89,3 +89,20 @@ def test_tf32_sparse_layer_selected_rows(cuda, port):
     ref = port.token_sparse_attention(q, k, v, idx)
     assert np.abs(out.cpu().numpy() - ref).max() <= parity.F32_GATE
     assert parity.unselected_rows_zero(out.cpu().numpy(), idx, 1500)
+
+
+@pytest.mark.parametrize("L", [100, 256, 385, 1000, 2047, 4096])
+@pytest.mark.parametrize("pairs", ["0", "1"])
+def test_tf32_single_and_pair_kernels(cuda, monkeypatch, L, pairs):
+    """Both implementations (TSA_TF32_PAIRS: 2-CTA clusters sharing K / V halves,
+    or one CTA per tile) at the gate, on odd and even tile counts (the last pair's
+    upper tile absent) -- and they agree with each other to f32 rounding."""
+    monkeypatch.setenv("TSA_TF32_PAIRS", pairs)
+    q, k, v = (uniform((3, L, 128), s) for s in (21, 22, 23))
+    out, _ = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), tsa.SparsePlan())
+    for h in range(3):
+        err = (out[h].double() - ref_attention(q[h], k[h], v[h])).abs().max().item()
+        assert err <= parity.F32_GATE, (h, err)
+    monkeypatch.setenv("TSA_TF32_PAIRS", "1" if pairs == "0" else "0")
+    other, _ = tsa.sparse_attention_layer(tsa.HeadTensors(q, k, v), tsa.SparsePlan())
+    assert (out - other).abs().max().item() <= 2e-6
