@@ -26,7 +26,22 @@ constexpr int LG_ROWS = 64;   // max lq rows handled per block (lq <= 64 per til
 constexpr int LG_KEYS = 128;  // keys per block
 constexpr int LG_PCH = 32;    // d-chunk staged in smem
 
-// Block: 256 threads = 16 row-groups (4 rows) x 16 key-groups (8 keys).
+// Four consecutive elements of a row as f32 (16-B / 8-B vector load).
+__device__ __forceinline__ void load4(const float* p, float (&x)[4]) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+}
+__device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&x)[4]) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    x[0] = __uint_as_float(v.x << 16), x[1] = __uint_as_float(v.x & 0xFFFF0000u);
+    x[2] = __uint_as_float(v.y << 16), x[3] = __uint_as_float(v.y & 0xFFFF0000u);
+}
+
+// Block: 256 threads = 16 row-groups (4 rows) x 16 key-groups (8 keys: 4 at
+// tk*4 and 4 at 64 + tk*4, so a half-warp's float4 reads of a staged key row
+// are 256 contiguous bytes -- two wavefronts, no bank conflicts).  Each
+// (row, key) dot product runs in p order with separate multiply and add
+// (matmul in p order, tensor_ops.cpp:19-23, called at token_coverage.cpp:31).
 template <typename T>
 // Lp > 0: the exact scorer's layout -- rows (local head, r) at stride Lp, and
 // each row's maximum (atomicMax of the ordered encoding into rowmax) for the
@@ -36,10 +51,10 @@ __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q,
                                                         int L, int d, int lq, int head_begin,
                                                         float inv_sqrt_d, int Lp,
                                                         int* __restrict__ rowmax) {
-    // +1 pitch: the staging stores walk p fastest (coalesced global reads), which
-    // without it would hit one bank 32 times per warp
-    __shared__ float qs[LG_PCH][LG_ROWS + 1];
-    __shared__ float ks[LG_PCH][LG_KEYS + 1];
+    // pitches of 4 floats over the tile widths: rows stay 16-B aligned for the
+    // float4 reads
+    __shared__ __align__(16) float qs[LG_PCH][LG_ROWS + 4];
+    __shared__ __align__(16) float ks[LG_PCH][LG_KEYS + 4];
     const int h = head_begin + blockIdx.y;
     const int r_base = blockIdx.z * LG_ROWS;
     const int j0 = blockIdx.x * LG_KEYS;
@@ -49,6 +64,7 @@ __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q,
     const T* qh = q + ((size_t)h * L + (L - lq)) * d;
     const T* kh = k + (size_t)kv * L * d;
     const int tr = threadIdx.x / 16, tk = threadIdx.x % 16;
+    const bool vec = (d % LG_PCH) == 0;  // whole chunks: 4-element vector staging
     float acc[4][8];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -58,23 +74,42 @@ __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q,
     for (int p0 = 0; p0 < d; p0 += LG_PCH) {
         const int pn = min(LG_PCH, d - p0);
         __syncthreads();
-        for (int e = threadIdx.x; e < LG_ROWS * LG_PCH; e += 256) {
-            const int r = e / LG_PCH, p = e % LG_PCH;
-            const int rr = r_base + r;
-            qs[p][r] = (rr < lq && p < pn) ? Elem<T>::to_f32(qh[(size_t)rr * d + p0 + p]) : 0.0f;
-        }
-        for (int e = threadIdx.x; e < LG_KEYS * LG_PCH; e += 256) {
-            const int j = e / LG_PCH, p = e % LG_PCH;
-            const int jj = j0 + j;
-            ks[p][j] = (jj < L && p < pn) ? Elem<T>::to_f32(kh[(size_t)jj * d + p0 + p]) : 0.0f;
+        if (vec) {
+            for (int e = threadIdx.x; e < LG_ROWS * LG_PCH / 4; e += 256) {
+                const int r = e / (LG_PCH / 4), p4 = 4 * (e % (LG_PCH / 4));
+                const int rr = r_base + r;
+                float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                if (rr < lq) load4(qh + (size_t)rr * d + p0 + p4, x);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) qs[p4 + i][r] = x[i];
+            }
+            for (int e = threadIdx.x; e < LG_KEYS * LG_PCH / 4; e += 256) {
+                const int j = e / (LG_PCH / 4), p4 = 4 * (e % (LG_PCH / 4));
+                const int jj = j0 + j;
+                float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                if (jj < L) load4(kh + (size_t)jj * d + p0 + p4, x);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) ks[p4 + i][j] = x[i];
+            }
+        } else {
+            for (int e = threadIdx.x; e < LG_ROWS * LG_PCH; e += 256) {
+                const int r = e / LG_PCH, p = e % LG_PCH;
+                const int rr = r_base + r;
+                qs[p][r] = (rr < lq && p < pn) ? Elem<T>::to_f32(qh[(size_t)rr * d + p0 + p]) : 0.0f;
+            }
+            for (int e = threadIdx.x; e < LG_KEYS * LG_PCH; e += 256) {
+                const int j = e / LG_PCH, p = e % LG_PCH;
+                const int jj = j0 + j;
+                ks[p][j] = (jj < L && p < pn) ? Elem<T>::to_f32(kh[(size_t)jj * d + p0 + p]) : 0.0f;
+            }
         }
         __syncthreads();
         for (int p = 0; p < pn; ++p) {
-            float qa[4], kb[8];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) qa[a] = qs[p][tr * 4 + a];
-#pragma unroll
-            for (int b = 0; b < 8; ++b) kb[b] = ks[p][tk * 8 + b];
+            const float4 qv = *reinterpret_cast<const float4*>(&qs[p][tr * 4]);
+            const float4 k0 = *reinterpret_cast<const float4*>(&ks[p][tk * 4]);
+            const float4 k1 = *reinterpret_cast<const float4*>(&ks[p][64 + tk * 4]);
+            const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+            const float kb[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -90,7 +125,7 @@ __global__ void __launch_bounds__(256) score_logits_ref(const T* __restrict__ q,
         float m = -INFINITY;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
-            const int j = j0 + tk * 8 + b;
+            const int j = j0 + (b < 4 ? tk * 4 + b : 64 + tk * 4 + (b - 4));
             const float x = __fmul_rn(acc[a][b], inv_sqrt_d);
             if (r < lq && j < allowed) {
                 out[j] = x;
