@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
 attend_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ n_dev,
                    int n_const, int kv_group, int rows_per_head, int head_begin, float scale,
-                   float* __restrict__ o) {
+                   float* __restrict__ o, const int32_t* __restrict__ o_rows) {
     extern __shared__ uint8_t smem_raw[];
     Tf32Smem& sm = *reinterpret_cast<Tf32Smem*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -347,7 +347,9 @@ attend_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         mbar_wait(&sm.pv_done, (nkv - 1) & 1);
         tc_fence_after();
         const float inv_l = 1.0f / l;
-        float* dst = o + ((size_t)h * rows_per_head + row) * TD;
+        // o_rows: the decompress fused -- kept row `row` lands at its original position
+        const int orow = (o_rows && row < n) ? __ldg(o_rows + (size_t)h * rows_per_head + row) : row;
+        float* dst = o + ((size_t)h * rows_per_head + orow) * TD;
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
             uint32_t r[32];
@@ -425,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTf32Threads, 1)
 attend_tf32_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const int32_t* __restrict__ n_dev,
                         int n_const, int kv_group, int rows_per_head, int head_begin, float scale,
-                        float* __restrict__ o) {
+                        float* __restrict__ o, const int32_t* __restrict__ o_rows) {
     extern __shared__ uint8_t smem_raw[];
     Tf32PairSmem& sm = *reinterpret_cast<Tf32PairSmem*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -626,7 +628,9 @@ attend_tf32_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
         mbar_wait(&sm.pv_done, (nkv - 1) & 1);
         tc_fence_after();
         const float inv_l = 1.0f / l;
-        float* dst = o + ((size_t)h * rows_per_head + row) * TD;
+        // o_rows: the decompress fused -- kept row `row` lands at its original position
+        const int orow = (o_rows && row < n) ? __ldg(o_rows + (size_t)h * rows_per_head + row) : row;
+        float* dst = o + ((size_t)h * rows_per_head + orow) * TD;
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
             uint32_t r[32];
@@ -679,7 +683,8 @@ bool attend_tf32_supported(const tsa_desc& d) { return d.dtype == TSA_F32 && d.d
 
 int launch_attend_tf32(const tsa_desc& d, const void* q, const void* k, const void* v,
                        const int32_t* n_dev, int32_t n_const, int32_t kv_group,
-                       int32_t rows_per_head, int32_t kv_rows_per_head, void* o, cudaStream_t st) {
+                       int32_t rows_per_head, int32_t kv_rows_per_head, void* o, cudaStream_t st,
+                       const int32_t* o_rows) {
     if (!attend_tf32_supported(d)) return invalid("attend_tf32: needs f32, d_head 128");
     const int nh = d.head_end - d.head_begin;
     const int n_kv_buf = (d.n_heads + kv_group - 1) / kv_group;
@@ -699,7 +704,7 @@ int launch_attend_tf32(const tsa_desc& d, const void* q, const void* k, const vo
         dim3 grid(2 * nh, max_pairs);
         attend_tf32_pair_kernel<<<grid, kTf32Threads, smem, st>>>(
             mq, mk, mv, n_dev, n_const, kv_group, rows_per_head, d.head_begin, scale,
-            static_cast<float*>(o));
+            static_cast<float*>(o), o_rows);
         TSA_LAUNCH_CHECK("attend_tf32_pair");
         return 0;
     }
@@ -708,7 +713,7 @@ int launch_attend_tf32(const tsa_desc& d, const void* q, const void* k, const vo
     dim3 grid(nh, (rows_per_head + TBM - 1) / TBM);
     attend_tf32_kernel<<<grid, kTf32Threads, smem, st>>>(mq, mk, mv, n_dev, n_const, kv_group,
                                                         rows_per_head, d.head_begin, scale,
-                                                        static_cast<float*>(o));
+                                                        static_cast<float*>(o), o_rows);
     TSA_LAUNCH_CHECK("attend_tf32");
     return 0;
 }

@@ -161,6 +161,22 @@ int attend_dispatch(const tsa_desc& d, const void* q, const void* k, const void*
     return launch_attend_simt(d, q, k, v, n_dev, n_const, kv_group, rph, kvrph, o, st);
 }
 
+// f32 on the tensor cores: compress -> attend -> decompress with the decompress
+// fused -- the gather also zeroes the output rows the selection dropped
+// (scatter_rows' zero rows, tensor_ops.cpp:107) and the attention epilogue
+// writes each kept row at its original position (idx), so there is no oc
+// buffer and no scatter pass.  inv must be current (select / inverse).
+static int sparse_attend_tf32(const tsa_desc& d, const void* q, const void* k, const void* v,
+                              const int32_t* idx, const int32_t* k_keep, const int32_t* inv,
+                              void* out, const Workspace& w, void* ws, cudaStream_t st) {
+    int rc;
+    if ((rc = launch_gather_zero(d, q, k, v, idx, k_keep, at<void>(ws, w.qc), at<void>(ws, w.kc),
+                                 at<void>(ws, w.vc), inv, out, st)))
+        return rc;
+    return launch_attend_tf32(d, at<void>(ws, w.qc), at<void>(ws, w.kc), at<void>(ws, w.vc), k_keep,
+                              d.seq_len, 1, d.seq_len, d.seq_len, out, st, idx);
+}
+
 int budget_impl(const tsa_desc& d, const float* s, int32_t* k_keep, void* ws, int min_keep,
                 cudaStream_t st) {
     const Workspace w = workspace_layout(d);
@@ -414,6 +430,10 @@ int tsa_token_sparse_attention(const tsa_desc* d, const void* q, const void* k, 
         return launch_attend_indexed(*d, q, k, v, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
                                      k_keep, out, st);
     }
+    if (attend_tf32_supported(*d)) {
+        if ((rc = launch_inverse(*d, idx, k_keep, at<int32_t>(ws, w.inv), st))) return rc;
+        return sparse_attend_tf32(*d, q, k, v, idx, k_keep, at<int32_t>(ws, w.inv), out, w, ws, st);
+    }
     if ((rc = launch_gather(*d, q, k, v, idx, k_keep, at<void>(ws, w.qc), at<void>(ws, w.kc),
                             at<void>(ws, w.vc), st)))
         return rc;
@@ -456,6 +476,8 @@ static int layer_eager(const tsa_desc* d, const void* q, const void* k, const vo
             if ((rc = launch_attend_indexed(*d, q, k, v, at<void>(ws, w.kc), at<void>(ws, w.vc), idx,
                                             k_keep_out, out, st)))
                 return rc;
+        } else if (attend_tf32_supported(*d)) {
+            if ((rc = sparse_attend_tf32(*d, q, k, v, idx, k_keep_out, inv, out, w, ws, st))) return rc;
         } else {
         if ((rc = launch_gather(*d, q, k, v, idx, k_keep_out, at<void>(ws, w.qc), at<void>(ws, w.kc),
                                 at<void>(ws, w.vc), st)))

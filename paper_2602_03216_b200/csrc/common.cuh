@@ -208,7 +208,8 @@ bool attend_sm100_supported(const tsa_desc& d);
 bool attend_tf32_supported(const tsa_desc& d);
 int launch_attend_tf32(const tsa_desc& d, const void* q, const void* k, const void* v,
                        const int32_t* n_dev, int32_t n_const, int32_t kv_group,
-                       int32_t rows_per_head, int32_t kv_rows_per_head, void* o, cudaStream_t st);
+                       int32_t rows_per_head, int32_t kv_rows_per_head, void* o, cudaStream_t st,
+                       const int32_t* o_rows = nullptr);  // o_rows: scatter row r to o_rows[h, r]
 int launch_attend_sm100_rep(const tsa_desc& d, const void* q, const void* k, const void* v,
                             const OutReplicas& o, cudaStream_t st);
 // capi.cu (shared with sharded.cu)
