@@ -4,6 +4,7 @@ reference-order layer, host-tensor pipeline (back-to-back, overlapping), dense, 
 3xTF32 f32 attention, the exact budget total (chunk-monoid walk), the fused tcgen05
 projections (2-CTA GEMM) and the row statistic / weight layout kernels."""
 import math
+import os
 import sys
 
 import torch
@@ -25,8 +26,11 @@ for L in (1000, 1537):
         tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan, n_groups=2)
         tsa.sparse_attention_layer_host(hq, hk, hv, hout, plan)  # back to back, overlapping
     hf = tsa.HeadTensors(q.float(), k.float(), v.float())
-    tsa.sparse_attention_layer(hf, tsa.SparsePlan(mode=tsa.SparseMode.kDynamic, sparse_layers=[0],
-                                                  tau=0.3))
+    for pairs in ("0", "1"):  # the f32 attention, single-CTA and 2-CTA kernels
+        os.environ["TSA_TF32_PAIRS"] = pairs
+        tsa.sparse_attention_layer(hf, tsa.SparsePlan(mode=tsa.SparseMode.kDynamic,
+                                                      sparse_layers=[0], tau=0.3))
+    os.environ.pop("TSA_TF32_PAIRS")
     # exact total on adversarial values (ties, crossings) through aggregate_scores
     x = torch.linspace(-20, 5, 40000, device="cuda").exp()[None]
     tsa.aggregate_scores(tsa.HeadScores(x))
