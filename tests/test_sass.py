@@ -81,3 +81,19 @@ def test_tf32_attention_sass_is_tcgen05():
     assert p.count("UTCHMMA") >= 24 and "UTMALDG.3D" in p
     assert "LDTM" in p and "STTM" in p
     assert "LDL" not in p and "STL" not in p
+
+
+def test_tf32_pair_attention_sass_is_2cta():
+    """The opt-in 2-CTA f32 attention (TSA_TF32_PAIRS=1): paired MMAs
+    (UTCHMMA.2CTA) issued by the leader, TMA 3-D loads, no spills."""
+    if not LIB.exists() or not Path(CUOBJDUMP).exists():
+        pytest.skip("library not built or cuobjdump absent")
+    txt = subprocess.run([CUOBJDUMP, "-sass", str(LIB)], capture_output=True, text=True,
+                         check=True).stdout
+    parts = [p for p in re.split(r"\n\s*Function : ", txt)
+             if "attend_tf32_pair_kernel" in p.split("\n", 1)[0]]
+    assert len(parts) == 1
+    p = parts[0]
+    assert p.count("UTCHMMA.2CTA") >= 24 and "UTMALDG.3D" in p
+    assert "LDTM" in p and "STTM" in p
+    assert "LDL" not in p and "STL" not in p
