@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
+# build-time only (A/B experiments): extra nvcc flags, e.g. TSA_NVCC_EXTRA="-DTSA_XB_HELP=12"
+FLAGS += os.environ.get("TSA_NVCC_EXTRA", "").split()
 
 
 def _stale() -> bool:
