@@ -28,8 +28,8 @@
 //   score_exact_rowsum (XB): the sequential row sums, one CTA per ~n_rows/#SM
 //     rows (<= 16): X tiles arrive by TMA, 16 helper warps (thread = key x half
 //     the rows) compute e -- once: it is written back over X -- into a
-//     transposed shared tile, one warp (lane = row) runs the f32 chain in key
-//     order (L dependent FADDs per row: 0.32 ms at 128K).
+//     shared tile, one warp (lane = row, float4 loads) runs the f32 chain in
+//     key order (L dependent FADDs per row: 0.32 ms at 128K).
 //   score_exact_colsum (XC): thread = key, P = e / sum_r (Markstein division)
 //     accumulated over r in order -> raw column sums.
 //   pool: the shared edge-clamped pool kernel (score.cu).
@@ -298,14 +298,16 @@ constexpr int XB_STAGES = 4;                      // e tiles in flight
 constexpr int XB_XST = 8;                         // X tiles in flight (HBM latency x bandwidth)
 constexpr int XB_HELP = 16;                       // helper warps: thread = (key, half of the rows)
 constexpr int XB_THREADS = 32 * (XB_HELP + 1);    // + the summing warp
-constexpr int XB_EP = XB_MAXR + 1;                // e tile row pitch (conflict-free transpose)
+// e tile row pitch in floats: 4 mod 32 makes the helpers' row stores (lane = key)
+// and the summing warp's float4 loads (lane = row, 8 rows a wavefront) conflict-free
+constexpr int XB_EP = XB_KEYS + 4;
 // Rows per row-sum CTA (chain mode) at or below which the chains run apart
 // (row_chain_sum) and the exponentials split over key ranges.
 constexpr int kSplitRowsPerCta = 4;
 
 struct __align__(128) XbSmem {
     float x[XB_XST][XB_MAXR * XB_KEYS];           // X tile (TMA), rows x keys
-    float e[XB_STAGES][XB_KEYS * XB_EP];          // e tile, keys x rows
+    alignas(16) float e[XB_STAGES][XB_MAXR * XB_EP];  // e tile, rows x keys
     uint64_t tab[32];                             // glibc's exp2f table
     float m[XB_MAXR];
     int allowed[XB_MAXR];
@@ -375,7 +377,7 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
             mbar_wait(&sm.x_full[xt], (t / XB_XST) & 1);
             if (kChain && t >= XB_STAGES) mbar_wait(&sm.e_empty[st], ((t / XB_STAGES) - 1) & 1);
             const float* xs = sm.x[xt] + rbase * XB_KEYS + j;
-            float* es = sm.e[st] + j * XB_EP + rbase;
+            float* es = sm.e[st] + rbase * XB_EP + j;
             const int key = (tb + t) * XB_KEYS + j;
             float xv[RH];
 #pragma unroll
@@ -388,7 +390,7 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
                 // masked entries add +0 to the chain: exactly the reference's skip
                 const float e = expf_glibc(__fsub_rn(xv[i], mrow[i]), sm.tab);
                 const bool ok = key < arow[i];
-                if (kChain) es[i] = ok ? e : 0.0f;
+                if (kChain) es[i * XB_EP] = ok ? e : 0.0f;
                 if (ok) __stcs(xg + (size_t)i * Lp, e);
             }
             // every helper thread publishes its own e writes (release) to the chain warp
@@ -403,22 +405,27 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
         for (int t = 0; t < n_tiles; ++t) {
             const int st = t % XB_STAGES;
             mbar_wait(&sm.e_full[st], (t / XB_STAGES) & 1);
-            const float* es = sm.e[st] + row;
-            // the next 32 values load while the current 32 are added (the loads
-            // stay off the FADD chain)
-            float cur[32], nxt[32];
+            // the row's keys as float4 (one LDS.128 per 4 FADDs); the next 32
+            // values load while the current 32 are added (off the FADD chain)
+            const float4* es = reinterpret_cast<const float4*>(sm.e[st] + row * XB_EP);
+            float4 cur[8], nxt[8];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) cur[i] = es[i * XB_EP];
+            for (int i = 0; i < 8; ++i) cur[i] = es[i];
 #pragma unroll
             for (int c = 0; c < XB_KEYS / 32; ++c) {
                 if (c + 1 < XB_KEYS / 32) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) nxt[i] = es[((c + 1) * 32 + i) * XB_EP];
+                    for (int i = 0; i < 8; ++i) nxt[i] = es[(c + 1) * 8 + i];
                 }
 #pragma unroll
-                for (int i = 0; i < 32; ++i) s = __fadd_rn(s, cur[i]);
+                for (int i = 0; i < 8; ++i) {
+                    s = __fadd_rn(s, cur[i].x);
+                    s = __fadd_rn(s, cur[i].y);
+                    s = __fadd_rn(s, cur[i].z);
+                    s = __fadd_rn(s, cur[i].w);
+                }
 #pragma unroll
-                for (int i = 0; i < 32; ++i) cur[i] = nxt[i];
+                for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
             }
             mbar_arrive(&sm.e_empty[st]);  // each lane's reads of the stage are done
         }
