@@ -10,11 +10,14 @@ def load(path):
     return list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
 
 
-def main(path):
+def main(path, lib_only=False):
     rows = [r for r in load(path) if r["Metric Name"] == "gpu__time_duration.sum"]
+    if lib_only:  # this library's kernels (tsa::), not torch's input generation
+        rows = [r for r in rows if "tsa::" in r["Kernel Name"]]
     agg = {}
     for r in rows:
         name = r["Kernel Name"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+        name = name.replace("tsa::<unnamed>::", "")
         scale = {"ns": 1e-6, "us": 1e-3, "ms": 1.0}[r["Metric Unit"]]
         agg.setdefault(name, []).append(float(r["Metric Value"].replace(",", "")) * scale)
     tot = sum(sum(v) for v in agg.values())
@@ -25,4 +28,4 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], lib_only="--lib" in sys.argv[2:])

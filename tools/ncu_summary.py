@@ -1,5 +1,6 @@
 """Summarise an ncu report: per kernel duration, pipe utilisation, stalls,
-DRAM bytes.  python tools/ncu_summary.py report.ncu-rep [kernel-regex]"""
+DRAM bytes.  python tools/ncu_summary.py report.ncu-rep|raw.csv [kernel-regex]
+(a .csv argument is an already exported `ncu -i REP --page raw --csv`)"""
 import csv
 import io
 import re
@@ -8,8 +9,11 @@ import sys
 
 rep = sys.argv[1]
 pat = re.compile(sys.argv[2]) if len(sys.argv) > 2 else None
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                     text=True).stdout
+if rep.endswith(".csv"):
+    out = open(rep).read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[0]
 KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second",

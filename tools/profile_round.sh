@@ -13,8 +13,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -c 9 \
     -k regex:"attend|gather|select|budget|score|headsum|zero" \
     -o gpurun_out/$TAG/layer128k python tools/profile_layer.py > gpurun_out/$TAG/ncu_full.log 2>&1
 ncu -i gpurun_out/$TAG/layer128k.ncu-rep --page raw --csv > gpurun_out/$TAG/ncu_raw.csv 2>&1
-python tools/ncu_summary.py gpurun_out/$TAG/ncu_raw.csv gpurun_out/$TAG/ncu_full.json \
-    > gpurun_out/$TAG/ncu_full.txt 2>&1
+python tools/ncu_summary.py gpurun_out/$TAG/ncu_raw.csv > gpurun_out/$TAG/ncu_full.txt 2>&1
 ls -la gpurun_out/$TAG
 ncu -i gpurun_out/$TAG/layer128k.ncu-rep --page details > gpurun_out/$TAG/ncu_details.txt 2>&1
 du -sh gpurun_out/$TAG/layer128k.ncu-rep
@@ -24,6 +23,5 @@ timeout 900 ncu --set full --clock-control none -c 9 \
     -k regex:"attend|gather|select|budget|score|headsum|zero" \
     -o gpurun_out/$TAG/cfg5shard python tools/profile_layer.py 131072 8 1 > gpurun_out/$TAG/cfg5.log 2>&1
 ncu -i gpurun_out/$TAG/cfg5shard.ncu-rep --page raw --csv > gpurun_out/$TAG/ncu_cfg5_raw.csv 2>&1
-python tools/ncu_summary.py gpurun_out/$TAG/ncu_cfg5_raw.csv gpurun_out/$TAG/ncu_cfg5_shard.json \
-    > gpurun_out/$TAG/ncu_cfg5_shard.txt 2>&1
+python tools/ncu_summary.py gpurun_out/$TAG/ncu_cfg5_raw.csv > gpurun_out/$TAG/ncu_cfg5_shard.txt 2>&1
 [ -n "$KEEP_REP" ] || rm -f gpurun_out/$TAG/cfg5shard.ncu-rep
