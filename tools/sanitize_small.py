@@ -34,6 +34,10 @@ for L in (1000, 1537):
     # exact total on adversarial values (ties, crossings) through aggregate_scores
     x = torch.linspace(-20, 5, 40000, device="cuda").exp()[None]
     tsa.aggregate_scores(tsa.HeadScores(x))
+# the exact scorer's chain mode (>= 5 rows per row-sum CTA: the summing warp's float4
+# reads of the e tile), ragged L
+q, k, v = workloads.heavy_tailed_heads(32, 8, 1537, 128, seed=5)
+tsa.score_tokens(tsa.HeadTensors(q, k, v), 64, 7)
 # projections: QKV with norm / RoPE / split, W_o with residual, plain GEMM (ragged M)
 L, D, H, Hkv = 300, 512, 4, 2
 x = torch.randn((L, D), device="cuda").to(torch.bfloat16)
