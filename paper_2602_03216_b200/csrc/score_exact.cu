@@ -26,7 +26,7 @@
 //     on an ordered-int encoding).  34.4 G FMA at 128K / Llama-3-8B: the
 //     FP32 pipe is the roofline.
 //   score_exact_rowsum (XB): the sequential row sums, one CTA per ~n_rows/#SM
-//     rows (<= 16): X tiles arrive by TMA, 16 helper warps (thread = key x half
+//     rows (<= 16): X tiles arrive by TMA, 15 helper warps (thread = key x half
 //     the rows) compute e -- once: it is written back over X -- into a
 //     shared tile, one warp (lane = row, float4 loads) runs the f32 chain in
 //     key order (L dependent FADDs per row: 0.32 ms at 128K).
@@ -293,13 +293,28 @@ score_exact_logits(const __grid_constant__ CUtensorMap tm_k, const __nv_bfloat16
 // Rows per CTA are chosen at run time (<= 16, one chain lane each) so the
 // exponentials -- the bulk of this kernel's work -- spread over every SM.
 constexpr int XB_MAXR = 16;
-constexpr int XB_KEYS = 256;
+// 15 helper warps over 240-key tiles: warp 15 sums, on a sub-partition that holds
+// three helpers instead of four (less issue competition for its dependent FADDs);
+// 16 x 256, 12 x 192, 14 x 224, 11 x 176 and a sub-partition to itself all measured
+// slower (profiles/r2/ab_notes.txt).  Build-time knobs for such A/B runs:
+#ifndef TSA_XB_KEYS
+#define TSA_XB_KEYS 240
+#endif
+#ifndef TSA_XB_HELP
+#define TSA_XB_HELP 15
+#endif
+constexpr int XB_KEYS = TSA_XB_KEYS;
 constexpr int XB_STAGES = 4;                      // e tiles in flight
 constexpr int XB_XST = 8;                         // X tiles in flight (HBM latency x bandwidth)
-constexpr int XB_HELP = 16;                       // helper warps: thread = (key, half of the rows)
+constexpr int XB_HELP = TSA_XB_HELP;              // helper warps: thread = (key, part of the rows)
+constexpr int XB_PARTS = XB_HELP * 32 / XB_KEYS;  // row parts per key column
+constexpr int XB_CH = XB_KEYS % 32 == 0 ? 32 : 16;  // chain chunk (keys)
+static_assert(XB_PARTS * XB_KEYS == XB_HELP * 32 && XB_MAXR % XB_PARTS == 0 && XB_KEYS % 16 == 0,
+              "row-sum helper geometry");
 constexpr int XB_THREADS = 32 * (XB_HELP + 1);    // + the summing warp
-// e tile row pitch in floats: 4 mod 32 makes the helpers' row stores (lane = key)
-// and the summing warp's float4 loads (lane = row, 8 rows a wavefront) conflict-free
+// e tile row pitch in floats: 4 (256 keys) or 20 (240) mod 32 makes the helpers' row
+// stores (lane = key) and the summing warp's float4 loads (lane = row, 8 rows a
+// wavefront) conflict-free
 constexpr int XB_EP = XB_KEYS + 4;
 // Rows per row-sum CTA (chain mode) at or below which the chains run apart
 // (row_chain_sum) and the exponentials split over key ranges.
@@ -362,8 +377,8 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
         // thread = key column j of the tile: XB_MAXR independent exponentials per
         // tile, unconditionally (rows >= R are padding the chain never reads), so
         // they interleave
-        constexpr int RH = XB_MAXR / 2;
-        const int j = tid & (XB_KEYS - 1), rbase = (tid / XB_KEYS) * RH;
+        constexpr int RH = XB_MAXR / XB_PARTS;
+        const int j = tid % XB_KEYS, rbase = (tid / XB_KEYS) * RH;
         float mrow[RH];
         int arow[RH];
 #pragma unroll
@@ -408,24 +423,25 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
             // the row's keys as float4 (one LDS.128 per 4 FADDs); the next 32
             // values load while the current 32 are added (off the FADD chain)
             const float4* es = reinterpret_cast<const float4*>(sm.e[st] + row * XB_EP);
-            float4 cur[8], nxt[8];
+            constexpr int V = XB_CH / 4;
+            float4 cur[V], nxt[V];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) cur[i] = es[i];
+            for (int i = 0; i < V; ++i) cur[i] = es[i];
 #pragma unroll
-            for (int c = 0; c < XB_KEYS / 32; ++c) {
-                if (c + 1 < XB_KEYS / 32) {
+            for (int c = 0; c < XB_KEYS / XB_CH; ++c) {
+                if (c + 1 < XB_KEYS / XB_CH) {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) nxt[i] = es[(c + 1) * 8 + i];
+                    for (int i = 0; i < V; ++i) nxt[i] = es[(c + 1) * V + i];
                 }
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int i = 0; i < V; ++i) {
                     s = __fadd_rn(s, cur[i].x);
                     s = __fadd_rn(s, cur[i].y);
                     s = __fadd_rn(s, cur[i].z);
                     s = __fadd_rn(s, cur[i].w);
                 }
 #pragma unroll
-                for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
+                for (int i = 0; i < V; ++i) cur[i] = nxt[i];
             }
             mbar_arrive(&sm.e_empty[st]);  // each lane's reads of the stage are done
         }
