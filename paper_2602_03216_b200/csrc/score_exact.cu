@@ -386,6 +386,7 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
             mrow[i] = sm.m[rbase + i];
             arow[i] = sm.allowed[rbase + i];
         }
+        const bool full_rows = R == XB_MAXR && row0 + XB_MAXR <= n_rows;
         for (int t = 0; t < n_tiles; ++t) {
             if (tid == 0 && t + XB_XST - 1 < n_tiles) issue(t + XB_XST - 1);
             const int xt = t % XB_XST, st = t % XB_STAGES;
@@ -399,7 +400,16 @@ score_exact_rowsum(const __grid_constant__ CUtensorMap tm_x, float* __restrict__
             for (int i = 0; i < RH; ++i) xv[i] = xs[i * XB_KEYS];
             // e overwrites X in HBM (the column pass reads it: the exponentials run once)
             float* xg = X + (size_t)(row0 + rbase) * Lp + key;
-            if (rbase < R)  // (warp-uniform) a half with no live rows skips its exponentials
+            // (CTA-uniform) every row live and no key of the tile past any row's causal
+            // limit: no per-element mask
+            if (full_rows && (tb + t + 1) * XB_KEYS <= L - lq + 1) {
+#pragma unroll
+                for (int i = 0; i < RH; ++i) {
+                    const float e = expf_glibc(__fsub_rn(xv[i], mrow[i]), sm.tab);
+                    if (kChain) es[i * XB_EP] = e;
+                    __stcs(xg + (size_t)i * Lp, e);
+                }
+            } else if (rbase < R)  // (warp-uniform) a half with no live rows skips its exponentials
 #pragma unroll
             for (int i = 0; i < RH; ++i) {
                 // masked entries add +0 to the chain: exactly the reference's skip
@@ -631,7 +641,10 @@ int launch_score_exact_rows(const tsa_desc& d, float* X, int* rowmax, float* row
     const int n_rows = nh * lq;
     const int nsm = num_sms();
     // rows per row-sum CTA: spread the rows over every SM (<= 16: one chain lane each)
-    const int rpc = std::min(XB_MAXR, std::max(1, (n_rows + nsm - 1) / nsm));
+    // full 16-row CTAs once the rows reach 8 per SM (the chain length, not the CTA
+    // count, sets the time; full CTAs take the unmasked tile path)
+    const int rpc0 = std::max(1, (n_rows + nsm - 1) / nsm);
+    const int rpc = rpc0 >= 8 ? XB_MAXR : std::min(XB_MAXR, rpc0);
     CUtensorMap mx;
     int rc;
     if ((rc = make_f32_map_2d(&mx, X, (uint64_t)Lp, (uint64_t)n_rows, (uint64_t)Lp * 4, XB_KEYS,
