@@ -26,10 +26,11 @@
 //     on an ordered-int encoding).  34.4 G FMA at 128K / Llama-3-8B: the
 //     FP32 pipe is the roofline.
 //   score_exact_rowsum (XB): the sequential row sums, one CTA per ~n_rows/#SM
-//     rows (<= 16): X tiles arrive by TMA, 15 helper warps (thread = key x half
-//     the rows) compute e -- once: it is written back over X -- into a
-//     shared tile, one warp (lane = row, float4 loads) runs the f32 chain in
-//     key order (L dependent FADDs per row: 0.32 ms at 128K).
+//     rows (16 once that reaches 8): X tiles arrive by TMA, 15 helper warps
+//     (thread = key x half the rows) compute e -- once: it is written back over
+//     X -- into a shared tile, one warp (lane = row, float4 loads) runs the f32
+//     chain in key order (L dependent FADDs per row: 0.32 ms floor at 128K,
+//     0.51 ms measured).
 //   score_exact_colsum (XC): thread = key, P = e / sum_r (Markstein division)
 //     accumulated over r in order -> raw column sums.
 //   pool: the shared edge-clamped pool kernel (score.cu).
