@@ -192,7 +192,9 @@ __global__ void __launch_bounds__(256) gather_tma_kernel(
         tma_store_3d(&tm_kc, sm.k, 0, r0, h);
         tma_store_3d(&tm_vc, sm.v, 0, r0, h);
         bulk_commit();
-        bulk_wait0();
+        // only the shared-memory reads need to finish before the CTA ends (the writes
+        // complete with the grid); waiting for them would hold the CTA's slot
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
 }
 
